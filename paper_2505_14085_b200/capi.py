@@ -1,0 +1,115 @@
+"""ctypes binding of the C ABI (include/ekv_capi.h) in libekv.so.
+
+This is plumbing for the Python host layer, tests and bench: every call goes
+straight to the sm_100a library.  There is no fallback -- if libekv.so is
+missing or the device is not a B200, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIBEKV = os.path.join(PKG, "lib", "libekv.so")
+
+EKV_OK = 0
+EKV_KV_BF16, EKV_KV_INT8, EKV_KV_INT4 = 16, 8, 4
+_STATUS = {-1: "EINVAL", -2: "ECUDA", -3: "ENOMEM", -4: "ENODEV", -5: "EUNSUPPORTED"}
+
+
+class EkvError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{_STATUS.get(status, status)}] {msg}")
+        self.status = status
+        self.msg = msg
+
+
+class ekv_segment(C.Structure):
+    _fields_ = [("format", C.c_int), ("S", C.c_int), ("group", C.c_int), ("k", C.c_void_p),
+                ("v", C.c_void_p), ("k_scales", C.c_void_p), ("v_scales", C.c_void_p)]
+
+
+class ekv_model_config(C.Structure):
+    _fields_ = [("num_layers", C.c_int), ("num_heads", C.c_int), ("head_dim", C.c_int),
+                ("max_positions", C.c_int)]
+
+
+_vp, _i, _i64, _u64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_double
+_dp, _ip, _fp = C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_float)
+_pp = C.POINTER(C.c_void_p)
+
+# name -> argtypes (all return int status unless listed in _RET)
+PROTOS = {
+    "ekv_abi_version": [],
+    "ekv_last_error": [],
+    "ekv_ctx_create": [_i, _vp, _pp],
+    "ekv_ctx_destroy": [_vp],
+    "ekv_ctx_stream": [_vp, _pp],
+    "ekv_ctx_synchronize": [_vp],
+    "ekv_ctx_kernel_launches": [_vp, C.POINTER(C.c_int64)],
+    "ekv_fill_uniform_bf16": [_vp, _vp, _i64, _u64, _u64, _d, _d],
+    "ekv_prune_retained": [_d, _i, _ip],
+    "ekv_align_qnorm": [_vp, _vp, _vp, _i, _i, _i, _i, _vp],
+    "ekv_kv_colnorm": [_vp, _vp, _i64, _i, _vp],
+    "ekv_rank_channels": [_dp, _dp, _i, _i, _ip, _dp],
+    "ekv_match_layers": [_dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
+    "ekv_kv_gather": [_vp, _vp, _i64, _i, _vp, _i, _vp],
+    "ekv_kv_compress": [_vp, _vp, _i64, _i, _vp, _i, _i, _i, _vp, _vp],
+    "ekv_kv_dequant": [_vp, _vp, _vp, _i64, _i, _i, _i, _vp],
+    "ekv_decode_attention": [_vp, _i, _i, _i, _vp, C.POINTER(ekv_segment), _vp, _vp, _i, _i, _vp,
+                             _vp],
+    "ekv_model_create": [_vp, C.POINTER(ekv_model_config), _pp],
+    "ekv_model_destroy": [_vp],
+    "ekv_model_set_layer": [_vp, _i, _vp, _vp],
+    "ekv_model_set_io": [_vp, _vp, _vp, _vp],
+    "ekv_model_synthesize": [_vp, _u64, _d, _d],
+    "ekv_model_weights": [_vp, _i, _pp, _pp],
+    "ekv_model_io": [_vp, _pp, _pp, _pp],
+    "ekv_kvctx_create": [_vp, _i, _ip, _i, _pp],
+    "ekv_kvctx_destroy": [_vp],
+    "ekv_kvctx_layer": [_vp, _i, C.POINTER(ekv_segment)],
+    "ekv_kvctx_upload_bf16": [_vp, _i, _vp, _vp],
+    "ekv_kvctx_set_layer": [_vp, _i, _vp, _vp, _vp, _vp],
+    "ekv_kvctx_synthesize": [_vp, _u64],
+    "ekv_session_create": [_vp, _vp, _i, _pp],
+    "ekv_session_destroy": [_vp],
+    "ekv_session_reset": [_vp],
+    "ekv_session_length": [_vp, _ip],
+    "ekv_session_forward": [_vp, _vp, _i, _vp],
+    "ekv_session_decode": [_vp, _i, _vp],
+    "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
+    "ekv_collaborative_decode": [_vp, _vp, _i, _i, _vp, _vp],
+    "ekv_cache_source": [_i, _d, _d, _i, _i, _ip],
+    "ekv_pipeline_schedule": [_dp, _dp, _i, _dp, _dp, _dp],
+}
+_RET = {"ekv_last_error": C.c_char_p}
+
+_lib = None
+
+
+def load(path: str = LIBEKV):
+    """Load libekv.so (raises if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is not built: run `python -m paper_2505_14085_b200.build` "
+                               "(the B200 path has no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, args in PROTOS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = _RET.get(name, C.c_int)
+        _lib = lib
+    return _lib
+
+
+def call(name: str, *args):
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != EKV_OK:
+        raise EkvError(rc, lib.ekv_last_error().decode())
+    return rc
+
+
+def last_error() -> str:
+    return load().ekv_last_error().decode()

@@ -1,0 +1,1103 @@
+// The C-ABI (include/ekv_capi.h): argument validation with the reference's
+// error texts, object lifetimes, and the collaborative-decode engine that
+// strings K4/K5 together per layer and replays one captured CUDA graph per
+// decode step.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "ekv_common.cuh"
+#include "ekv_kernels.h"
+
+namespace ekv {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launches(int64_t n) { g_launches += n; }
+
+void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
+                                int n_cols, double* colsq, int num_sms, cudaStream_t st);
+
+}  // namespace ekv
+
+using namespace ekv;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return EKV_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return EKV_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return EKV_EINVAL;
+    }
+}
+
+template <class T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error(EKV_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+    }
+    return (T*)p;
+}
+
+}  // namespace
+
+struct ekv_ctx_s {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaStream_t capture = nullptr;  // graphs are captured here, launched on `stream`
+    bool own_stream = false;
+};
+
+struct ekv_model_s {
+    ekv_ctx_s* ctx = nullptr;
+    ekv_model_config cfg{};
+    int h = 0;
+    uint16_t* weights = nullptr;  // per layer: [3h][h] wqkvT then [h][h] woT
+    float* gamma = nullptr;
+    float* bias = nullptr;
+    uint16_t* pos = nullptr;
+    size_t layer_elems() const { return (size_t)4 * h * h; }
+    uint16_t* wqkvT(int l) const { return weights + (size_t)l * layer_elems(); }
+    uint16_t* woT(int l) const { return wqkvT(l) + (size_t)3 * h * h; }
+};
+
+struct ekv_kvctx_s {
+    ekv_model_s* model = nullptr;
+    int S = 0, group = 0;
+    std::vector<int> fmt;
+    std::vector<ekv_segment> seg;
+    std::vector<void*> allocs;
+};
+
+struct ekv_session_s {
+    ekv_model_s* model = nullptr;
+    ekv_kvctx_s* kv = nullptr;
+    int cap = 0;                   // user/generated rows
+    uint16_t* uk = nullptr;        // [L][H][cap][d]
+    uint16_t* uv = nullptr;
+    float* xa = nullptr;           // [8][h]
+    float* xb = nullptr;           // [8][h]
+    float* q = nullptr;            // [8][h]
+    float* emb = nullptr;          // [cap][h] staged user embeddings
+    float* pre_out = nullptr;      // [cap][h] prefill outputs by user row
+    float* hist = nullptr;         // [cap][h] decode-step outputs by step
+    DevState* state = nullptr;
+    float* ws = nullptr;
+    unsigned* counters = nullptr;
+    int user_len = 0;              // host mirror of state->user_len
+    int steps = 0;                 // host mirror of state->step
+    cudaGraphExec_t step_graph = nullptr;
+    int64_t graph_kernels = 0;
+    size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
+};
+
+namespace {
+
+void check_device(int device, int* sms) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        (void)cudaGetLastError();
+        throw Error(EKV_ENODEV, "no CUDA device (the B200 path has no CPU fallback)");
+    }
+    require(device >= 0 && device < n, "device " + std::to_string(device) + " out of range",
+            EKV_ENODEV);
+    cudaDeviceProp p;
+    EKV_CUDA(cudaGetDeviceProperties(&p, device));
+    require(p.major == 10, std::string("device ") + p.name + " is not sm_100 (B200)", EKV_ENODEV);
+    *sms = p.multiProcessorCount;
+}
+
+void set_dev(ekv_ctx_s* c) { EKV_CUDA(cudaSetDevice(c->device)); }
+
+int d_of(const ekv_model_s* m) { return m->cfg.head_dim; }
+
+// One forward chunk of R <= 8 rows through every layer (merged_forward,
+// cache_merge.cpp:156-226).  `in` holds the R input rows (fp32 [R][h]);
+// `out_hist`/`hist_row_dev` receive the final-layer rows.
+void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
+                   const int* hist_row_dev, cudaStream_t st) {
+    ekv_model_s* m = s->model;
+    const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
+    for (int l = 0; l < L; ++l) {
+        GemvArgs g{};
+        g.N = 3 * h;
+        g.K = h;
+        g.R = R;
+        g.W = m->wqkvT(l);
+        g.x = (l == 0) ? in : s->xa;
+        if (l == 0) {
+            g.gamma = m->gamma;
+            g.bias = m->bias;
+            g.pos = m->pos;
+            g.pos_offset = s->kv->S;
+            g.pos_base_dev = &s->state->user_len;
+        }
+        g.mode = 1;
+        g.qkv_d = d;
+        g.qkv_H = H;
+        g.q_out = s->q;
+        g.uk = s->uk + (size_t)l * s->ukv_layer();
+        g.uv = s->uv + (size_t)l * s->ukv_layer();
+        g.ucap = s->cap;
+        g.user_base_dev = &s->state->user_len;
+        launch_gemv(g, st);
+
+        AttnArgs a{};
+        a.R = R;
+        a.H = H;
+        a.D = d;
+        a.q = s->q;
+        const ekv_segment& sg = s->kv->seg[l];
+        a.fmt = sg.format;
+        a.S = sg.S;
+        a.group = sg.group;
+        a.ck = sg.k;
+        a.cv = sg.v;
+        a.cks = sg.k_scales;
+        a.cvs = sg.v_scales;
+        a.uk = g.uk;
+        a.uv = g.uv;
+        a.ucap = s->cap;
+        a.user_base_dev = &s->state->user_len;
+        a.out = s->xb;
+        a.lse = nullptr;
+        a.ws = s->ws;
+        a.counters = s->counters;
+        launch_decode_attention(a, st);
+
+        GemvArgs o{};
+        o.N = h;
+        o.K = h;
+        o.R = R;
+        o.W = m->woT(l);
+        o.x = s->xb;
+        o.mode = 0;
+        o.y = s->xa;
+        if (l == L - 1 && out_hist) {
+            o.y_hist = out_hist;
+            o.hist_row_dev = hist_row_dev;
+        }
+        launch_gemv(o, st);
+    }
+    launch_advance(s->state, R, st);
+}
+
+size_t attn_ws_floats(int R, int H, int S, int d) {
+    int rpi = 0;
+    const int items = attn_items(R, H, S, &rpi) + 1;
+    return (size_t)R * H * items * (d + 2);
+}
+
+void session_alloc(ekv_session_s* s) {
+    ekv_model_s* m = s->model;
+    const int L = m->cfg.num_layers, h = m->h;
+    s->uk = dalloc<uint16_t>((size_t)L * s->ukv_layer());
+    s->uv = dalloc<uint16_t>((size_t)L * s->ukv_layer());
+    s->xa = dalloc<float>((size_t)8 * h);
+    s->xb = dalloc<float>((size_t)8 * h);
+    s->q = dalloc<float>((size_t)8 * h);
+    s->emb = dalloc<float>((size_t)s->cap * h);
+    s->pre_out = dalloc<float>((size_t)s->cap * h);
+    s->hist = dalloc<float>((size_t)s->cap * h);
+    s->state = dalloc<DevState>(1);
+    size_t ws = 0;
+    for (int R = 1; R <= 8; ++R)
+        ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim));
+    s->ws = dalloc<float>(ws);
+    s->counters = dalloc<unsigned>((size_t)8 * m->cfg.num_heads);
+    EKV_CUDA(cudaMemset(s->counters, 0, sizeof(unsigned) * 8 * m->cfg.num_heads));
+    EKV_CUDA(cudaMemset(s->state, 0, sizeof(DevState)));
+    EKV_CUDA(cudaMemset(s->uk, 0, sizeof(uint16_t) * L * s->ukv_layer()));
+    EKV_CUDA(cudaMemset(s->uv, 0, sizeof(uint16_t) * L * s->ukv_layer()));
+}
+
+void session_reset(ekv_session_s* s, cudaStream_t st) {
+    EKV_CUDA(cudaMemsetAsync(s->state, 0, sizeof(DevState), st));
+    s->user_len = 0;
+    s->steps = 0;
+}
+
+void check_overflow(ekv_session_s* s, int n) {
+    const int total = s->kv->S + s->user_len + n;
+    require(total <= s->model->cfg.max_positions,
+            "position overflow: " + std::to_string(total) + " > max_positions " +
+                std::to_string(s->model->cfg.max_positions));
+    require(s->user_len + n <= s->cap,
+            "session full: " + std::to_string(s->user_len + n) + " user rows > capacity " +
+                std::to_string(s->cap));
+}
+
+// rows [0, n) of emb_dev through merged_forward in chunks of <= 8 rows;
+// final-layer rows land in s->pre_out[user_row].
+void session_forward(ekv_session_s* s, const float* emb_dev, int n, cudaStream_t st) {
+    check_overflow(s, n);
+    for (int r0 = 0; r0 < n; r0 += 8) {
+        const int R = std::min(8, n - r0);
+        forward_chunk(s, emb_dev + (size_t)r0 * s->model->h, R, s->pre_out,
+                      &s->state->user_len, st);
+        s->user_len += R;
+    }
+    // decode feeds back the last row: place it in xa[0]; steps count from 0
+    const int last = (n - 1) % 8;
+    if (last > 0)
+        EKV_CUDA(cudaMemcpyAsync(s->xa, s->xa + (size_t)last * s->model->h,
+                                 sizeof(float) * s->model->h, cudaMemcpyDeviceToDevice, st));
+    EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
+    s->steps = 0;
+}
+
+void ensure_step_graph(ekv_session_s* s) {
+    if (s->step_graph) return;
+    ekv_ctx_s* c = s->model->ctx;
+    const int64_t before = g_launches.load();
+    EKV_CUDA(cudaStreamBeginCapture(c->capture, cudaStreamCaptureModeThreadLocal));
+    try {
+        forward_chunk(s, s->xa, 1, s->hist, &s->state->step, c->capture);
+    } catch (...) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(c->capture, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    cudaGraph_t g = nullptr;
+    EKV_CUDA(cudaStreamEndCapture(c->capture, &g));
+    EKV_CUDA(cudaGraphInstantiate(&s->step_graph, g, 0));
+    EKV_CUDA(cudaGraphDestroy(g));
+    s->graph_kernels = g_launches.load() - before;
+    g_launches -= s->graph_kernels;  // capture launched nothing; replays are counted
+}
+
+void session_decode(ekv_session_s* s, int steps, cudaStream_t st) {
+    require(steps >= 1, "collaborative_decode: steps must be >= 1");
+    check_overflow(s, steps);
+    require(s->steps + steps <= s->cap, "decode history full");
+    ensure_step_graph(s);
+    for (int t = 0; t < steps; ++t) EKV_CUDA(cudaGraphLaunch(s->step_graph, st));
+    count_launches(s->graph_kernels * steps);
+    s->user_len += steps;
+    s->steps += steps;
+}
+
+void ctx_storage(ekv_kvctx_s* c) {
+    ekv_model_s* m = c->model;
+    const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m);
+    c->seg.assign(L, ekv_segment{});
+    for (int l = 0; l < L; ++l) {
+        ekv_segment& s = c->seg[l];
+        s.format = c->fmt[l];
+        s.S = c->S;
+        s.group = c->fmt[l] == EKV_KV_BF16 ? d : c->group;
+        if (c->S == 0) continue;
+        const size_t rows = (size_t)H * c->S;
+        if (s.format == EKV_KV_BF16) {
+            void* k = dalloc<uint16_t>(rows * d);
+            void* v = dalloc<uint16_t>(rows * d);
+            c->allocs.push_back(k);
+            c->allocs.push_back(v);
+            s.k = k;
+            s.v = v;
+        } else {
+            const size_t bytes = rows * d * s.format / 8;
+            void* k = dalloc<uint8_t>(bytes);
+            void* v = dalloc<uint8_t>(bytes);
+            float* ks = dalloc<float>(rows * (d / s.group));
+            float* vs = dalloc<float>(rows * (d / s.group));
+            for (void* p : {k, v, (void*)ks, (void*)vs}) c->allocs.push_back(p);
+            s.k = k;
+            s.v = v;
+            s.k_scales = ks;
+            s.v_scales = vs;
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int ekv_abi_version(void) { return EKV_ABI_VERSION; }
+const char* ekv_last_error(void) { return g_err.c_str(); }
+
+int ekv_ctx_create(int device, void* stream, ekv_ctx_t* out) {
+    return guard([&] {
+        require(out != nullptr, "ekv_ctx_create: null output");
+        int sms = 0;
+        check_device(device, &sms);
+        auto* c = new ekv_ctx_s();
+        c->device = device;
+        c->num_sms = sms;
+        EKV_CUDA(cudaSetDevice(device));
+        if (stream) {
+            c->stream = (cudaStream_t)stream;
+        } else {
+            EKV_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        EKV_CUDA(cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking));
+        *out = c;
+    });
+}
+
+int ekv_ctx_destroy(ekv_ctx_t c) {
+    return guard([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        cudaStreamDestroy(c->capture);
+        delete c;
+    });
+}
+
+int ekv_ctx_stream(ekv_ctx_t c, void** stream) {
+    return guard([&] {
+        require(c && stream, "ekv_ctx_stream: null argument");
+        *stream = (void*)c->stream;
+    });
+}
+
+int ekv_ctx_synchronize(ekv_ctx_t c) {
+    return guard([&] {
+        require(c != nullptr, "null context");
+        set_dev(c);
+        EKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ekv_ctx_kernel_launches(ekv_ctx_t c, int64_t* count) {
+    return guard([&] {
+        require(c && count, "null argument");
+        *count = g_launches.load();
+    });
+}
+
+int ekv_fill_uniform_bf16(ekv_ctx_t c, void* dst, int64_t n, uint64_t seed, uint64_t stream_id,
+                          double lo, double hi) {
+    return guard([&] {
+        require(c && (dst || n == 0), "ekv_fill_uniform_bf16: null argument");
+        set_dev(c);
+        launch_fill_uniform_bf16(dst, n, seed, stream_id, lo, hi, c->stream);
+    });
+}
+
+// ---------------------------------------------------------------- stage 1
+int ekv_prune_retained(double lambda, int head_dim, int* retained) {
+    return guard([&] {
+        require(retained != nullptr, "null argument");
+        require(lambda >= 0.0 && lambda <= 1.0, "PruneSpec: lambda outside [0,1]");
+        require(head_dim >= 1, "PruneSpec: head_dim must be >= 1");
+        *retained = (int)std::floor((1.0 - lambda) * head_dim + 1e-9);
+    });
+}
+
+int ekv_align_qnorm(ekv_ctx_t c, const void* X, const void* WqT, int m, int S, int h_c,
+                    int n_cols, double* colsq) {
+    return guard([&] {
+        require(c && X && WqT && colsq, "ekv_align_qnorm: null argument");
+        require(m >= 1 && S >= 1 && h_c >= 1 && n_cols >= 1, "ekv_align_qnorm: empty shape");
+        set_dev(c);
+        launch_align_qnorm_batched(X, WqT, m, S, h_c, n_cols, colsq, c->num_sms, c->stream);
+    });
+}
+
+int ekv_kv_colnorm(ekv_ctx_t c, const void* K, int64_t rows, int d_c, double* colsq) {
+    return guard([&] {
+        require(c && K && colsq, "ekv_kv_colnorm: null argument");
+        require(rows >= 0 && d_c >= 1, "ekv_kv_colnorm: bad shape");
+        set_dev(c);
+        launch_kv_colnorm(K, rows, d_c, colsq, c->stream);
+    });
+}
+
+int ekv_rank_channels(const double* q_colsq, const double* k_colsq, int d_c, int retained,
+                      int* kept, double* cut_margin) {
+    return guard([&] {
+        require(q_colsq && k_colsq && (kept || retained == 0), "ekv_rank_channels: null argument");
+        require(d_c >= 1 && retained >= 0 && retained <= d_c,
+                "PruneSpec: retained " + std::to_string(retained) + " outside [0," +
+                    std::to_string(d_c) + "]");
+        std::vector<double> score(d_c);
+        for (int i = 0; i < d_c; ++i) score[i] = std::sqrt(q_colsq[i]) * std::sqrt(k_colsq[i]);
+        std::vector<int> order(d_c);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int a, int b) { return score[a] > score[b]; });
+        std::vector<int> k(order.begin(), order.begin() + retained);
+        std::sort(k.begin(), k.end());
+        std::copy(k.begin(), k.end(), kept);
+        if (cut_margin) {
+            double mg = INFINITY;
+            if (retained > 0 && retained < d_c) {
+                const double a = score[order[retained - 1]], b = score[order[retained]];
+                mg = a > 0 ? (a - b) / a : 0.0;
+            }
+            *cut_margin = mg;
+        }
+    });
+}
+
+// --- host layer map (match_layers, layer_match.cpp:166-228) ---------------
+namespace {
+void gram(const double* o, int n, int c, std::vector<double>& s) {
+    s.assign((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)j * c + k];
+            s[(size_t)i * n + j] = acc;
+        }
+}
+double hsic_of(const std::vector<double>& se, const std::vector<double>& sc, int n) {
+    std::vector<double> rm(n, 0.0), cm(n, 0.0);
+    double tot = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            rm[i] += se[(size_t)i * n + j];
+            cm[j] += se[(size_t)i * n + j];
+            tot += se[(size_t)i * n + j];
+        }
+    for (int i = 0; i < n; ++i) {
+        rm[i] /= n;
+        cm[i] /= n;
+    }
+    tot /= (double)n * n;
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j)
+            tr += (se[(size_t)i * n + j] - rm[i] - cm[j] + tot) * sc[(size_t)j * n + i];
+    return tr / ((double)(n - 1) * (n - 1));
+}
+std::vector<double> cos_lower(const double* o, int n, int c) {
+    std::vector<double> norms(n), flat;
+    for (int i = 0; i < n; ++i) {
+        double acc = 0.0;
+        for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)i * c + k];
+        norms[i] = std::sqrt(acc);
+        require(norms[i] != 0.0, "rsa: zero-norm row " + std::to_string(i));
+    }
+    for (int i = 1; i < n; ++i)
+        for (int j = 0; j < i; ++j) {
+            double acc = 0.0;
+            for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)j * c + k];
+            flat.push_back(acc / (norms[i] * norms[j]));
+        }
+    return flat;
+}
+double pearson(const std::vector<double>& x, const std::vector<double>& y) {
+    const size_t n = x.size();
+    double mx = 0, my = 0;
+    for (size_t i = 0; i < n; ++i) {
+        mx += x[i];
+        my += y[i];
+    }
+    mx /= n;
+    my /= n;
+    double sxy = 0, sxx = 0, syy = 0;
+    for (size_t i = 0; i < n; ++i) {
+        sxy += (x[i] - mx) * (y[i] - my);
+        sxx += (x[i] - mx) * (x[i] - mx);
+        syy += (y[i] - my) * (y[i] - my);
+    }
+    require(sxx != 0.0 && syy != 0.0, "pearson_corr: zero variance");
+    return std::clamp(sxy / std::sqrt(sxx * syy), -1.0, 1.0);
+}
+std::vector<double> normalized(const double* o, int n, int c) {
+    std::vector<double> out(o, o + (size_t)n * c);
+    double f = 0.0;
+    for (double v : out) f += v * v;
+    f = std::sqrt(f);
+    if (f == 0.0) return out;
+    const double t = std::sqrt((double)n);
+    for (double& v : out) v *= t / f;
+    return out;
+}
+}  // namespace
+
+int ekv_match_layers(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc,
+                     int cc, int n, double theta_cka, double theta_rsa, double* cka_out,
+                     double* rsa_out, int* best) {
+    return guard([&] {
+        require(edge_outs && cloud_outs && cka_out && rsa_out && best, "null argument");
+        require(me >= 1 && nc >= 1, "match_layers: empty layer output list");
+        require(theta_cka >= 0.0, "SimilarityConfig: theta_cka must be >= 0");
+        require(theta_rsa >= -1.0, "SimilarityConfig: theta_rsa must be >= -1");
+        require(n >= 3, "rsa: need N >= 3 samples");
+        std::vector<std::vector<double>> eg(me), cg(nc), ef(me), cf(nc);
+        std::vector<double> self_e(me), self_c(nc);
+        for (int l = 0; l < me; ++l) {
+            auto o = normalized(edge_outs + (size_t)l * n * ce, n, ce);
+            gram(o.data(), n, ce, eg[l]);
+            self_e[l] = hsic_of(eg[l], eg[l], n);
+            ef[l] = cos_lower(o.data(), n, ce);
+        }
+        for (int l = 0; l < nc; ++l) {
+            auto o = normalized(cloud_outs + (size_t)l * n * cc, n, cc);
+            gram(o.data(), n, cc, cg[l]);
+            self_c[l] = hsic_of(cg[l], cg[l], n);
+            cf[l] = cos_lower(o.data(), n, cc);
+        }
+        for (int le = 0; le < me; ++le) {
+            int bl = -1;
+            double bc = 0.0;
+            for (int lc = 0; lc < nc; ++lc) {
+                require(self_e[le] >= 1e-15 && self_c[lc] >= 1e-15,
+                        "cka: degenerate representation");
+                const double ck = hsic_of(eg[le], cg[lc], n) / std::sqrt(self_e[le] * self_c[lc]);
+                const double r = pearson(ef[le], cf[lc]);
+                cka_out[(size_t)le * nc + lc] = ck;
+                rsa_out[(size_t)le * nc + lc] = r;
+                if (ck >= theta_cka && r >= theta_rsa && (bl < 0 || ck > bc)) {
+                    bl = lc;
+                    bc = ck;
+                }
+            }
+            best[le] = bl;
+        }
+    });
+}
+
+// ---------------------------------------------------------------- stage 2
+static void check_rows_args(ekv_ctx_t c, const void* a, const void* b, int64_t rows, int d_c,
+                            const int* kept, int d_e, const char* fn) {
+    require(c && a && b && kept, std::string(fn) + ": null argument");
+    require(rows >= 0 && d_c >= 1 && d_e >= 1 && d_e <= d_c,
+            std::string(fn) + ": need 1 <= d_e <= d_c");
+}
+
+int ekv_kv_gather(ekv_ctx_t c, const void* src, int64_t rows, int d_c, const int* kept, int d_e,
+                  void* dst) {
+    return guard([&] {
+        check_rows_args(c, src, dst, rows, d_c, kept, d_e, "ekv_kv_gather");
+        set_dev(c);
+        launch_kv_gather(src, rows, d_c, kept, d_e, dst, c->stream);
+    });
+}
+
+int ekv_kv_compress(ekv_ctx_t c, const void* src, int64_t rows, int d_c, const int* kept, int d_e,
+                    int bits, int group, void* codes, float* scales) {
+    return guard([&] {
+        check_rows_args(c, src, codes, rows, d_c, kept, d_e, "ekv_kv_compress");
+        require(scales != nullptr, "ekv_kv_compress: null scales");
+        require(bits == 8 || bits == 4, "ekv_kv_compress: bits must be 8 or 4");
+        require(group >= 1 && d_e % group == 0, "ekv_kv_compress: group must divide d_e");
+        require(bits == 8 || (group % 2 == 0 && d_e % 2 == 0),
+                "ekv_kv_compress: int4 needs an even group");
+        set_dev(c);
+        launch_kv_compress(src, rows, d_c, kept, d_e, bits, group, codes, scales, c->stream);
+    });
+}
+
+int ekv_kv_dequant(ekv_ctx_t c, const void* codes, const float* scales, int64_t rows, int d_e,
+                   int bits, int group, void* dst) {
+    return guard([&] {
+        require(c && codes && scales && dst, "ekv_kv_dequant: null argument");
+        require(bits == 8 || bits == 4, "ekv_kv_dequant: bits must be 8 or 4");
+        require(group >= 1 && d_e % group == 0, "ekv_kv_dequant: group must divide d_e");
+        set_dev(c);
+        launch_kv_dequant(codes, scales, rows, d_e, bits, group, dst, c->stream);
+    });
+}
+
+// ---------------------------------------------------------------- stage 3
+static void check_segment(const ekv_segment& s, int d) {
+    require(s.S >= 0, "decode_attention: negative context length");
+    if (s.S == 0) return;
+    require(s.k && s.v, "decode_attention: null context K/V");
+    require(s.format == EKV_KV_BF16 || s.format == EKV_KV_INT8 || s.format == EKV_KV_INT4,
+            "decode_attention: unknown context format");
+    if (s.format != EKV_KV_BF16) {
+        require(s.k_scales && s.v_scales, "decode_attention: null scales");
+        const int epl = s.format == EKV_KV_INT8 ? 16 : 32;
+        require(s.group >= epl && s.group % epl == 0 && d % s.group == 0,
+                "decode_attention: group must be a multiple of " + std::to_string(epl) +
+                    " dividing head_dim",
+                EKV_EUNSUPPORTED);
+    }
+}
+
+int ekv_decode_attention(ekv_ctx_t c, int R, int H, int d, const float* q,
+                         const ekv_segment* ctx_seg, const void* uk, const void* uv, int user_cap,
+                         int user_base, float* out, float* lse) {
+    return guard([&] {
+        require(c && q && ctx_seg && uk && uv && out, "ekv_decode_attention: null argument");
+        require(R >= 1 && H >= 1, "ekv_decode_attention: empty shape");
+        require(d == 32 || d == 64 || d == 128, "ekv_decode_attention: head_dim must be 32, 64 or 128",
+                EKV_EUNSUPPORTED);
+        require(user_base >= 0 && user_base + R <= user_cap,
+                "segment_attention: empty segment (user rows exceed the cache)");
+        check_segment(*ctx_seg, d);
+        set_dev(c);
+        static thread_local float* ws = nullptr;
+        static thread_local size_t ws_n = 0;
+        static thread_local unsigned* ctr = nullptr;
+        static thread_local size_t ctr_n = 0;
+        const size_t need = attn_ws_floats(R, H, ctx_seg->S, d);
+        if (need > ws_n) {
+            if (ws) cudaFree(ws);
+            ws = dalloc<float>(need);
+            ws_n = need;
+        }
+        if ((size_t)R * H > ctr_n) {
+            if (ctr) cudaFree(ctr);
+            ctr = dalloc<unsigned>((size_t)R * H);
+            EKV_CUDA(cudaMemset(ctr, 0, sizeof(unsigned) * R * H));
+            ctr_n = (size_t)R * H;
+        }
+        AttnArgs a{};
+        a.R = R;
+        a.H = H;
+        a.D = d;
+        a.q = q;
+        a.fmt = ctx_seg->S > 0 ? ctx_seg->format : EKV_KV_BF16;
+        a.S = ctx_seg->S;
+        a.group = ctx_seg->group;
+        a.ck = ctx_seg->k;
+        a.cv = ctx_seg->v;
+        a.cks = ctx_seg->k_scales;
+        a.cvs = ctx_seg->v_scales;
+        a.uk = (const uint16_t*)uk;
+        a.uv = (const uint16_t*)uv;
+        a.ucap = user_cap;
+        a.user_base = user_base;
+        a.out = out;
+        a.lse = lse;
+        a.ws = ws;
+        a.counters = ctr;
+        launch_decode_attention(a, c->stream);
+    });
+}
+
+// ---------------------------------------------------------------- model
+int ekv_model_create(ekv_ctx_t c, const ekv_model_config* cfg, ekv_model_t* out) {
+    return guard([&] {
+        require(c && cfg && out, "ekv_model_create: null argument");
+        require(cfg->num_layers >= 1, "ModelConfig: num_layers must be >= 1");
+        require(cfg->head_dim >= 1, "ModelConfig: head_dim must be >= 1");
+        require(cfg->num_heads >= 1, "ModelConfig: num_heads must be >= 1");
+        require(cfg->max_positions >= 1, "ModelConfig: max_positions must be >= 1");
+        const int h = cfg->num_heads * cfg->head_dim;
+        require(h % 256 == 0 && h <= 4096,
+                "ModelConfig: hidden_size must be a multiple of 256 (<= 4096) for the B200 "
+                "projection kernels",
+                EKV_EUNSUPPORTED);
+        require(cfg->head_dim == 32 || cfg->head_dim == 64 || cfg->head_dim == 128,
+                "ModelConfig: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
+        set_dev(c);
+        auto* m = new ekv_model_s();
+        m->ctx = c;
+        m->cfg = *cfg;
+        m->h = h;
+        try {
+            m->weights = dalloc<uint16_t>((size_t)cfg->num_layers * m->layer_elems());
+            m->gamma = dalloc<float>(h);
+            m->bias = dalloc<float>(h);
+            m->pos = dalloc<uint16_t>((size_t)cfg->max_positions * h);
+        } catch (...) {
+            cudaFree(m->weights);
+            cudaFree(m->gamma);
+            cudaFree(m->bias);
+            cudaFree(m->pos);
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int ekv_model_destroy(ekv_model_t m) {
+    return guard([&] {
+        if (!m) return;
+        cudaSetDevice(m->ctx->device);
+        cudaFree(m->weights);
+        cudaFree(m->gamma);
+        cudaFree(m->bias);
+        cudaFree(m->pos);
+        delete m;
+    });
+}
+
+int ekv_model_set_layer(ekv_model_t m, int layer, const uint16_t* wqkvT, const uint16_t* woT) {
+    return guard([&] {
+        require(m && wqkvT && woT, "ekv_model_set_layer: null argument");
+        require(layer >= 0 && layer < m->cfg.num_layers,
+                "project_qkv: layer " + std::to_string(layer) + " out of range");
+        set_dev(m->ctx);
+        const size_t h = m->h;
+        EKV_CUDA(cudaMemcpyAsync(m->wqkvT(layer), wqkvT, 3 * h * h * 2, cudaMemcpyHostToDevice,
+                                 m->ctx->stream));
+        EKV_CUDA(cudaMemcpyAsync(m->woT(layer), woT, h * h * 2, cudaMemcpyHostToDevice,
+                                 m->ctx->stream));
+        EKV_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    });
+}
+
+int ekv_model_set_io(ekv_model_t m, const float* gamma, const float* bias, const uint16_t* pos) {
+    return guard([&] {
+        require(m && gamma && bias && pos, "ekv_model_set_io: null argument");
+        set_dev(m->ctx);
+        const size_t h = m->h;
+        EKV_CUDA(cudaMemcpyAsync(m->gamma, gamma, h * 4, cudaMemcpyHostToDevice, m->ctx->stream));
+        EKV_CUDA(cudaMemcpyAsync(m->bias, bias, h * 4, cudaMemcpyHostToDevice, m->ctx->stream));
+        EKV_CUDA(cudaMemcpyAsync(m->pos, pos, (size_t)m->cfg.max_positions * h * 2,
+                                 cudaMemcpyHostToDevice, m->ctx->stream));
+        EKV_CUDA(cudaStreamSynchronize(m->ctx->stream));
+    });
+}
+
+int ekv_model_synthesize(ekv_model_t m, uint64_t seed, double w_scale, double pos_scale) {
+    return guard([&] {
+        require(m != nullptr, "null model");
+        set_dev(m->ctx);
+        cudaStream_t st = m->ctx->stream;
+        const int L = m->cfg.num_layers, h = m->h;
+        const double qs = w_scale / std::sqrt((double)m->cfg.head_dim);  // 1/sqrt(d) folded into W_Q
+        for (int l = 0; l < L; ++l) {
+            launch_fill_uniform_bf16(m->wqkvT(l), (int64_t)h * h, seed, 4 * l + 0, -qs, qs, st);
+            launch_fill_uniform_bf16(m->wqkvT(l) + (size_t)h * h, (int64_t)2 * h * h, seed,
+                                     4 * l + 1, -w_scale, w_scale, st);
+            launch_fill_uniform_bf16(m->woT(l), (int64_t)h * h, seed, 4 * l + 2, -w_scale,
+                                     w_scale, st);
+        }
+        launch_fill_uniform_bf16(m->pos, (int64_t)m->cfg.max_positions * h, seed, 0x706F73,
+                                 -pos_scale, pos_scale, st);
+        std::vector<float> ones(h, 1.0f), zeros(h, 0.0f);
+        EKV_CUDA(cudaMemcpyAsync(m->gamma, ones.data(), h * 4, cudaMemcpyHostToDevice, st));
+        EKV_CUDA(cudaMemcpyAsync(m->bias, zeros.data(), h * 4, cudaMemcpyHostToDevice, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ekv_model_weights(ekv_model_t m, int layer, void** wqkvT, void** woT) {
+    return guard([&] {
+        require(m && wqkvT && woT, "null argument");
+        require(layer >= 0 && layer < m->cfg.num_layers, "layer out of range");
+        *wqkvT = m->wqkvT(layer);
+        *woT = m->woT(layer);
+    });
+}
+
+int ekv_model_io(ekv_model_t m, float** gamma, float** bias, void** pos) {
+    return guard([&] {
+        require(m && gamma && bias && pos, "null argument");
+        *gamma = m->gamma;
+        *bias = m->bias;
+        *pos = m->pos;
+    });
+}
+
+// ---------------------------------------------------------------- context
+int ekv_kvctx_create(ekv_model_t m, int S, const int* layer_format, int group, ekv_kvctx_t* out) {
+    return guard([&] {
+        require(m && layer_format && out, "ekv_kvctx_create: null argument");
+        require(S >= 0, "assemble_context: negative context length");
+        const int L = m->cfg.num_layers, d = m->cfg.head_dim;
+        auto* c = new ekv_kvctx_s();
+        c->model = m;
+        c->S = S;
+        c->group = group;
+        c->fmt.assign(layer_format, layer_format + L);
+        try {
+            for (int l = 0; l < L; ++l) {
+                const int f = c->fmt[l];
+                require(f == EKV_KV_BF16 || f == EKV_KV_INT8 || f == EKV_KV_INT4,
+                        "assemble_context: layer " + std::to_string(l) + " has an unknown format");
+                if (f != EKV_KV_BF16) {
+                    const int epl = f == EKV_KV_INT8 ? 16 : 32;
+                    require(group >= epl && group % epl == 0 && d % group == 0,
+                            "assemble_context: layer " + std::to_string(l) +
+                                " dim mismatch (group " + std::to_string(group) +
+                                " incompatible with head_dim " + std::to_string(d) + ")",
+                            EKV_EUNSUPPORTED);
+                }
+            }
+            set_dev(m->ctx);
+            ctx_storage(c);
+        } catch (...) {
+            for (void* p : c->allocs) cudaFree(p);
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int ekv_kvctx_destroy(ekv_kvctx_t c) {
+    return guard([&] {
+        if (!c) return;
+        cudaSetDevice(c->model->ctx->device);
+        for (void* p : c->allocs) cudaFree(p);
+        delete c;
+    });
+}
+
+int ekv_kvctx_layer(ekv_kvctx_t c, int layer, ekv_segment* seg) {
+    return guard([&] {
+        require(c && seg, "null argument");
+        require(layer >= 0 && layer < (int)c->seg.size(),
+                "assemble_context: missing layer " + std::to_string(layer));
+        *seg = c->seg[layer];
+    });
+}
+
+int ekv_kvctx_upload_bf16(ekv_kvctx_t c, int layer, const uint16_t* k, const uint16_t* v) {
+    return guard([&] {
+        require(c && k && v, "null argument");
+        require(layer >= 0 && layer < (int)c->seg.size(),
+                "assemble_context: missing layer " + std::to_string(layer));
+        const ekv_segment& s = c->seg[layer];
+        require(s.format == EKV_KV_BF16,
+                "assemble_context: layer " + std::to_string(layer) + " is not a bf16 layer");
+        if (c->S == 0) return;
+        set_dev(c->model->ctx);
+        const size_t bytes = (size_t)c->model->cfg.num_heads * c->S * c->model->cfg.head_dim * 2;
+        cudaStream_t st = c->model->ctx->stream;
+        EKV_CUDA(cudaMemcpyAsync((void*)s.k, k, bytes, cudaMemcpyHostToDevice, st));
+        EKV_CUDA(cudaMemcpyAsync((void*)s.v, v, bytes, cudaMemcpyHostToDevice, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ekv_kvctx_set_layer(ekv_kvctx_t c, int layer, const void* k, const void* v, const float* ks,
+                        const float* vs) {
+    return guard([&] {
+        require(c && k && v, "ekv_kvctx_set_layer: null argument");
+        require(layer >= 0 && layer < (int)c->seg.size(),
+                "assemble_context: missing layer " + std::to_string(layer));
+        const ekv_segment& s = c->seg[layer];
+        if (c->S == 0) return;
+        ekv_model_s* m = c->model;
+        set_dev(m->ctx);
+        cudaStream_t st = m->ctx->stream;
+        const size_t rows = (size_t)m->cfg.num_heads * c->S, d = m->cfg.head_dim;
+        const size_t bytes = rows * d * s.format / 8;
+        EKV_CUDA(cudaMemcpyAsync((void*)s.k, k, bytes, cudaMemcpyDeviceToDevice, st));
+        EKV_CUDA(cudaMemcpyAsync((void*)s.v, v, bytes, cudaMemcpyDeviceToDevice, st));
+        if (s.format != EKV_KV_BF16) {
+            require(ks && vs, "ekv_kvctx_set_layer: quantised layer needs scales");
+            const size_t sb = rows * (d / s.group) * sizeof(float);
+            EKV_CUDA(cudaMemcpyAsync((void*)s.k_scales, ks, sb, cudaMemcpyDeviceToDevice, st));
+            EKV_CUDA(cudaMemcpyAsync((void*)s.v_scales, vs, sb, cudaMemcpyDeviceToDevice, st));
+        }
+    });
+}
+
+int ekv_kvctx_synthesize(ekv_kvctx_t c, uint64_t seed) {
+    return guard([&] {
+        require(c != nullptr, "null context");
+        if (c->S == 0) return;
+        ekv_model_s* m = c->model;
+        set_dev(m->ctx);
+        cudaStream_t st = m->ctx->stream;
+        const int H = m->cfg.num_heads, d = m->cfg.head_dim;
+        const int64_t rows = (int64_t)H * c->S;
+        for (size_t l = 0; l < c->seg.size(); ++l) {
+            const ekv_segment& s = c->seg[l];
+            if (s.format == EKV_KV_BF16) {
+                launch_fill_uniform_bf16((void*)s.k, rows * d, seed, 1000 + 2 * l, -1.0, 1.0, st);
+                launch_fill_uniform_bf16((void*)s.v, rows * d, seed, 1001 + 2 * l, -1.0, 1.0, st);
+            } else {
+                // random bf16 staging rows, then the real compressor (kept = identity)
+                uint16_t* tmp = dalloc<uint16_t>((size_t)rows * d);
+                int* kept = dalloc<int>(d);
+                std::vector<int> id(d);
+                std::iota(id.begin(), id.end(), 0);
+                EKV_CUDA(cudaMemcpyAsync(kept, id.data(), sizeof(int) * d, cudaMemcpyHostToDevice, st));
+                for (int kv = 0; kv < 2; ++kv) {
+                    launch_fill_uniform_bf16(tmp, rows * d, seed, 1000 + 2 * l + kv, -1.0, 1.0, st);
+                    launch_kv_compress(tmp, rows, d, kept, d, s.format, s.group,
+                                       (void*)(kv ? s.v : s.k),
+                                       (float*)(kv ? s.v_scales : s.k_scales), st);
+                }
+                EKV_CUDA(cudaStreamSynchronize(st));
+                cudaFree(tmp);
+                cudaFree(kept);
+            }
+        }
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// ---------------------------------------------------------------- sessions
+int ekv_session_create(ekv_model_t m, ekv_kvctx_t c, int max_user_rows, ekv_session_t* out) {
+    return guard([&] {
+        require(m && c && out, "ekv_session_create: null argument");
+        require(c->model == m || (c->model->cfg.num_heads == m->cfg.num_heads &&
+                                  c->model->cfg.head_dim == m->cfg.head_dim),
+                "collaborative_decode: context dims do not match model; align with head pruning "
+                "first");
+        require((int)c->seg.size() == m->cfg.num_layers,
+                "collaborative_decode: context has " + std::to_string(c->seg.size()) +
+                    " layers, model has " + std::to_string(m->cfg.num_layers));
+        require(max_user_rows >= 1, "ekv_session_create: max_user_rows must be >= 1");
+        set_dev(m->ctx);
+        auto* s = new ekv_session_s();
+        s->model = m;
+        s->kv = c;
+        s->cap = max_user_rows;
+        try {
+            session_alloc(s);
+        } catch (...) {
+            for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
+                            (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
+                            (void*)s->ws, (void*)s->counters})
+                cudaFree(p);
+            delete s;
+            throw;
+        }
+        *out = s;
+    });
+}
+
+int ekv_session_destroy(ekv_session_t s) {
+    return guard([&] {
+        if (!s) return;
+        cudaSetDevice(s->model->ctx->device);
+        cudaStreamSynchronize(s->model->ctx->stream);
+        if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
+        for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
+                        (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
+                        (void*)s->ws, (void*)s->counters})
+            cudaFree(p);
+        delete s;
+    });
+}
+
+int ekv_session_reset(ekv_session_t s) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        set_dev(s->model->ctx);
+        session_reset(s, s->model->ctx->stream);
+    });
+}
+
+int ekv_session_length(ekv_session_t s, int* rows) {
+    return guard([&] {
+        require(s && rows, "null argument");
+        *rows = s->user_len;
+    });
+}
+
+int ekv_session_forward(ekv_session_t s, const float* emb, int n, float* out) {
+    return guard([&] {
+        require(s && emb && out, "ekv_session_forward: null argument");
+        require(n >= 1, "ekv_session_forward: n must be >= 1");
+        set_dev(s->model->ctx);
+        cudaStream_t st = s->model->ctx->stream;
+        const int first = s->user_len;
+        session_forward(s, emb, n, st);
+        EKV_CUDA(cudaMemcpyAsync(out, s->pre_out + (size_t)first * s->model->h,
+                                 sizeof(float) * n * s->model->h, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+int ekv_session_decode(ekv_session_t s, int steps, float* out) {
+    return guard([&] {
+        require(s && out, "ekv_session_decode: null argument");
+        set_dev(s->model->ctx);
+        cudaStream_t st = s->model->ctx->stream;
+        if (s->user_len == 0 && s->steps == 0)  // no prefill: the first input row is zeros
+            EKV_CUDA(cudaMemsetAsync(s->xa, 0, sizeof(float) * s->model->h, st));
+        const int first = s->steps;
+        session_decode(s, steps, st);
+        EKV_CUDA(cudaMemcpyAsync(out, s->hist + (size_t)first * s->model->h,
+                                 sizeof(float) * steps * s->model->h, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+int ekv_session_user_kv(ekv_session_t s, int layer, void** k, void** v, int* cap) {
+    return guard([&] {
+        require(s && k && v && cap, "null argument");
+        require(layer >= 0 && layer < s->model->cfg.num_layers, "layer out of range");
+        *k = s->uk + (size_t)layer * s->ukv_layer();
+        *v = s->uv + (size_t)layer * s->ukv_layer();
+        *cap = s->cap;
+    });
+}
+
+int ekv_collaborative_decode(ekv_session_t s, const float* user_emb, int U, int steps,
+                             float* prefill_out, float* step_out) {
+    return guard([&] {
+        require(s && step_out && (U == 0 || user_emb), "collaborative_decode: null argument");
+        require(steps >= 1, "collaborative_decode: steps must be >= 1");
+        require(U >= 0, "collaborative_decode: negative user rows");
+        ekv_model_s* m = s->model;
+        set_dev(m->ctx);
+        cudaStream_t st = m->ctx->stream;
+        const int total = s->kv->S + U + steps;
+        require(total <= m->cfg.max_positions,
+                "position overflow: " + std::to_string(total) + " > max_positions " +
+                    std::to_string(m->cfg.max_positions));
+        session_reset(s, st);
+        const size_t h = m->h;
+        if (U > 0) {
+            check_overflow(s, U);
+            EKV_CUDA(cudaMemcpyAsync(s->emb, user_emb, sizeof(float) * U * h,
+                                     cudaMemcpyHostToDevice, st));
+            session_forward(s, s->emb, U, st);
+            if (prefill_out)
+                EKV_CUDA(cudaMemcpyAsync(prefill_out, s->pre_out, sizeof(float) * U * h,
+                                         cudaMemcpyDeviceToHost, st));
+        } else {
+            EKV_CUDA(cudaMemsetAsync(s->xa, 0, sizeof(float) * h, st));
+        }
+        session_decode(s, steps, st);
+        EKV_CUDA(cudaMemcpyAsync(step_out, s->hist, sizeof(float) * steps * h,
+                                 cudaMemcpyDeviceToHost, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+// ---------------------------------------------------------------- scheduler
+int ekv_cache_source(int layer, double cost_local, double cost_peer, int boundary, int m,
+                     int* source) {
+    return guard([&] {
+        require(source != nullptr, "null argument");
+        require(layer >= 1 && layer <= m, "cache_source: layer " + std::to_string(layer) +
+                                              " outside 1.." + std::to_string(m));
+        *source = layer > boundary ? 2 : (cost_local <= cost_peer ? 0 : 1);
+    });
+}
+
+int ekv_pipeline_schedule(const double* t_comm, const double* t_comp, int n, double* t_pip,
+                          double* sequential_total, double* pipelined_total) {
+    return guard([&] {
+        require(n >= 1, "pipeline_schedule: empty layer list");
+        require(t_comm && t_comp && t_pip && sequential_total && pipelined_total,
+                "pipeline_schedule: null argument");
+        for (int l = 0; l < n; ++l)
+            require(t_comm[l] >= 0.0 && t_comp[l] >= 0.0, "pipeline_schedule: negative time");
+        double prev = 0.0, pip = 0.0, seq = 0.0;
+        for (int l = 0; l < n; ++l) {
+            t_pip[l] = std::max(t_comm[l], prev);
+            pip += t_pip[l];
+            prev = t_comp[l];
+        }
+        for (int l = 0; l < n; ++l) seq += t_comm[l] + t_comp[l];
+        *pipelined_total = pip + t_comp[n - 1];
+        *sequential_total = seq;
+    });
+}
+
+}  // extern "C"

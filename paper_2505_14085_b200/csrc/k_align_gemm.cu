@@ -1,0 +1,360 @@
+// K1: the alignment projection Q = X * W_Q of every matched cloud layer, on
+// the 5th-generation tensor cores, reduced in the epilogue to per-column sums
+// of squares (the Q half of the channel score of select_channels,
+// head_prune.cpp:92-97).  Q itself is never written to memory.
+//
+// Replaces project_qkv (transformer.cpp:133-152) as used by build_deep_kv
+// (sim.cpp:240-253), which recomputes Q for each distinct matched cloud layer
+// lc from that layer's input hidden state X_lc.
+//
+// Structure (one CTA per SM, persistent over (layer, m-block, n-block) tiles):
+//   warp 0      TMA producer: X tile 128x64 and W tile 256x64 (bf16, 128-byte
+//               swizzle) per k-step into a 4-stage shared-memory ring
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               (kind::f16, M=128, N=256, K=16, fp32 accumulate in TMEM)
+//   warp 2      TMEM allocator (512 columns = two 256-column accumulators)
+//   warps 4..7  epilogue: tcgen05.ld 32 columns at a time, square, reduce the
+//               128 rows with a 31-shuffle butterfly reduce-scatter, combine
+//               the 4 warps in shared memory, one fp64 atomic per column.
+// The two TMEM accumulators let the epilogue of tile i overlap the MMAs of
+// tile i+1.  Every mbarrier wait is bounded (trap after ~2 s) so a pipeline
+// bug fails the launch instead of hanging the device.
+#include <cuda.h>
+
+#include "ekv_common.cuh"
+#include "ekv_kernels.h"
+
+namespace ekv {
+
+namespace k1 {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 512;
+constexpr int THREADS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 4 * BN * 4 /*red*/ + 256 /*barriers*/ + 1024;
+
+// instruction descriptor: D fp32 (bits 4-5 = 1), A bf16 (7-9 = 1), B bf16
+// (10-12 = 1), both K-major, N>>3 at 17-22, M>>4 at 24-28.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t addr = smem_u32(bar);
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 4000000000ll) __trap();  // pipeline bug: fail, do not hang
+    }
+}
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0,
+                                            int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: LBO = 16 B
+// (field 1), SBO = 1024 B between 8-row groups (field 64), version 1,
+// layout type 2 (SWIZZLE_128B).  Stage buffers are 1024-byte aligned.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)64 << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Sum over the 32 lanes of each of the 32 values; lane j returns column j.
+__device__ __forceinline__ float butterfly_colsum(float* v, int lane) {
+#pragma unroll
+    for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+        const bool upper = lane & off;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const float send = upper ? v[i] : v[i + n / 2];
+            const float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    return v[0];
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    align_qnorm_kernel(const __grid_constant__ CUtensorMap map_x,
+                       const __grid_constant__ CUtensorMap map_w, int m_layers, int S, int h_c,
+                       int n_cols, double* __restrict__ colsq) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    float* red = (float*)(smem + STAGES * STAGE_BYTES);  // [4][BN]
+    uint64_t* bars = (uint64_t*)(red + 4 * BN);
+    uint64_t* full = bars;               // [STAGES]
+    uint64_t* empty = bars + STAGES;     // [STAGES]
+    uint64_t* tfull = bars + 2 * STAGES; // [2]
+    uint64_t* tempty = tfull + 2;        // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mblocks = S / BM, nblocks = n_cols / BN, kblocks = h_c / BK;
+    const int tiles_per_layer = mblocks * nblocks;
+    const int total = m_layers * tiles_per_layer;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x) {
+                const int layer = t / tiles_per_layer;
+                const int rem = t - layer * tiles_per_layer;
+                const int mb = rem / nblocks, nb = rem - (rem / nblocks) * nblocks;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    tma_load_3d(&map_x, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM, layer);
+                    tma_load_3d(&map_w, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN, layer);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+                const int acc = local & 1;
+                mbar_wait(&tempty[acc], ((local >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dtmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        umma_bf16(dtmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                                  (kb | k) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int quad = warp - 4;  // TMEM lanes quad*32 .. quad*32+31
+        int local = 0;
+        for (int t = blockIdx.x; t < total; t += gridDim.x, ++local) {
+            const int layer = t / tiles_per_layer;
+            const int rem = t - layer * tiles_per_layer;
+            const int nb = rem - (rem / nblocks) * nblocks;
+            const int acc = local & 1;
+            mbar_wait(&tfull[acc], (local >> 1) & 1);
+            tc_fence_after();
+            const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                float v[32];
+                tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = v[i] * v[i];
+                red[quad * BN + c * 32 + lane] = butterfly_colsum(v, lane);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int et = threadIdx.x - 128;
+            for (int col = et; col < BN; col += 128) {
+                const float s = red[col] + red[BN + col] + red[2 * BN + col] + red[3 * BN + col];
+                atomicAdd(&colsq[(size_t)layer * n_cols + nb * BN + col], (double)s);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS)
+                     : "memory");
+    }
+}
+
+}  // namespace k1
+
+// ---------------------------------------------------------------------------
+// Host side: TMA descriptors through the driver entry point (no -lcuda).
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        EKV_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        require(p != nullptr && q == cudaDriverEntryPointSuccess,
+                "cuTensorMapEncodeTiled unavailable", EKV_ECUDA);
+        fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+static CUtensorMap make_map_3d(const void* base, uint64_t inner, uint64_t rows, uint64_t layers,
+                               uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {inner, rows, layers};
+    cuuint64_t strides[2] = {inner * 2, inner * rows * 2};
+    cuuint32_t box[3] = {(cuuint32_t)k1::BK, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")",
+            EKV_ECUDA);
+    return m;
+}
+
+void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
+                                int n_cols, double* colsq, int num_sms, cudaStream_t st) {
+    using namespace k1;
+    require(S % BM == 0, "align_qnorm: S must be a multiple of 128", EKV_EUNSUPPORTED);
+    require(n_cols % BN == 0, "align_qnorm: H*d_c must be a multiple of 256", EKV_EUNSUPPORTED);
+    require(h_c % BK == 0, "align_qnorm: h_c must be a multiple of 64", EKV_EUNSUPPORTED);
+    const CUtensorMap mx = make_map_3d(X, h_c, S, m_layers, BM);
+    const CUtensorMap mw = make_map_3d(WqT, h_c, n_cols, m_layers, BN);
+    static bool attr = false;
+    if (!attr) {
+        EKV_CUDA(cudaFuncSetAttribute(align_qnorm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SMEM_BYTES));
+        attr = true;
+    }
+    const int total = m_layers * (S / BM) * (n_cols / BN);
+    const int grid = total < num_sms ? total : num_sms;
+    align_qnorm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mx, mw, m_layers, S, h_c, n_cols, colsq);
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+void launch_align_qnorm(const void* X, const void* WqT, int S, int h_c, int n_cols, double* colsq,
+                        cudaStream_t st) {
+    int dev = 0, sms = 148;
+    EKV_CUDA(cudaGetDevice(&dev));
+    EKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    launch_align_qnorm_batched(X, WqT, 1, S, h_c, n_cols, colsq, sms, st);
+}
+
+}  // namespace ekv

@@ -1,0 +1,410 @@
+"""Python host layer over the C ABI, mirroring the reference's interface.
+
+Names, argument meaning and error texts follow namespace edgekv of the
+reference (/root/reference/proj/include/edgekv/*.hpp), so the parity tests read
+like the reference's own tests.  Device memory, streams and process groups
+come from PyTorch (plumbing); every computation is a call into libekv.so.
+
+Data layouts:
+  cloud / edge KV         [layer][head][token][head_dim]  (reference KVCache [l][h] matrices)
+  weights                 out-feature-major bf16 (W^T), QKV fused: wqkvT [3h][h], woT [h][h]
+  compressed KV           codes [head][token][d_e*bits/8], scales fp32 [head][token][d_e/group]
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import EKV_KV_BF16, EKV_KV_INT4, EKV_KV_INT8, EkvError, call, ekv_model_config, ekv_segment
+
+__all__ = [
+    "Context", "EkvError", "prune_retained", "align_qnorm", "kv_colnorm", "rank_channels",
+    "select_channels", "prune_cache", "kv_compress", "kv_dequant", "decode_attention",
+    "match_layers", "cache_source", "pipeline_schedule", "EdgeModel", "AssembledContext",
+    "Session", "collaborative_decode", "build_deep_kv", "EKV_KV_BF16", "EKV_KV_INT8",
+    "EKV_KV_INT4",
+]
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+class Context:
+    """ekv_ctx: one device + one CUDA stream (a torch.cuda.Stream we own)."""
+
+    def __init__(self, device: int = 0):
+        torch.cuda.set_device(device)
+        self.device = device
+        self.stream = torch.cuda.Stream(device=device)
+        h = C.c_void_p()
+        call("ekv_ctx_create", device, C.c_void_p(self.stream.cuda_stream), C.byref(h))
+        self.h = h
+
+    def synchronize(self):
+        call("ekv_ctx_synchronize", self.h)
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        call("ekv_ctx_kernel_launches", self.h, C.byref(n))
+        return n.value
+
+    def fill_uniform_bf16(self, out: torch.Tensor, seed: int, stream_id: int, lo: float, hi: float):
+        assert out.dtype == torch.bfloat16 and out.is_contiguous()
+        call("ekv_fill_uniform_bf16", self.h, _ptr(out), out.numel(), seed, stream_id, lo, hi)
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                capi.load().ekv_ctx_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def _sync_in():
+    torch.cuda.current_stream().synchronize()
+
+
+# ------------------------------------------------------------------ stage 1
+def prune_retained(lam: float, head_dim: int) -> int:
+    """PruneSpec::from_lambda(lambda, head_dim).retained (head_prune.cpp:14-22)."""
+    r = C.c_int()
+    call("ekv_prune_retained", lam, head_dim, C.byref(r))
+    return r.value
+
+
+def align_qnorm(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, colsq: torch.Tensor | None = None):
+    """K1: per-column sum over tokens of (X W_Q)^2 for m layers at once.
+    X bf16 [m][S][h_c] (or [S][h_c]), WqT bf16 [m][n_cols][h_c] -> fp64 [m][n_cols]."""
+    if X.dim() == 2:
+        X = X.unsqueeze(0)
+        WqT = WqT.unsqueeze(0)
+    m, S, hc = X.shape
+    n = WqT.shape[1]
+    assert WqT.shape == (m, n, hc) and X.dtype == WqT.dtype == torch.bfloat16
+    if colsq is None:
+        colsq = torch.zeros((m, n), dtype=torch.float64, device=X.device)
+    _sync_in()
+    call("ekv_align_qnorm", ctx.h, _ptr(X), _ptr(WqT), m, S, hc, n, _ptr(colsq))
+    ctx.synchronize()
+    return colsq
+
+
+def kv_colnorm(ctx: Context, K: torch.Tensor, colsq: torch.Tensor | None = None):
+    """K2: per-channel sum of squares over every row of K (bf16 [..., d_c]) -> fp64 [d_c]."""
+    d = K.shape[-1]
+    if colsq is None:
+        colsq = torch.zeros(d, dtype=torch.float64, device=K.device)
+    _sync_in()
+    call("ekv_kv_colnorm", ctx.h, _ptr(K), K.numel() // d, d, _ptr(colsq))
+    ctx.synchronize()
+    return colsq
+
+
+def rank_channels(q_colsq, k_colsq, retained: int):
+    """Reference ranking rule on column sums of squares (head_prune.cpp:98-107).
+    Returns (kept int32 ascending, cut margin)."""
+    q = np.ascontiguousarray(np.asarray(q_colsq, dtype=np.float64))
+    k = np.ascontiguousarray(np.asarray(k_colsq, dtype=np.float64))
+    kept = np.zeros(max(retained, 1), dtype=np.int32)
+    margin = C.c_double()
+    call("ekv_rank_channels", _dp(q), _dp(k), len(q), retained, _ip(kept), C.byref(margin))
+    return kept[:retained].copy(), margin.value
+
+
+def select_channels(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, K: torch.Tensor, lam: float,
+                    d_c: int):
+    """select_channels (head_prune.cpp:83-108) over the stacked rows of every matched
+    layer and head, with Q recomputed on the tensor cores (K1) and K norms read
+    from the cloud cache (K2).  Returns (kept, margin, q_colsq, k_colsq)."""
+    qs = align_qnorm(ctx, X, WqT)                             # [m][H*d_c]
+    q_c = qs.reshape(-1, d_c).sum(dim=0).cpu().numpy()        # fp64 over layers and heads
+    k_c = kv_colnorm(ctx, K).cpu().numpy()
+    retained = prune_retained(lam, d_c)
+    kept, margin = rank_channels(q_c, k_c, retained)
+    return kept, margin, q_c, k_c
+
+
+def prune_cache(ctx: Context, kv: torch.Tensor, kept) -> torch.Tensor:
+    """prune_cache column slice (head_prune.cpp:170-197): bf16 [..., d_c] -> [..., d_e]."""
+    kept_t = torch.as_tensor(np.asarray(kept, dtype=np.int32), device=kv.device)
+    d_c, d_e = kv.shape[-1], kept_t.numel()
+    out = torch.empty(kv.shape[:-1] + (d_e,), dtype=kv.dtype, device=kv.device)
+    _sync_in()
+    call("ekv_kv_gather", ctx.h, _ptr(kv), kv.numel() // d_c, d_c, _ptr(kept_t), d_e, _ptr(out))
+    ctx.synchronize()
+    return out
+
+
+def kv_compress(ctx: Context, src: torch.Tensor, kept, bits: int = 8, group: int | None = None,
+                codes: torch.Tensor | None = None, scales: torch.Tensor | None = None):
+    """K3: gather kept channels + quantise + pack.  src bf16 [..., d_c]."""
+    kept_t = kept if isinstance(kept, torch.Tensor) else torch.as_tensor(
+        np.asarray(kept, dtype=np.int32), device=src.device)
+    d_c, d_e = src.shape[-1], kept_t.numel()
+    group = group or (d_e if bits == 8 else 32)
+    rows = src.numel() // d_c
+    if codes is None:
+        codes = torch.empty(src.shape[:-1] + (d_e * bits // 8,), dtype=torch.uint8, device=src.device)
+    if scales is None:
+        scales = torch.empty(src.shape[:-1] + (d_e // group,), dtype=torch.float32, device=src.device)
+    _sync_in()
+    call("ekv_kv_compress", ctx.h, _ptr(src), rows, d_c, _ptr(kept_t), d_e, bits, group,
+         _ptr(codes), _ptr(scales))
+    ctx.synchronize()
+    return codes, scales
+
+
+def kv_dequant(ctx: Context, codes: torch.Tensor, scales: torch.Tensor, d_e: int, bits: int,
+               group: int) -> torch.Tensor:
+    """K6: bf16_rn(code * scale)."""
+    rows = codes.numel() // (d_e * bits // 8)
+    out = torch.empty(codes.shape[:-1] + (d_e,), dtype=torch.bfloat16, device=codes.device)
+    _sync_in()
+    call("ekv_kv_dequant", ctx.h, _ptr(codes), _ptr(scales), rows, d_e, bits, group, _ptr(out))
+    ctx.synchronize()
+    return out
+
+
+# ------------------------------------------------------------------ stage 3
+@dataclass
+class Segment:
+    """One layer's context segment (head-major)."""
+    format: int
+    S: int
+    k: torch.Tensor | None = None
+    v: torch.Tensor | None = None
+    k_scales: torch.Tensor | None = None
+    v_scales: torch.Tensor | None = None
+    group: int = 0
+
+    def c(self) -> ekv_segment:
+        return ekv_segment(self.format, self.S, self.group, _ptr(self.k), _ptr(self.v),
+                           _ptr(self.k_scales), _ptr(self.v_scales))
+
+
+def decode_attention(ctx: Context, q: torch.Tensor, seg: Segment, user_k: torch.Tensor,
+                     user_v: torch.Tensor, user_base: int, want_lse: bool = False):
+    """K4: q fp32 [R][H][d]; user_k/v bf16 [H][cap][d]; row r sees user rows
+    0..user_base+r (causal, cache_merge.cpp:206-207) and all S context rows."""
+    R, H, d = q.shape
+    out = torch.empty_like(q)
+    lse = torch.empty((R, H), dtype=torch.float32, device=q.device) if want_lse else None
+    cs = seg.c()
+    _sync_in()
+    call("ekv_decode_attention", ctx.h, R, H, d, _ptr(q), C.byref(cs), _ptr(user_k), _ptr(user_v),
+         user_k.shape[1], user_base, _ptr(out), _ptr(lse))
+    ctx.synchronize()
+    return (out, lse) if want_lse else out
+
+
+# ------------------------------------------------------------------ host logic
+def match_layers(edge_outs: np.ndarray, cloud_outs: np.ndarray, theta_cka: float, theta_rsa: float):
+    """match_layers (layer_match.cpp:166-228): returns (cka, rsa, best) with best[le] = -1
+    for an unmatched edge layer."""
+    e = np.ascontiguousarray(edge_outs, dtype=np.float64)
+    c = np.ascontiguousarray(cloud_outs, dtype=np.float64)
+    me, n, ce = e.shape
+    nc, _, cc = c.shape
+    cka = np.zeros((me, nc)); rsa = np.zeros((me, nc)); best = np.zeros(me, dtype=np.int32)
+    call("ekv_match_layers", _dp(e), me, ce, _dp(c), nc, cc, n, theta_cka, theta_rsa, _dp(cka),
+         _dp(rsa), _ip(best))
+    return cka, rsa, best
+
+
+def cache_source(layer: int, cost_local: float, cost_peer: float, boundary: int, m: int) -> str:
+    out = C.c_int()
+    call("ekv_cache_source", layer, cost_local, cost_peer, boundary, m, C.byref(out))
+    return ("local", "peer", "cloud")[out.value]
+
+
+def pipeline_schedule(t_comm, t_comp):
+    a = np.ascontiguousarray(t_comm, dtype=np.float64)
+    b = np.ascontiguousarray(t_comp, dtype=np.float64)
+    pip = np.zeros(len(a)); s = C.c_double(); p = C.c_double()
+    call("ekv_pipeline_schedule", _dp(a), _dp(b), len(a), _dp(pip), C.byref(s), C.byref(p))
+    return pip, s.value, p.value
+
+
+# ------------------------------------------------------------------ model / context / session
+class EdgeModel:
+    """ekv_model: the edge SLM (Model, transformer.hpp:76-83) resident in HBM."""
+
+    def __init__(self, ctx: Context, num_layers: int, num_heads: int, head_dim: int,
+                 max_positions: int):
+        self.ctx = ctx
+        self.L, self.H, self.d, self.max_pos = num_layers, num_heads, head_dim, max_positions
+        self.h = num_heads * head_dim
+        cfg = ekv_model_config(num_layers, num_heads, head_dim, max_positions)
+        hnd = C.c_void_p()
+        call("ekv_model_create", ctx.h, C.byref(cfg), C.byref(hnd))
+        self.hnd = hnd
+
+    def set_layer(self, layer: int, wqkvT_bf16: np.ndarray, woT_bf16: np.ndarray):
+        a = np.ascontiguousarray(wqkvT_bf16, dtype=np.uint16)
+        b = np.ascontiguousarray(woT_bf16, dtype=np.uint16)
+        assert a.shape == (3 * self.h, self.h) and b.shape == (self.h, self.h)
+        call("ekv_model_set_layer", self.hnd, layer, a.ctypes.data_as(C.c_void_p),
+             b.ctypes.data_as(C.c_void_p))
+
+    def set_io(self, gamma: np.ndarray, bias: np.ndarray, pos_bf16: np.ndarray):
+        g = np.ascontiguousarray(gamma, dtype=np.float32)
+        b = np.ascontiguousarray(bias, dtype=np.float32)
+        p = np.ascontiguousarray(pos_bf16, dtype=np.uint16)
+        assert p.shape == (self.max_pos, self.h)
+        call("ekv_model_set_io", self.hnd, g.ctypes.data_as(C.c_void_p),
+             b.ctypes.data_as(C.c_void_p), p.ctypes.data_as(C.c_void_p))
+
+    def synthesize(self, seed: int, w_scale: float | None = None, pos_scale: float = 0.1):
+        call("ekv_model_synthesize", self.hnd, seed,
+             w_scale if w_scale is not None else float(np.sqrt(3.0 / self.h)), pos_scale)
+
+    def weight_ptrs(self, layer: int):
+        a = C.c_void_p(); b = C.c_void_p()
+        call("ekv_model_weights", self.hnd, layer, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def __del__(self):
+        try:
+            capi.load().ekv_model_destroy(self.hnd)
+        except Exception:
+            pass
+
+
+class AssembledContext:
+    """ekv_kvctx (AssembledContext, cache_merge.hpp:48-51): per-layer context KV,
+    bf16 for local layers, int8/int4 for layers delivered from the cloud."""
+
+    def __init__(self, model: EdgeModel, S: int, layer_formats, group: int = 0):
+        self.model = model
+        self.S = S
+        fm = np.ascontiguousarray(np.asarray(layer_formats, dtype=np.int32))
+        assert len(fm) == model.L
+        self.formats = fm.tolist()
+        self.group = group
+        hnd = C.c_void_p()
+        call("ekv_kvctx_create", model.hnd, S, _ip(fm), group, C.byref(hnd))
+        self.hnd = hnd
+
+    def segment(self, layer: int) -> ekv_segment:
+        s = ekv_segment()
+        call("ekv_kvctx_layer", self.hnd, layer, C.byref(s))
+        return s
+
+    def upload_bf16(self, layer: int, k_bf16: np.ndarray, v_bf16: np.ndarray):
+        k = np.ascontiguousarray(k_bf16, dtype=np.uint16)
+        v = np.ascontiguousarray(v_bf16, dtype=np.uint16)
+        call("ekv_kvctx_upload_bf16", self.hnd, layer, k.ctypes.data_as(C.c_void_p),
+             v.ctypes.data_as(C.c_void_p))
+
+    def set_layer(self, layer: int, k: torch.Tensor, v: torch.Tensor,
+                  k_scales: torch.Tensor | None = None, v_scales: torch.Tensor | None = None):
+        """Deliver one layer from device tensors (bf16 K/V, or codes + scales)."""
+        _sync_in()
+        call("ekv_kvctx_set_layer", self.hnd, layer, _ptr(k), _ptr(v), _ptr(k_scales),
+             _ptr(v_scales))
+        self.model.ctx.synchronize()
+
+    def synthesize(self, seed: int):
+        call("ekv_kvctx_synthesize", self.hnd, seed)
+
+    def __del__(self):
+        try:
+            capi.load().ekv_kvctx_destroy(self.hnd)
+        except Exception:
+            pass
+
+
+class Session:
+    """ekv_session: one request's user/generated KV cache + decode state."""
+
+    def __init__(self, model: EdgeModel, context: AssembledContext, max_user_rows: int):
+        self.model, self.context, self.cap = model, context, max_user_rows
+        hnd = C.c_void_p()
+        call("ekv_session_create", model.hnd, context.hnd, max_user_rows, C.byref(hnd))
+        self.hnd = hnd
+
+    def reset(self):
+        call("ekv_session_reset", self.hnd)
+
+    def forward(self, emb: torch.Tensor) -> torch.Tensor:
+        """merged_forward over n new rows (device fp32 [n][h])."""
+        emb = emb.contiguous().float()
+        out = torch.empty_like(emb)
+        _sync_in()
+        call("ekv_session_forward", self.hnd, _ptr(emb), emb.shape[0], _ptr(out))
+        self.model.ctx.synchronize()
+        return out
+
+    def decode(self, steps: int, out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((steps, self.model.h), dtype=torch.float32,
+                              device=f"cuda:{self.model.ctx.device}")
+        call("ekv_session_decode", self.hnd, steps, _ptr(out))
+        if sync:
+            self.model.ctx.synchronize()
+        return out
+
+    def user_kv(self, layer: int):
+        k = C.c_void_p(); v = C.c_void_p(); cap = C.c_int()
+        call("ekv_session_user_kv", self.hnd, layer, C.byref(k), C.byref(v), C.byref(cap))
+        return k.value, v.value, cap.value
+
+    def __del__(self):
+        try:
+            capi.load().ekv_session_destroy(self.hnd)
+        except Exception:
+            pass
+
+
+def collaborative_decode(session: Session, user_embeddings: np.ndarray, steps: int):
+    """collaborative_decode (cache_merge.cpp:230-273) through the host-buffer C-ABI entry
+    point.  Returns (prefill_outputs [U][h], step_outputs [steps][h]) as fp32 numpy."""
+    h = session.model.h
+    ue = np.ascontiguousarray(np.asarray(user_embeddings, dtype=np.float32).reshape(-1, h))
+    U = ue.shape[0]
+    pre = np.zeros((max(U, 1), h), dtype=np.float32)
+    st = np.zeros((max(steps, 1), h), dtype=np.float32)
+    call("ekv_collaborative_decode", session.hnd, ue.ctypes.data_as(C.c_void_p), U, steps,
+         pre.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p))
+    return pre[:U], st[:steps]
+
+
+def build_deep_kv(ctx: Context, context: AssembledContext, deep_match: dict, X: torch.Tensor,
+                  WqT: torch.Tensor, cloud_k: torch.Tensor, cloud_v: torch.Tensor, lam: float,
+                  cloud_layers: list):
+    """Artifacts::build_deep_kv (sim.cpp:217-265) on the GPU: K1+K2 channel scores
+    over every distinct matched cloud layer, host ranking, then K3 compression of
+    each matched layer's K/V straight into the context's deep-layer storage.
+
+    deep_match: {edge_layer: cloud_layer}; cloud_layers: the distinct matched cloud
+    layers in the order X / WqT / cloud_k / cloud_v are stacked (m of them):
+      X [m][S][h_c], WqT [m][H*d_c][h_c], cloud_k/v [m][H][S][d_c] (bf16).
+    Returns (kept, cut_margin)."""
+    m, H, S, d_c = cloud_k.shape
+    kept, margin, _, _ = select_channels(ctx, X, WqT, cloud_k, lam, d_c)
+    kept_t = torch.as_tensor(kept, device=cloud_k.device)
+    for le, lc in sorted(deep_match.items()):
+        i = cloud_layers.index(lc)
+        seg = context.segment(le)
+        assert seg.format in (EKV_KV_INT8, EKV_KV_INT4) and seg.S == S
+        rows = H * S
+        for src, codes, scales in ((cloud_k[i], seg.k, seg.k_scales), (cloud_v[i], seg.v, seg.v_scales)):
+            call("ekv_kv_compress", ctx.h, _ptr(src.contiguous()), rows, d_c, _ptr(kept_t),
+                 len(kept), seg.format, seg.group, C.c_void_p(codes), C.c_void_p(scales))
+    ctx.synchronize()
+    return kept, margin

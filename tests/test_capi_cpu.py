@@ -1,0 +1,107 @@
+"""CPU-only checks of the drop-in boundary: the C-ABI library loads, exports every
+symbol include/ekv_capi.h declares, the ctypes prototypes cover them, host-only
+entry points follow the reference, and compute entry points refuse to run
+without a B200 (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "ekv_capi.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2505_14085_b200 import build, capi
+    build.build()
+    return capi.load()
+
+
+def declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(ekv_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_path():
+    names = declared()
+    for must in ["ekv_align_qnorm", "ekv_kv_colnorm", "ekv_rank_channels", "ekv_match_layers",
+                 "ekv_kv_gather", "ekv_kv_compress", "ekv_kv_dequant", "ekv_decode_attention",
+                 "ekv_collaborative_decode", "ekv_cache_source", "ekv_pipeline_schedule"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_2505_14085_b200 import capi
+    out = subprocess.run(["nm", "-D", "--defined-only", capi.LIBEKV], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\sT\s(ekv_\w+)", out))
+    missing = [n for n in declared() if n not in exported]
+    assert not missing, missing
+    assert set(declared()) == set(capi.PROTOS), set(declared()) ^ set(capi.PROTOS)
+
+
+def test_library_is_sm100a_only(lib):
+    from paper_2505_14085_b200 import capi
+    out = subprocess.run(["cuobjdump", "--list-elf", capi.LIBEKV], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", capi.LIBEKV], capture_output=True, text=True).stdout
+    # K1 runs on the 5th-gen tensor cores fed by TMA, with TMEM loads
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+def test_abi_version_and_host_entry_points(lib, oracle):
+    from paper_2505_14085_b200 import edgekv as ek
+    assert lib.ekv_abi_version() == 1
+    for lam, d, want in [(0.2, 80, 64), (1 / 3, 6, 4), (0.5, 7, 3), (1.0, 7, 0)]:
+        assert ek.prune_retained(lam, d) == want
+    with pytest.raises(ek.EkvError, match="lambda outside"):
+        ek.prune_retained(-0.1, 4)
+    # ranking rule incl. the tie-break golden (head_prune_test.cpp:160-167)
+    kept, _ = ek.rank_channels([1, 1, 1], [1, 1, 1], 2)
+    assert kept.tolist() == [0, 1]
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        d = int(rng.integers(2, 129))
+        q = rng.uniform(0, 2, d) ** 2
+        k = rng.uniform(0, 2, d) ** 2
+        r = int(rng.integers(0, d + 1))
+        assert ek.rank_channels(q, k, r)[0].tolist() == oracle.rank_channels(q, k, r).tolist()
+    # scheduler interface (cost_model_test.cpp:92-114)
+    assert ek.cache_source(5, 0.1, 99.0, 4, 6) == "cloud"
+    assert ek.cache_source(2, 3.0, 2.0, 4, 6) == "peer"
+    assert ek.cache_source(1, 2.0, 2.0, 4, 6) == "local"
+    with pytest.raises(ek.EkvError, match="outside 1..6"):
+        ek.cache_source(0, 1, 1, 4, 6)
+    pip, seq, tot = ek.pipeline_schedule([2, 1, 4], [3, 2, 5])
+    assert pip.tolist() == [2, 3, 4] and seq == 17.0 and tot == 14.0
+    with pytest.raises(ek.EkvError, match="negative time"):
+        ek.pipeline_schedule([-1], [0])
+
+
+def test_host_match_layers_equals_oracle(lib, oracle):
+    from paper_2505_14085_b200 import edgekv as ek
+    from oracle import model_from_reference_layout
+    e = model_from_reference_layout(oracle.init_model(3, 2, 6, 64, 41), 3, 2, 6, 64)
+    c = model_from_reference_layout(oracle.init_model(5, 4, 6, 64, 43), 5, 4, 6, 64)
+    eo = oracle.prefill(e, oracle.generate_embeddings(9, 16, 12))[0]
+    co = oracle.prefill(c, oracle.generate_embeddings(9, 16, 24))[0]
+    a = ek.match_layers(eo, co, 0.5, 0.3)
+    b = oracle.match_layers(eo, co, 0.5, 0.3)
+    assert np.array_equal(a[2], b[2])
+    assert np.allclose(a[0], b[0], rtol=1e-12, atol=1e-14)
+    assert np.allclose(a[1], b[1], rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_compute_entry_points_refuse_without_b200(lib):
+    h = C.c_void_p()
+    rc = lib.ekv_ctx_create(0, None, C.byref(h))
+    assert rc == -4  # EKV_ENODEV
+    assert "no CPU fallback" in lib.ekv_last_error().decode()
