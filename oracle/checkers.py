@@ -346,8 +346,10 @@ class Reference:
                                        C.c_double, C.c_double, _dp, _dp, _ip]
         L.ref_cache_source.argtypes = [C.c_int, C.c_double, C.c_double, C.c_int, C.c_int]
         L.ref_pipeline_schedule.argtypes = [_dp, _dp, C.c_int, _dp, _dp, _dp]
-        L.ref_bench_decode.argtypes = ([C.c_int] * 8 + [C.c_double, _dp, _dp,
-                                       C.POINTER(C.c_int64)])
+        L.ref_bench_setup.restype = C.c_void_p
+        L.ref_bench_setup.argtypes = [C.c_int] * 6 + [C.c_uint64]
+        L.ref_bench_run.argtypes = [C.c_void_p] + [C.c_int] * 4 + [_dp, C.POINTER(C.c_int64)]
+        L.ref_bench_free.argtypes = [C.c_void_p]
 
     def _chk(self, rc):
         if rc < 0:
@@ -472,11 +474,19 @@ class Reference:
                                                  C.byref(p)))
         return pip, s.value, p.value
 
-    def bench_decode(self, L, H, d, S, boundary, U, steps, threads, min_seconds):
-        r = C.c_double(); w = C.c_double(); n = C.c_int64()
-        self._chk(self.lib.ref_bench_decode(L, H, d, S, boundary, U, steps, threads, min_seconds,
-                                            C.byref(r), C.byref(w), C.byref(n)))
-        return r.value, w.value, n.value
+    def bench_setup(self, L, H, d, S, boundary, max_pos, seed=42):
+        h = self.lib.ref_bench_setup(L, H, d, S, boundary, max_pos, seed)
+        if not h:
+            raise RefError(self.lib.ref_last_error().decode())
+        return h
+
+    def bench_run(self, handle, U, steps, threads, calls):
+        s = C.c_double(); n = C.c_int64()
+        self._chk(self.lib.ref_bench_run(handle, U, steps, threads, calls, C.byref(s), C.byref(n)))
+        return s.value, n.value
+
+    def bench_free(self, handle):
+        self.lib.ref_bench_free(handle)
 
 
 def model_from_reference_layout(ref_model: dict, L: int, H: int, d: int, max_pos: int) -> dict:

@@ -13,6 +13,7 @@
 // scaled-init models.
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -336,24 +337,29 @@ int ref_pipeline_schedule(const double* t_comm, const double* t_comp, int n, dou
     });
 }
 
-// CPU baseline: the reference's own collaborative_decode (fp64, 1 thread per
-// session) on an edge model of the given shape with random scaled weights and
-// a random S-row assembled context, run by `threads` independent sessions for
-// at least `min_seconds`.  Reports forward rows per second (prefill + decode
-// rows; each row is one token through every layer) aggregated over threads.
-int ref_bench_decode(int L, int H, int d, int S, int boundary, int U, int steps, int threads,
-                     double min_seconds, double* rows_per_s, double* wall_s, int64_t* rows_done) {
-    return guarded([&] {
+// CPU baseline: the reference's own collaborative_decode (fp64, one session
+// per thread) on an edge model of the given shape with random scaled weights
+// (populating edgekv::Model directly) and a random
+// S-row assembled context (layers < boundary local, the rest "cloud").
+struct RefBench {
+    Model model;
+    AssembledContext ctx;
+    int h = 0;
+};
+
+void* ref_bench_setup(int L, int H, int d, int S, int boundary, int max_pos, uint64_t seed) {
+    try {
+        auto* b = new RefBench();
         const int h = H * d;
-        const int max_pos = S + U + steps;
-        Model m;
+        b->h = h;
+        Model& m = b->model;
         m.config.num_layers = L;
         m.config.num_heads = H;
         m.config.head_dim = d;
         m.config.hidden_size = h;
         m.config.max_positions = max_pos;
-        Rng rng(42);
-        const double a = 1.0 / std::sqrt((double)h);
+        Rng rng(seed);
+        const double a = std::sqrt(3.0 / (double)h);
         m.layers.resize(L);
         for (int l = 0; l < L; ++l) {
             m.layers[l].heads.resize(H);
@@ -381,33 +387,47 @@ int ref_bench_decode(int L, int H, int d, int S, int boundary, int U, int steps,
                 kv.keys.push_back(std::move(k));
                 kv.values.push_back(std::move(v));
             }
-            if (l < boundary) local[l] = std::move(kv);
-            else {
+            if (l < boundary) {
+                local[l] = std::move(kv);
+            } else {
                 shared[l] = std::move(kv);
                 origins[l] = CacheOrigin::cloud;
             }
         }
-        AssembledContext ctx = assemble_context(shared, local, origins, L);
-        Matrix user = generate_embeddings(7, U, h);
+        b->ctx = assemble_context(shared, local, origins, L);
+        return b;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// `threads` sessions in parallel, each running `calls` collaborative_decode
+// calls (U user rows + `steps` generated rows).  Reports wall seconds and the
+// forward rows processed (each row = one token through every layer).
+int ref_bench_run(void* handle, int U, int steps, int threads, int calls, double* seconds,
+                  int64_t* rows) {
+    return guarded([&] {
+        auto* b = static_cast<RefBench*>(handle);
+        Matrix user = generate_embeddings(7, U, b->h);
         std::atomic<int64_t> total{0};
+        std::string err;
         const auto t0 = std::chrono::steady_clock::now();
-        auto worker = [&] {
-            for (;;) {
-                CollaborativeResult r = collaborative_decode(m, ctx, user, steps);
-                total += (int64_t)(r.prefill_outputs.size() + r.step_outputs.size());
-                const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-                if (el >= min_seconds) break;
-            }
-        };
         std::vector<std::thread> pool;
-        for (int t = 0; t < threads; ++t) pool.emplace_back(worker);
+        for (int t = 0; t < threads; ++t)
+            pool.emplace_back([&] {
+                for (int c = 0; c < calls; ++c) {
+                    CollaborativeResult r = collaborative_decode(b->model, b->ctx, user, steps);
+                    total += (int64_t)(r.prefill_outputs.size() + r.step_outputs.size());
+                }
+            });
         for (auto& t : pool) t.join();
-        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        *rows_per_s = (double)total.load() / el;
-        *wall_s = el;
-        *rows_done = total.load();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *rows = total.load();
         return 0;
     });
 }
+
+void ref_bench_free(void* handle) { delete static_cast<RefBench*>(handle); }
 
 }  // extern "C"

@@ -136,10 +136,15 @@ int d_of(const ekv_model_s* m) { return m->cfg.head_dim; }
 // cache_merge.cpp:156-226).  `in` holds the R input rows (fp32 [R][h]);
 // `out_hist`/`hist_row_dev` receive the final-layer rows.
 void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
-                   const int* hist_row_dev, cudaStream_t st) {
+                   const int* hist_row_dev, cudaStream_t st, cudaEvent_t* ev = nullptr) {
     ekv_model_s* m = s->model;
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
+    int ei = 0;
+    auto mark = [&] {
+        if (ev) EKV_CUDA(cudaEventRecord(ev[ei++], st));
+    };
     for (int l = 0; l < L; ++l) {
+        mark();
         GemvArgs g{};
         g.N = 3 * h;
         g.K = h;
@@ -162,6 +167,7 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
         g.ucap = s->cap;
         g.user_base_dev = &s->state->user_len;
         launch_gemv(g, st);
+        mark();
 
         AttnArgs a{};
         a.R = R;
@@ -185,6 +191,7 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
         a.ws = s->ws;
         a.counters = s->counters;
         launch_decode_attention(a, st);
+        mark();
 
         GemvArgs o{};
         o.N = h;
@@ -200,7 +207,9 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
         }
         launch_gemv(o, st);
     }
+    mark();
     launch_advance(s->state, R, st);
+    mark();
 }
 
 size_t attn_ws_floats(int R, int H, int S, int d) {
@@ -1023,6 +1032,35 @@ int ekv_session_decode(ekv_session_t s, int steps, float* out) {
         session_decode(s, steps, st);
         EKV_CUDA(cudaMemcpyAsync(out, s->hist + (size_t)first * s->model->h,
                                  sizeof(float) * steps * s->model->h, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+int ekv_session_profile_step(ekv_session_t s, float* kernel_ms, int capacity, int* n_kernels) {
+    return guard([&] {
+        require(s && kernel_ms && n_kernels, "ekv_session_profile_step: null argument");
+        const int n = 3 * s->model->cfg.num_layers + 1;
+        require(capacity >= n, "ekv_session_profile_step: need room for " + std::to_string(n) +
+                                   " kernel times");
+        check_overflow(s, 1);
+        require(s->steps + 1 <= s->cap, "decode history full");
+        set_dev(s->model->ctx);
+        cudaStream_t st = s->model->ctx->stream;
+        if (s->user_len == 0 && s->steps == 0)
+            EKV_CUDA(cudaMemsetAsync(s->xa, 0, sizeof(float) * s->model->h, st));
+        std::vector<cudaEvent_t> ev(n + 1);
+        for (auto& e : ev) EKV_CUDA(cudaEventCreate(&e));
+        try {
+            forward_chunk(s, s->xa, 1, s->hist, &s->state->step, st, ev.data());
+            EKV_CUDA(cudaStreamSynchronize(st));
+            for (int i = 0; i < n; ++i) EKV_CUDA(cudaEventElapsedTime(&kernel_ms[i], ev[i], ev[i + 1]));
+        } catch (...) {
+            for (auto& e : ev) cudaEventDestroy(e);
+            throw;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        s->user_len += 1;
+        s->steps += 1;
+        *n_kernels = n;
     });
 }
 

@@ -359,6 +359,16 @@ class Session:
             self.model.ctx.synchronize()
         return out
 
+    def profile_step(self) -> np.ndarray:
+        """One real decode step, kernel by kernel, with CUDA-event times (ms):
+        [3l] QKV projection, [3l+1] attention, [3l+2] output projection, [3L] advance."""
+        n = 3 * self.model.L + 1
+        out = np.zeros(n, dtype=np.float32)
+        got = C.c_int()
+        call("ekv_session_profile_step", self.hnd, out.ctypes.data_as(C.POINTER(C.c_float)), n,
+             C.byref(got))
+        return out
+
     def user_kv(self, layer: int):
         k = C.c_void_p(); v = C.c_void_p(); cap = C.c_int()
         call("ekv_session_user_kv", self.hnd, layer, C.byref(k), C.byref(v), C.byref(cap))
