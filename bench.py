@@ -136,6 +136,10 @@ def run_reference_arm(args, rank: int, world: int):
     }))
 
 
+def _jsonable(o):
+    return o.item() if hasattr(o, "item") else str(o)
+
+
 METRIC = "edge decode tok/s w/ reused cloud KV; KV align+compress GB/s vs HBM roofline"
 
 
@@ -208,7 +212,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     Hc, dc = CLOUD["H"], CLOUD["d"]
     hc = Hc * dc
     K, W = args.steps, args.warmup
-    cap = U + W + K + 8
+    cap = U + W + K + 64  # + the kernel-by-kernel profiling steps (<= 50)
     max_pos = S + cap + T_E2E + 8
 
     # --- edge model + assembled context (local layers bf16, deep layers int8) ---
@@ -260,12 +264,15 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             kept_t.copy_(torch.from_numpy(kept))
             torch.cuda.synchronize()
             e2.record(st)
+            srcs, cds, scs = [], [], []
             for i, (le, lc) in enumerate(sorted(deep_match.items())):
                 j = lcs.index(lc)
-                for src, cd, sc in ((Kc[j], codes_k[i], sc_k[i]), (Vc[j], codes_v[i], sc_v[i])):
-                    call("ekv_kv_compress", ctx.h, C.c_void_p(src.data_ptr()), Hc * S, dc,
-                         C.c_void_p(kept_t.data_ptr()), d, BITS, d, C.c_void_p(cd.data_ptr()),
-                         C.c_void_p(sc.data_ptr()))
+                srcs += [Kc[j].data_ptr(), Vc[j].data_ptr()]
+                cds += [codes_k[i].data_ptr(), codes_v[i].data_ptr()]
+                scs += [sc_k[i].data_ptr(), sc_v[i].data_ptr()]
+            arr = lambda xs: (C.c_void_p * len(xs))(*xs)
+            ek.compress_batched(ctx, len(srcs), arr(srcs), Hc * S, dc, kept_t, d, BITS, d,
+                                arr(cds), arr(scs))
             e3.record(st)
             st.synchronize()
             if it > 0:
@@ -282,8 +289,8 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "k1_frac": flops / k1 / 1e9 / bf16_burst,
             "k3_ms": k3, "k3_gbs": k3_bytes / k3 / 1e6, "k3_frac": k3_bytes / k3 / 1e6 / hbm,
             "k3_bytes": k3_bytes, "pipeline_ms": statistics.median(tot_ms),
-            "note": "K1 per launch over all m layers (grouped GEMM, 2*m*S*h_c^2 flop); K3 = "
-                    f"{2 * DEEP} launches (K and V of {DEEP} deep layers)",
+            "note": "K1 = one launch over all m layers (grouped GEMM, 2*m*S*h_c^2 flop); K3 = "
+                    f"one batched launch over K and V of the {DEEP} deep layers",
         }
         del X, Wq, Kc, Vc
     kv_transfer = None
@@ -424,7 +431,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "kv_transfer": kv_transfer,
             "outputs_finite": finite,
         }
-        print(json.dumps(line))
+        print(json.dumps(line, default=_jsonable))
 
 
 def main():

@@ -138,6 +138,13 @@ int ekv_kv_compress(ekv_ctx_t ctx, const void* src_dev, int64_t rows, int d_c,
                     const int* kept_dev, int d_e, int bits, int group, void* codes_dev,
                     float* scales_dev);
 
+/* K3 over n (src, codes, scales) triples in ONE launch (e.g. K and V of every
+ * deep layer of build_deep_kv, sim.cpp:258-264).  The three arrays are HOST
+ * arrays of DEVICE pointers; all jobs share rows/d_c/kept/d_e/bits/group. */
+int ekv_kv_compress_batched(ekv_ctx_t ctx, int n, const void* const* src_dev, int64_t rows,
+                            int d_c, const int* kept_dev, int d_e, int bits, int group,
+                            void* const* codes_dev, float* const* scales_dev);
+
 /* K6: dst = bf16_rn(code * scale) (fp32 product), dev bf16 [rows][d_e]. */
 int ekv_kv_dequant(ekv_ctx_t ctx, const void* codes_dev, const float* scales_dev, int64_t rows,
                    int d_e, int bits, int group, void* dst_dev);

@@ -55,6 +55,7 @@ PROTOS = {
     "ekv_match_layers": [_dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
     "ekv_kv_gather": [_vp, _vp, _i64, _i, _vp, _i, _vp],
     "ekv_kv_compress": [_vp, _vp, _i64, _i, _vp, _i, _i, _i, _vp, _vp],
+    "ekv_kv_compress_batched": [_vp, _i, _pp, _i64, _i, _vp, _i, _i, _i, _pp, _pp],
     "ekv_kv_dequant": [_vp, _vp, _vp, _i64, _i, _i, _i, _vp],
     "ekv_decode_attention": [_vp, _i, _i, _i, _vp, C.POINTER(ekv_segment), _vp, _vp, _i, _i, _vp,
                              _vp],

@@ -212,9 +212,9 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
     mark();
 }
 
-size_t attn_ws_floats(int R, int H, int S, int d) {
+size_t attn_ws_floats(int R, int H, int S, int d, int ucap) {
     int rpi = 0;
-    const int items = attn_items(R, H, S, &rpi) + 1;
+    const int items = attn_items(R, H, S, &rpi) + attn_user_items(ucap);
     return (size_t)R * H * items * (d + 2);
 }
 
@@ -232,7 +232,7 @@ void session_alloc(ekv_session_s* s) {
     s->state = dalloc<DevState>(1);
     size_t ws = 0;
     for (int R = 1; R <= 8; ++R)
-        ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim));
+        ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim, s->cap));
     s->ws = dalloc<float>(ws);
     s->counters = dalloc<unsigned>((size_t)8 * m->cfg.num_heads);
     EKV_CUDA(cudaMemset(s->counters, 0, sizeof(unsigned) * 8 * m->cfg.num_heads));
@@ -618,6 +618,28 @@ int ekv_kv_compress(ekv_ctx_t c, const void* src, int64_t rows, int d_c, const i
     });
 }
 
+int ekv_kv_compress_batched(ekv_ctx_t c, int n, const void* const* src, int64_t rows, int d_c,
+                            const int* kept, int d_e, int bits, int group, void* const* codes,
+                            float* const* scales) {
+    return guard([&] {
+        require(c && src && codes && scales && kept, "ekv_kv_compress_batched: null argument");
+        require(n >= 0 && n <= kMaxCompressJobs, "ekv_kv_compress_batched: 0.." +
+                                                     std::to_string(kMaxCompressJobs) + " jobs");
+        require(rows >= 0 && d_c >= 1 && d_e >= 1 && d_e <= d_c,
+                "ekv_kv_compress_batched: need 1 <= d_e <= d_c");
+        require(bits == 8 || bits == 4, "ekv_kv_compress: bits must be 8 or 4");
+        require(group >= 1 && d_e % group == 0, "ekv_kv_compress: group must divide d_e");
+        require(bits == 8 || group % 2 == 0, "ekv_kv_compress: int4 needs an even group");
+        std::vector<CompressJob> jobs(n);
+        for (int i = 0; i < n; ++i) {
+            require(src[i] && codes[i] && scales[i], "ekv_kv_compress_batched: null job pointer");
+            jobs[i] = CompressJob{src[i], codes[i], scales[i]};
+        }
+        set_dev(c);
+        launch_kv_compress_jobs(jobs.data(), n, rows, d_c, kept, d_e, bits, group, c->stream);
+    });
+}
+
 int ekv_kv_dequant(ekv_ctx_t c, const void* codes, const float* scales, int64_t rows, int d_e,
                    int bits, int group, void* dst) {
     return guard([&] {
@@ -662,7 +684,7 @@ int ekv_decode_attention(ekv_ctx_t c, int R, int H, int d, const float* q,
         static thread_local size_t ws_n = 0;
         static thread_local unsigned* ctr = nullptr;
         static thread_local size_t ctr_n = 0;
-        const size_t need = attn_ws_floats(R, H, ctx_seg->S, d);
+        const size_t need = attn_ws_floats(R, H, ctx_seg->S, d, user_cap);
         if (need > ws_n) {
             if (ws) cudaFree(ws);
             ws = dalloc<float>(need);

@@ -14,6 +14,19 @@ struct DevState {
 
 void launch_fill_uniform_bf16(void* dst, int64_t n, uint64_t seed, uint64_t stream_id, double lo,
                               double hi, cudaStream_t st);
+// Batched compression: one launch over up to kMaxCompressJobs (src, codes,
+// scales) triples sharing rows / d_c / kept / d_e / bits / group.
+struct CompressJob {
+    const void* src;
+    void* codes;
+    float* scales;
+};
+constexpr int kMaxCompressJobs = 128;
+struct CompressJobs {
+    CompressJob job[kMaxCompressJobs];
+};
+void launch_kv_compress_jobs(const CompressJob* jobs, int n_jobs, int64_t rows, int d_c,
+                             const int* kept, int d_e, int bits, int group, cudaStream_t st);
 void launch_kv_compress(const void* src, int64_t rows, int d_c, const int* kept, int d_e, int bits,
                         int group, void* codes, float* scales, cudaStream_t st);
 void launch_kv_gather(const void* src, int64_t rows, int d_c, const int* kept, int d_e, void* dst,
@@ -46,8 +59,10 @@ struct AttnArgs {
     float* ws;
     unsigned* counters;  // [R*H], zero on entry, zero on exit
 };
-// Items per (row, head): chosen from S, H, R.  Workspace = R*H*items*(D+2) floats.
+// Context items per (row, head): chosen from S, H, R; user items cover ucap rows.
+// Workspace = R*H*(ctx items + user items)*(D+2) floats.
 int attn_items(int R, int H, int S, int* rows_per_item);
+int attn_user_items(int ucap);
 void launch_decode_attention(const AttnArgs& a, cudaStream_t st);
 
 // ---- K5 projections (GEMV / skinny GEMM over R <= 8 rows) ---------------------

@@ -30,6 +30,7 @@ namespace ekv {
 
 constexpr int kAttnThreads = 128;
 constexpr int kSub = 128;  // rows per sub-chunk (one per thread in the softmax)
+constexpr int kUserRows = 256;  // user-segment rows per item (split like the context)
 constexpr float kLog2e = 1.4426950408889634f;
 
 template <int D, int FMT>
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(kAttnThreads) decode_attn_kernel(AttnArgs a, i
     __shared__ float s_o[kAttnThreads / 32][D];
     __shared__ int s_last;
     const int item = blockIdx.x, h = blockIdx.y, r = blockIdx.z;
-    const int n_items = n_ctx_items + 1;
+    const int n_items = gridDim.x;  // context items, then user items of kUserRows rows
     const float* qf = a.q + ((size_t)r * a.H + h) * D;
     float m = -CUDART_INF_F, l = 0.0f;
     if (item < n_ctx_items) {
@@ -231,12 +232,14 @@ __global__ void __launch_bounds__(kAttnThreads) decode_attn_kernel(AttnArgs a, i
         using T = SegT<D, 16>;
         const int base = a.user_base_dev ? *a.user_base_dev : a.user_base;
         const int vis = base + r + 1;
+        const int u0 = (item - n_ctx_items) * kUserRows;
+        const int u1 = min(vis, u0 + kUserRows);  // u0 >= u1: empty partial (l = 0)
         const size_t hoff = (size_t)h * a.ucap;
         float acc[T::EPL];
 #pragma unroll
         for (int e = 0; e < T::EPL; ++e) acc[e] = 0.0f;
         attend_rows<D, 16>(qf, (const uint8_t*)(a.uk + hoff * D), (const uint8_t*)(a.uv + hoff * D),
-                           nullptr, nullptr, 1, D, 0, vis, &m, &l, acc, sc);
+                           nullptr, nullptr, 1, D, u0, u1, &m, &l, acc, sc);
         fold_partial<D, 16>(acc, s_o);
     }
     __syncthreads();
@@ -287,6 +290,8 @@ __global__ void __launch_bounds__(kAttnThreads) decode_attn_kernel(AttnArgs a, i
     if (a.lse && threadIdx.x == 0) a.lse[(size_t)r * a.H + h] = M + logf(Lsum);
 }
 
+int attn_user_items(int ucap) { return (ucap + kUserRows - 1) / kUserRows; }
+
 int attn_items(int R, int H, int S, int* rows_per_item) {
     if (S <= 0) {
         *rows_per_item = kSub;
@@ -303,7 +308,7 @@ int attn_items(int R, int H, int S, int* rows_per_item) {
 
 template <int D>
 static void launch_d(const AttnArgs& a, int rpi, int nci, cudaStream_t st) {
-    dim3 grid(nci + 1, a.H, a.R);
+    dim3 grid(nci + attn_user_items(a.ucap), a.H, a.R);
     switch (a.fmt) {
         case 16: decode_attn_kernel<D, 16><<<grid, kAttnThreads, 0, st>>>(a, rpi, nci); break;
         case 8: decode_attn_kernel<D, 8><<<grid, kAttnThreads, 0, st>>>(a, rpi, nci); break;

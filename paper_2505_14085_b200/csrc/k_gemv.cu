@@ -19,10 +19,25 @@ namespace ekv {
 
 constexpr int kGemvThreads = 256;
 
+template <int KC>
+__device__ __forceinline__ void load_row(const uint16_t* __restrict__ W, int n, int lane, uint4* w) {
+    const uint16_t* wrow = W + (size_t)n * (KC * 256);
+#pragma unroll
+    for (int c = 0; c < KC; ++c) w[c] = ld_stream(wrow + c * 256 + lane * 8);
+}
+
 template <int R, int KC>
 __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvArgs a) {
     extern __shared__ float xs[];  // [R][K]
     const int K = KC * 256;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * kGemvThreads + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * kGemvThreads) >> 5;
+    // The weight stream does not depend on x: put the first row's loads in
+    // flight before staging x so HBM latency overlaps the staging.
+    uint4 w[KC];
+    int n = warp;
+    if (n < a.N) load_row<KC>(a.W, n, lane, w);
     // ---- stage x (with the optional layer-0 input transform) ----
     int p0 = 0;
     if (a.pos) p0 = a.pos_offset + (a.pos_base_dev ? *a.pos_base_dev : a.pos_base);
@@ -36,11 +51,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvArgs a) {
         xs[i] = v;
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * kGemvThreads + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * kGemvThreads) >> 5;
     int ubase = 0;
-    if (a.mode == 1) ubase = a.user_base_dev ? *a.user_base_dev : a.user_base;
+    if (a.mode == 1) ubase = a.user_base + (a.user_base_dev ? *a.user_base_dev : 0);
     int hrow = 0;
     if (a.y_hist) hrow = a.hist_row_dev ? *a.hist_row_dev : 0;
 
@@ -51,11 +63,10 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvArgs a) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) xr[c * 8 + e] = xs[c * 256 + lane * 8 + e];
     }
-    for (int n = warp; n < a.N; n += nwarps) {
-        const uint16_t* wrow = a.W + (size_t)n * K;
-        uint4 w[KC];
-#pragma unroll
-        for (int c = 0; c < KC; ++c) w[c] = ld_stream(wrow + c * 256 + lane * 8);
+    for (; n < a.N; n += nwarps) {
+        uint4 wn[KC];
+        const int nn = n + nwarps;
+        if (nn < a.N) load_row<KC>(a.W, nn, lane, wn);  // software pipeline: next row in flight
         float acc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) acc[r] = 0.0f;
@@ -110,6 +121,8 @@ __global__ void __launch_bounds__(kGemvThreads) gemv_kernel(GemvArgs a) {
                 }
             }
         }
+#pragma unroll
+        for (int c = 0; c < KC; ++c) w[c] = wn[c];
     }
 }
 

@@ -92,9 +92,13 @@ __device__ __forceinline__ float fetch_channel(const RowLoad<DC>& r, int ch) {
 }
 
 template <int DC, int DE, int BITS>
-__global__ void __launch_bounds__(256) kv_compress_fast_kernel(
-    const uint16_t* __restrict__ src, int64_t rows, const int* __restrict__ kept, int group,
-    uint8_t* __restrict__ codes, float* __restrict__ scales) {
+__global__ void __launch_bounds__(256) kv_compress_fast_kernel(CompressJobs jobs, int64_t rows,
+                                                               const int* __restrict__ kept,
+                                                               int group) {
+    // one job (layer x {K, V}) per blockIdx.y: a single launch compresses every deep layer
+    const uint16_t* __restrict__ src = (const uint16_t*)jobs.job[blockIdx.y].src;
+    uint8_t* __restrict__ codes = (uint8_t*)jobs.job[blockIdx.y].codes;
+    float* __restrict__ scales = jobs.job[blockIdx.y].scales;
     constexpr int EPL = DE / 32;  // kept channels per lane (1, 2 or 4)
     constexpr float Q = BITS == 8 ? 127.0f : 7.0f;
     const int lane = threadIdx.x & 31;
@@ -213,47 +217,65 @@ static int grid_for(int64_t work, int per_block) {
 }
 
 template <int DC, int DE, int BITS>
-static bool try_fast(const void* src, int64_t rows, int d_c, const int* kept, int d_e, int group,
-                     void* codes, float* scales, cudaStream_t st) {
+static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c, const int* kept,
+                     int d_e, int group, cudaStream_t st) {
     if (d_c != DC || d_e != DE) return false;
     constexpr int EPL = DE / 32;
     if (group % EPL != 0) return false;
     const int gl = group / EPL;
     if (gl < 1 || gl > 32 || (gl & (gl - 1))) return false;
     const int64_t warps = (rows + 3) / 4;
-    kv_compress_fast_kernel<DC, DE, BITS><<<grid_for(warps * 32, 256), 256, 0, st>>>(
-        (const uint16_t*)src, rows, kept, group, (uint8_t*)codes, scales);
+    int bx = grid_for(warps * 32, 256);
+    const int cap = (148 * 8 + n_jobs - 1) / n_jobs;  // ~8 CTAs per SM over all jobs
+    if (bx > cap) bx = cap < 1 ? 1 : cap;
+    kv_compress_fast_kernel<DC, DE, BITS><<<dim3(bx, n_jobs), 256, 0, st>>>(jobs, rows, kept, group);
     return true;
+}
+
+void launch_kv_compress_jobs(const CompressJob* job, int n_jobs, int64_t rows, int d_c,
+                             const int* kept, int d_e, int bits, int group, cudaStream_t st) {
+    if (rows <= 0 || n_jobs <= 0) return;
+    require(n_jobs <= kMaxCompressJobs, "kv_compress: at most " +
+                                            std::to_string(kMaxCompressJobs) + " jobs per launch");
+    CompressJobs jobs{};
+    for (int i = 0; i < n_jobs; ++i) jobs.job[i] = job[i];
+    bool done = false;
+    if (bits == 8) {
+        done = try_fast<128, 64, 8>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<64, 32, 8>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<128, 128, 8>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<256, 128, 8>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<64, 64, 8>(jobs, n_jobs, rows, d_c, kept, d_e, group, st);
+    } else {
+        done = try_fast<128, 64, 4>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<64, 32, 4>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<128, 128, 4>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<256, 128, 4>(jobs, n_jobs, rows, d_c, kept, d_e, group, st) ||
+               try_fast<64, 64, 4>(jobs, n_jobs, rows, d_c, kept, d_e, group, st);
+    }
+    if (done) {
+        count_launches(1);
+    } else {
+        const int64_t work = rows * (d_e / group);
+        for (int i = 0; i < n_jobs; ++i) {
+            if (bits == 8)
+                kv_compress_generic_kernel<8><<<grid_for(work, 256), 256, 0, st>>>(
+                    (const uint16_t*)job[i].src, rows, d_c, kept, d_e, group,
+                    (uint8_t*)job[i].codes, job[i].scales);
+            else
+                kv_compress_generic_kernel<4><<<grid_for(work, 256), 256, 0, st>>>(
+                    (const uint16_t*)job[i].src, rows, d_c, kept, d_e, group,
+                    (uint8_t*)job[i].codes, job[i].scales);
+        }
+        count_launches(n_jobs);
+    }
+    EKV_CUDA(cudaGetLastError());
 }
 
 void launch_kv_compress(const void* src, int64_t rows, int d_c, const int* kept, int d_e, int bits,
                         int group, void* codes, float* scales, cudaStream_t st) {
-    if (rows <= 0) return;
-    bool done = false;
-    if (bits == 8) {
-        done = try_fast<128, 64, 8>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<64, 32, 8>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<128, 128, 8>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<256, 128, 8>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<64, 64, 8>(src, rows, d_c, kept, d_e, group, codes, scales, st);
-    } else {
-        done = try_fast<128, 64, 4>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<64, 32, 4>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<128, 128, 4>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<256, 128, 4>(src, rows, d_c, kept, d_e, group, codes, scales, st) ||
-               try_fast<64, 64, 4>(src, rows, d_c, kept, d_e, group, codes, scales, st);
-    }
-    if (!done) {
-        const int64_t work = rows * (d_e / group);
-        if (bits == 8)
-            kv_compress_generic_kernel<8><<<grid_for(work, 256), 256, 0, st>>>(
-                (const uint16_t*)src, rows, d_c, kept, d_e, group, (uint8_t*)codes, scales);
-        else
-            kv_compress_generic_kernel<4><<<grid_for(work, 256), 256, 0, st>>>(
-                (const uint16_t*)src, rows, d_c, kept, d_e, group, (uint8_t*)codes, scales);
-    }
-    EKV_CUDA(cudaGetLastError());
-    count_launches(1);
+    CompressJob j{src, codes, scales};
+    launch_kv_compress_jobs(&j, 1, rows, d_c, kept, d_e, bits, group, st);
 }
 
 // ---------------------------------------------------------------------------

@@ -408,13 +408,29 @@ def build_deep_kv(ctx: Context, context: AssembledContext, deep_match: dict, X: 
     m, H, S, d_c = cloud_k.shape
     kept, margin, _, _ = select_channels(ctx, X, WqT, cloud_k, lam, d_c)
     kept_t = torch.as_tensor(kept, device=cloud_k.device)
+    srcs, codes, scales = [], [], []
+    fmt = None
     for le, lc in sorted(deep_match.items()):
         i = cloud_layers.index(lc)
         seg = context.segment(le)
         assert seg.format in (EKV_KV_INT8, EKV_KV_INT4) and seg.S == S
-        rows = H * S
-        for src, codes, scales in ((cloud_k[i], seg.k, seg.k_scales), (cloud_v[i], seg.v, seg.v_scales)):
-            call("ekv_kv_compress", ctx.h, _ptr(src.contiguous()), rows, d_c, _ptr(kept_t),
-                 len(kept), seg.format, seg.group, C.c_void_p(codes), C.c_void_p(scales))
+        assert fmt in (None, seg.format)
+        fmt, group = seg.format, seg.group
+        srcs += [cloud_k[i].data_ptr(), cloud_v[i].data_ptr()]
+        codes += [seg.k, seg.v]
+        scales += [seg.k_scales, seg.v_scales]
+    n = len(srcs)
+    arr = lambda xs: (C.c_void_p * n)(*xs)
+    compress_batched(ctx, n, arr(srcs), H * S, d_c, kept_t, len(kept), fmt, group, arr(codes),
+                     arr(scales))
     ctx.synchronize()
     return kept, margin
+
+
+def compress_batched(ctx: Context, n: int, src_ptrs, rows: int, d_c: int, kept_t: torch.Tensor,
+                     d_e: int, bits: int, group: int, code_ptrs, scale_ptrs):
+    """K3 over n (src, codes, scales) device-pointer triples in one launch."""
+    _sync_in()
+    call("ekv_kv_compress_batched", ctx.h, n, C.cast(src_ptrs, C.POINTER(C.c_void_p)), rows, d_c,
+         _ptr(kept_t), d_e, bits, group, C.cast(code_ptrs, C.POINTER(C.c_void_p)),
+         C.cast(scale_ptrs, C.POINTER(C.c_void_p)))
