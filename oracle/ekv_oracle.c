@@ -299,18 +299,20 @@ EKVO_EXPORT void ekvo_prune_rows_bf16(const uint16_t* src, int64_t rows, int d_c
 /* ------------------------------------------------------------------------ */
 /* a8: quantise / pack / dequant.  NO REFERENCE.  This   */
 /* is the build's own contract, restated here in the exact fp32 operation   */
-/* order of kernel K3 (csrc/ekv_compress.cu):                               */
+/* order of kernel K3 (paper_2505_14085_b200/csrc/k_kvcodec.cu):            */
 /*   per row (token, head) and group of g gathered channels:                */
 /*   amax  = max |x| (fp32, x = bf16 input)                                 */
-/*   scale = amax / Q   (fp32 IEEE division, RN), Q = 127 (int8) / 7 (int4) */
-/*   code  = scale == 0 ? 0 : clamp(rint_even(x / scale), -Q, Q)            */
+/*   amax < 2^-120: the group is all-zero (scale 0, codes 0)                */
+/*   scale = RN(amax / Q), inv = RN(Q / amax), Q = 127 (int8) / 7 (int4)    */
+/*   code  = round_half_even(RN(x * inv))   (|x*inv| <= Q(1+2^-22): no clamp) */
 /*   int4: two's-complement nibbles, element 2j in the low nibble           */
-/*   dequant: bf16_rn(code * scale) computed in fp32.                       */
+/*   dequant: code * scale (exact in fp64); K6 materialises bf16_rn(fp32).  */
 /* Layout: codes [rows][d_e*bits/8], scales [rows][d_e/g] fp32.             */
 /* ------------------------------------------------------------------------ */
 EKVO_EXPORT void ekvo_kv_compress(const uint16_t* src, int64_t rows, int d_c, const int* kept,
                                   int d_e, int bits, int group, uint8_t* codes, float* scales) {
     const float Q = bits == 8 ? 127.0f : 7.0f;
+    const float tiny = 0x1.0p-120f;
     const int ng = d_e / group;
     const int row_bytes = d_e * bits / 8;
     float* x = (float*)malloc(sizeof(float) * (size_t)d_e);
@@ -324,16 +326,15 @@ EKVO_EXPORT void ekvo_kv_compress(const uint16_t* src, int64_t rows, int d_c, co
                 float a = fabsf(x[c]);
                 if (a > amax) amax = a;
             }
-            volatile float scale = amax / Q;
+            const int zero = !(amax >= tiny);
+            volatile float scale = zero ? 0.0f : amax / Q;
+            volatile float inv = zero ? 0.0f : Q / amax;
             scales[i * ng + gi] = scale;
             for (int c = gi * group; c < (gi + 1) * group; ++c) {
                 int code = 0;
-                if (scale != 0.0f) {
-                    volatile float t = x[c] / scale;
-                    float r = nearbyintf(t);
-                    if (r > Q) r = Q;
-                    if (r < -Q) r = -Q;
-                    code = (int)r;
+                if (!zero) {
+                    volatile float t = x[c] * inv;
+                    code = (int)nearbyintf(t);
                 }
                 if (bits == 8) {
                     crow[c] = (uint8_t)(int8_t)code;

@@ -36,138 +36,137 @@ void launch_fill_uniform_bf16(void* dst, int64_t n, uint64_t seed, uint64_t stre
 }
 
 // ---------------------------------------------------------------------------
-// K3 fast path: one warp per row of DC bf16 channels (row-wide coalesced
-// load, DC/32 channels per lane), gather of the DE kept channels by warp
-// shuffles, per-group absmax by shuffles, quantise, pack, coalesced store.
-// Quantiser contract (DESIGN.md s.3 / oracle ekvo_kv_compress):
-//   scale = amax / Q; code = clamp(rint(x / scale), -Q, Q); scale==0 -> 0.
+// K3: gather + quantise + pack.  Quantiser contract (DESIGN.md s.3, oracle
+// ekvo_kv_compress): per row and group, amax = max|x|; amax < 2^-120 -> zero
+// group; scale = RN(amax/Q), inv = RN(Q/amax); code = rne(RN(x*inv)).  The
+// round-half-even of the fp32 product is done with the 1.5*2^23 magic add,
+// whose low mantissa bits ARE the two's-complement code, so a code costs one
+// FMUL + one FADD + a byte select (no F2I, no clamp: |x*inv| <= Q(1+2^-22)).
 // ---------------------------------------------------------------------------
-template <int DC>
-struct RowLoad;  // lane-local slice of one row
-template <>
-struct RowLoad<64> {
-    uint32_t w[1];
-};
-template <>
-struct RowLoad<128> {
-    uint32_t w[2];
-};
-template <>
-struct RowLoad<256> {
-    uint32_t w[4];
-};
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr float kTiny = 0x1.0p-120f;
 
-template <int DC>
-__device__ __forceinline__ RowLoad<DC> load_row(const uint16_t* row, int lane) {
-    RowLoad<DC> r;
-    if constexpr (DC == 64) {
-        r.w[0] = __ldcs(reinterpret_cast<const uint32_t*>(row) + lane);
-    } else if constexpr (DC == 128) {
-        uint2 v = __ldcs(reinterpret_cast<const uint2*>(row) + lane);
-        r.w[0] = v.x;
-        r.w[1] = v.y;
-    } else {
-        uint4 v = __ldcs(reinterpret_cast<const uint4*>(row) + lane);
-        r.w[0] = v.x;
-        r.w[1] = v.y;
-        r.w[2] = v.z;
-        r.w[3] = v.w;
-    }
-    return r;
+__device__ __forceinline__ uint32_t quant_bits(float x, float inv) {
+    return __float_as_uint(__fadd_rn(__fmul_rn(x, inv), kMagic));
 }
 
-// Channel ch lives in lane ch / (DC/32), word (ch % (DC/32)) / 2, half ch & 1.
+// Tile kernel: TILE contiguous rows of one job are moved global -> shared by a
+// single bulk-async copy (TMA 1D, mbarrier completion), double-buffered, so the
+// HBM stream runs ahead of the quantisation.  8 kept channels per lane, LPR =
+// DE/8 lanes per row, 32/LPR rows per warp pass; per-group absmax by xor
+// shuffles inside the row's lanes; 8 (int8) or 4 (int4) code bytes stored per
+// lane (coalesced rows).
 template <int DC>
-__device__ __forceinline__ float fetch_channel(const RowLoad<DC>& r, int ch) {
-    constexpr int EPL = DC / 32;  // elements per lane
-    const int src = ch / EPL;
-    const int wsel = (ch % EPL) >> 1;
-    uint32_t got = 0;
-#pragma unroll
-    for (int k = 0; k < EPL / 2; ++k) {
-        uint32_t v = __shfl_sync(0xffffffffu, r.w[k], src);
-        if (k == wsel) got = v;
-    }
-    return (ch & 1) ? bf16_hi(got) : bf16_lo(got);
+struct TileCfg {
+    static constexpr int TILE = 8192 / DC;              // rows per stage (16 KB)
+    static constexpr int BYTES = TILE * DC * 2;         // 16 KB
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 template <int DC, int DE, int BITS>
-__global__ void __launch_bounds__(256) kv_compress_fast_kernel(CompressJobs jobs, int64_t rows,
+__global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs, int64_t rows,
                                                                const int* __restrict__ kept,
                                                                int group) {
-    // one job (layer x {K, V}) per blockIdx.y: a single launch compresses every deep layer
-    const uint16_t* __restrict__ src = (const uint16_t*)jobs.job[blockIdx.y].src;
-    uint8_t* __restrict__ codes = (uint8_t*)jobs.job[blockIdx.y].codes;
-    float* __restrict__ scales = jobs.job[blockIdx.y].scales;
-    constexpr int EPL = DE / 32;  // kept channels per lane (1, 2 or 4)
+    using TC = TileCfg<DC>;
+    constexpr int LPR = DE / 8, RPW = 32 / LPR, NWARP = 4;
+    constexpr int PASSES = TC::TILE / (RPW * NWARP);
     constexpr float Q = BITS == 8 ? 127.0f : 7.0f;
-    const int lane = threadIdx.x & 31;
+    static_assert(PASSES >= 1 && TC::TILE % (RPW * NWARP) == 0, "tile shape");
+    __shared__ __align__(128) uint8_t buf[2][TC::BYTES];
+    __shared__ __align__(8) uint64_t bar[2];
+    const CompressJob job = jobs.job[blockIdx.y];
+    const uint8_t* src = (const uint8_t*)job.src;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane % LPR, rsub = lane / LPR;
+    const int glanes = group / 8;  // lanes per group (power of two, <= LPR)
     const int ng = DE / group;
-    const int glanes = group / EPL;  // lanes per group (power of two)
-    int ch[EPL];
+    int ch2[8];  // byte offsets of my kept channels inside a row
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) ch[e] = kept[lane * EPL + e];
-    const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    constexpr int UNROLL = 4;
-    for (int64_t base = warp0 * UNROLL; base < rows; base += nwarps * UNROLL) {
-        RowLoad<DC> rl[UNROLL];
+    for (int e = 0; e < 8; ++e) ch2[e] = 2 * kept[sub * 8 + e];
+    const int64_t ntiles = (rows + TC::TILE - 1) / TC::TILE;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int64_t t, int stage) {
+        const int64_t r0 = t * TC::TILE;
+        const int n = (int)min((int64_t)TC::TILE, rows - r0);
+        const uint32_t bytes = (uint32_t)n * DC * 2;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_addr(&bar[stage])),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(buf[stage])),
+            "l"(src + r0 * DC * 2), "r"(bytes), "r"(smem_addr(&bar[stage]))
+            : "memory");
+    };
+    int64_t t = blockIdx.x;
+    if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
+    uint32_t phase[2] = {0, 0};
+    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
+        const int stage = it & 1;
+        const int64_t tn = t + gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles) issue(tn, stage ^ 1);  // next tile in flight
+        // wait for this tile
+        {
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n\t}"
+                    : "=r"(done)
+                    : "r"(smem_addr(&bar[stage])), "r"(phase[stage])
+                    : "memory");
+            }
+            phase[stage] ^= 1;
+        }
+        const int64_t r0 = t * TC::TILE;
+        const uint8_t* tile = buf[stage];
 #pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-            if (base + u < rows) rl[u] = load_row<DC>(src + (base + u) * DC, lane);
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const int64_t row = base + u;
-            if (row >= rows) break;
-            float x[EPL];
+        for (int p = 0; p < PASSES; ++p) {
+            const int lr = (p * NWARP + warp) * RPW + rsub;
+            const int64_t row = r0 + lr;
+            const uint8_t* rp = tile + lr * (DC * 2);
+            float x[8];
             float amax = 0.0f;
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                x[e] = fetch_channel<DC>(rl[u], ch[e]);
+            for (int e = 0; e < 8; ++e) {
+                x[e] = __uint_as_float((uint32_t)(*(const uint16_t*)(rp + ch2[e])) << 16);
                 amax = fmaxf(amax, fabsf(x[e]));
             }
             for (int o = glanes >> 1; o > 0; o >>= 1)
                 amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            const float scale = __fdiv_rn(amax, Q);
-            int code[EPL];
+            const bool zero = !(amax >= kTiny);
+            const float scale = zero ? 0.0f : __fdiv_rn(amax, Q);
+            const float inv = zero ? 0.0f : __fdiv_rn(Q, amax);
+            uint32_t q[8];
 #pragma unroll
-            for (int e = 0; e < EPL; ++e) {
-                int c = 0;
-                if (scale != 0.0f) {
-                    float r = rintf(__fdiv_rn(x[e], scale));
-                    r = fminf(fmaxf(r, -Q), Q);
-                    c = (int)r;
-                }
-                code[e] = c;
-            }
-            if ((lane % glanes) == 0) scales[row * ng + lane / glanes] = scale;
-            if constexpr (BITS == 8) {
-                uint8_t* crow = codes + row * DE;
-                if constexpr (EPL == 1) {
-                    crow[lane] = (uint8_t)code[0];
-                } else if constexpr (EPL == 2) {
-                    reinterpret_cast<uint16_t*>(crow)[lane] =
-                        (uint16_t)((code[0] & 0xFF) | ((code[1] & 0xFF) << 8));
+            for (int e = 0; e < 8; ++e) q[e] = zero ? 0u : quant_bits(x[e], inv);
+            if (row < rows) {
+                if ((sub % glanes) == 0) job.scales[row * ng + sub / glanes] = scale;
+                if constexpr (BITS == 8) {
+                    const uint32_t lo = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
+                                                    __byte_perm(q[2], q[3], 0x0040), 0x5410);
+                    const uint32_t hi = __byte_perm(__byte_perm(q[4], q[5], 0x0040),
+                                                    __byte_perm(q[6], q[7], 0x0040), 0x5410);
+                    reinterpret_cast<uint2*>((uint8_t*)job.codes + row * DE)[sub] = make_uint2(lo, hi);
                 } else {
-                    reinterpret_cast<uint32_t*>(crow)[lane] =
-                        (uint32_t)((code[0] & 0xFF) | ((code[1] & 0xFF) << 8) |
-                                   ((code[2] & 0xFF) << 16) | ((uint32_t)(code[3] & 0xFF) << 24));
-                }
-            } else {
-                uint8_t* crow = codes + row * (DE / 2);
-                if constexpr (EPL == 1) {
-                    // pair lanes (2j, 2j+1) into one byte
-                    int other = __shfl_down_sync(0xffffffffu, code[0], 1);
-                    if ((lane & 1) == 0) crow[lane >> 1] = (uint8_t)((code[0] & 0xF) | ((other & 0xF) << 4));
-                } else if constexpr (EPL == 2) {
-                    crow[lane] = (uint8_t)((code[0] & 0xF) | ((code[1] & 0xF) << 4));
-                } else {
-                    reinterpret_cast<uint16_t*>(crow)[lane] =
-                        (uint16_t)((code[0] & 0xF) | ((code[1] & 0xF) << 4) | ((code[2] & 0xF) << 8) |
-                                   ((code[3] & 0xF) << 12));
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) w |= (q[e] & 0xFu) << (4 * e);
+                    reinterpret_cast<uint32_t*>((uint8_t*)job.codes + row * (DE / 2))[sub] = w;
                 }
             }
         }
+        __syncthreads();  // every warp is done with this stage before it is refilled
     }
 }
 
@@ -188,21 +187,19 @@ __global__ void kv_compress_generic_kernel(const uint16_t* __restrict__ src, int
         float amax = 0.0f;
         for (int c = g * group; c < (g + 1) * group; ++c)
             amax = fmaxf(amax, fabsf(__uint_as_float((uint32_t)s[kept[c]] << 16)));
-        const float scale = __fdiv_rn(amax, Q);
+        const bool zero = !(amax >= kTiny);
+        const float scale = zero ? 0.0f : __fdiv_rn(amax, Q);
+        const float inv = zero ? 0.0f : __fdiv_rn(Q, amax);
         scales[row * ng + g] = scale;
         uint8_t* crow = codes + row * row_bytes;
         for (int c = g * group; c < (g + 1) * group; ++c) {
-            int code = 0;
-            if (scale != 0.0f) {
-                float r = rintf(__fdiv_rn(__uint_as_float((uint32_t)s[kept[c]] << 16), scale));
-                code = (int)fminf(fmaxf(r, -Q), Q);
-            }
+            const uint32_t q = zero ? 0u : quant_bits(__uint_as_float((uint32_t)s[kept[c]] << 16), inv);
             if (BITS == 8) {
-                crow[c] = (uint8_t)code;
+                crow[c] = (uint8_t)(q & 0xFF);
             } else if ((c & 1) == 0) {
-                crow[c >> 1] = (uint8_t)(code & 0xF);  // low nibble first
+                crow[c >> 1] = (uint8_t)(q & 0xF);  // low nibble first
             } else {
-                crow[c >> 1] |= (uint8_t)((code & 0xF) << 4);
+                crow[c >> 1] |= (uint8_t)((q & 0xF) << 4);
             }
         }
     }
@@ -220,15 +217,19 @@ template <int DC, int DE, int BITS>
 static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c, const int* kept,
                      int d_e, int group, cudaStream_t st) {
     if (d_c != DC || d_e != DE) return false;
-    constexpr int EPL = DE / 32;
-    if (group % EPL != 0) return false;
-    const int gl = group / EPL;
-    if (gl < 1 || gl > 32 || (gl & (gl - 1))) return false;
-    const int64_t warps = (rows + 3) / 4;
-    int bx = grid_for(warps * 32, 256);
-    const int cap = (148 * 8 + n_jobs - 1) / n_jobs;  // ~8 CTAs per SM over all jobs
-    if (bx > cap) bx = cap < 1 ? 1 : cap;
-    kv_compress_fast_kernel<DC, DE, BITS><<<dim3(bx, n_jobs), 256, 0, st>>>(jobs, rows, kept, group);
+    constexpr int LPR = DE / 8;
+    if (group % 8 != 0) return false;
+    const int gl = group / 8;
+    if (gl < 1 || gl > LPR || (gl & (gl - 1))) return false;
+    for (int i = 0; i < n_jobs; ++i)  // bulk copies need 16-byte aligned sources
+        if (((uintptr_t)jobs.job[i].src & 15) || ((uintptr_t)jobs.job[i].codes & 7))
+            return false;
+    const int64_t tiles = (rows + TileCfg<DC>::TILE - 1) / TileCfg<DC>::TILE;
+    int64_t bx = (148 * 12 + n_jobs - 1) / n_jobs;  // ~12 CTAs (2 tiles each in flight) per SM
+    if (bx > tiles) bx = tiles;
+    if (bx < 1) bx = 1;
+    kv_compress_tile_kernel<DC, DE, BITS><<<dim3((unsigned)bx, n_jobs), 128, 0, st>>>(jobs, rows, kept,
+                                                                                 group);
     return true;
 }
 
