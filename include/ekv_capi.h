@@ -246,10 +246,16 @@ int ekv_session_forward(ekv_session_t s, const float* emb_dev, int n, float* out
  * row (collaborative_decode loop, cache_merge.cpp:256-271).  Outputs fp32
  * [steps][h] on the device.  Replays one captured CUDA graph per step. */
 int ekv_session_decode(ekv_session_t s, int steps, float* out_dev);
+/* Decode implementation: 0 = one persistent kernel per step (k_decode_mega.cu,
+ * default when the shape allows: S % 16 == 0, h <= 2048, <= 64 layers),
+ * 1 = the per-layer kernels (K5, K4, K5) replayed from a CUDA graph.
+ * active (optional) receives the path that will actually run. */
+int ekv_session_set_decode_path(ekv_session_t s, int path, int* active);
 /* One decode step launched kernel by kernel with CUDA events between the
  * launches (diagnostics / roofline attribution; the step is real and advances
- * the session).  kernel_ms[3l+0] = layer l QKV projection, [3l+1] = decode
- * attention, [3l+2] = output projection, [3L] = state advance. */
+ * the session).  Graph path: kernel_ms[3l+0] = layer l QKV projection,
+ * [3l+1] = decode attention, [3l+2] = output projection, [3L] = state advance.
+ * Persistent path: kernel_ms[0] = the whole step (one kernel). */
 int ekv_session_profile_step(ekv_session_t s, float* kernel_ms, int capacity, int* n_kernels);
 /* Device pointer of the user cache of one layer (bf16 [H][cap][d]). */
 int ekv_session_user_kv(ekv_session_t s, int layer, void** k_dev, void** v_dev, int* cap);

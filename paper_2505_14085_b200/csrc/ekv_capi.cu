@@ -12,6 +12,7 @@
 
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
+#include "ekv_mega.h"
 
 namespace ekv {
 
@@ -108,6 +109,12 @@ struct ekv_session_s {
     int steps = 0;                 // host mirror of state->step
     cudaGraphExec_t step_graph = nullptr;
     int64_t graph_kernels = 0;
+    // persistent decode-step kernel (k_decode_mega.cu)
+    int path = 0;                  // 0 = megakernel when supported, 1 = per-layer graph
+    bool mega_ok = false;
+    float* mega_ws = nullptr;
+    unsigned* mega_sync = nullptr;  // [H] head counters + 2 barrier words
+    MegaArgs mega{};
     size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
 };
 
@@ -235,6 +242,49 @@ void session_alloc(ekv_session_s* s) {
         ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim, s->cap));
     s->ws = dalloc<float>(ws);
     s->counters = dalloc<unsigned>((size_t)8 * m->cfg.num_heads);
+    {
+        const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = m->cfg.head_dim;
+        const char* env = getenv("EKV_DECODE_PATH");
+        if (env && std::string(env) == "graph") s->path = 1;
+        s->mega_ok = mega_supported(L, H, D, s->kv->S, m->h);
+        if (s->mega_ok) {
+            const int G = m->ctx->num_sms;
+            s->mega_ws = dalloc<float>((size_t)G * 4 * (D + 2));
+            s->mega_sync = dalloc<unsigned>((size_t)H + 2);
+            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * (H + 2)));
+            MegaArgs& a = s->mega;
+            a.L = L;
+            a.H = H;
+            a.D = D;
+            a.S = s->kv->S;
+            a.cap = s->cap;
+            a.gamma = m->gamma;
+            a.bias = m->bias;
+            a.pos = m->pos;
+            a.state = s->state;
+            a.x = s->xa;
+            a.q = s->q;
+            a.concat = s->xb;
+            a.hist = s->hist;
+            a.ws = s->mega_ws;
+            a.head_ctr = s->mega_sync;
+            a.bar = s->mega_sync + H;
+            for (int l = 0; l < L; ++l) {
+                const ekv_segment& sg = s->kv->seg[l];
+                MegaLayer& ly = a.layer[l];
+                ly.wqkv = m->wqkvT(l);
+                ly.wo = m->woT(l);
+                ly.fmt = sg.S > 0 ? sg.format : EKV_KV_BF16;
+                ly.group = sg.group > 0 ? sg.group : D;
+                ly.ck = (const uint8_t*)sg.k;
+                ly.cv = (const uint8_t*)sg.v;
+                ly.cks = sg.k_scales;
+                ly.cvs = sg.v_scales;
+                ly.uk = s->uk + (size_t)l * s->ukv_layer();
+                ly.uv = s->uv + (size_t)l * s->ukv_layer();
+            }
+        }
+    }
     EKV_CUDA(cudaMemset(s->counters, 0, sizeof(unsigned) * 8 * m->cfg.num_heads));
     EKV_CUDA(cudaMemset(s->state, 0, sizeof(DevState)));
     EKV_CUDA(cudaMemset(s->uk, 0, sizeof(uint16_t) * L * s->ukv_layer()));
@@ -297,10 +347,18 @@ void ensure_step_graph(ekv_session_s* s) {
     g_launches -= s->graph_kernels;  // capture launched nothing; replays are counted
 }
 
+bool use_mega(const ekv_session_s* s) { return s->mega_ok && s->path == 0; }
+
 void session_decode(ekv_session_s* s, int steps, cudaStream_t st) {
     require(steps >= 1, "collaborative_decode: steps must be >= 1");
     check_overflow(s, steps);
     require(s->steps + steps <= s->cap, "decode history full");
+    if (use_mega(s)) {
+        for (int t = 0; t < steps; ++t) launch_decode_mega(s->mega, s->model->ctx->num_sms, st);
+        s->user_len += steps;
+        s->steps += steps;
+        return;
+    }
     ensure_step_graph(s);
     for (int t = 0; t < steps; ++t) EKV_CUDA(cudaGraphLaunch(s->step_graph, st));
     count_launches(s->graph_kernels * steps);
@@ -1009,9 +1067,18 @@ int ekv_session_destroy(ekv_session_t s) {
         if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
         for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                         (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
-                        (void*)s->ws, (void*)s->counters})
+                        (void*)s->ws, (void*)s->counters, (void*)s->mega_ws, (void*)s->mega_sync})
             cudaFree(p);
         delete s;
+    });
+}
+
+int ekv_session_set_decode_path(ekv_session_t s, int path, int* active) {
+    return guard([&] {
+        require(s != nullptr, "null session");
+        require(path == 0 || path == 1, "decode path must be 0 (persistent kernel) or 1 (graph)");
+        s->path = path;
+        if (active) *active = use_mega(s) ? 0 : 1;
     });
 }
 
@@ -1060,7 +1127,7 @@ int ekv_session_decode(ekv_session_t s, int steps, float* out) {
 int ekv_session_profile_step(ekv_session_t s, float* kernel_ms, int capacity, int* n_kernels) {
     return guard([&] {
         require(s && kernel_ms && n_kernels, "ekv_session_profile_step: null argument");
-        const int n = 3 * s->model->cfg.num_layers + 1;
+        const int n = use_mega(s) ? 1 : 3 * s->model->cfg.num_layers + 1;
         require(capacity >= n, "ekv_session_profile_step: need room for " + std::to_string(n) +
                                    " kernel times");
         check_overflow(s, 1);
@@ -1069,6 +1136,22 @@ int ekv_session_profile_step(ekv_session_t s, float* kernel_ms, int capacity, in
         cudaStream_t st = s->model->ctx->stream;
         if (s->user_len == 0 && s->steps == 0)
             EKV_CUDA(cudaMemsetAsync(s->xa, 0, sizeof(float) * s->model->h, st));
+        if (use_mega(s)) {
+            cudaEvent_t e0, e1;
+            EKV_CUDA(cudaEventCreate(&e0));
+            EKV_CUDA(cudaEventCreate(&e1));
+            EKV_CUDA(cudaEventRecord(e0, st));
+            launch_decode_mega(s->mega, s->model->ctx->num_sms, st);
+            EKV_CUDA(cudaEventRecord(e1, st));
+            EKV_CUDA(cudaEventSynchronize(e1));
+            EKV_CUDA(cudaEventElapsedTime(&kernel_ms[0], e0, e1));
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            s->user_len += 1;
+            s->steps += 1;
+            *n_kernels = 1;
+            return;
+        }
         std::vector<cudaEvent_t> ev(n + 1);
         for (auto& e : ev) EKV_CUDA(cudaEventCreate(&e));
         try {

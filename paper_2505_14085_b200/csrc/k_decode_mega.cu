@@ -1,0 +1,719 @@
+// The decode step as ONE persistent kernel (batch-1 collaborative decode).
+//
+// merged_forward (cache_merge.cpp:156-226) for one new row, all layers:
+//   P1  QKV projection of the layer input (input transform fused at layer 0),
+//       K/V appended to the session's user cache
+//   P2  segment attention over the reused context + causal user segment,
+//       merged by the Eq. 5 normaliser rule (cache_merge.cpp:12-80)
+//   P3  output projection -> next layer's input (history row at the last layer)
+// separated by grid-wide barriers (one CTA per SM, cooperative launch).
+//
+// Why one kernel: at batch 1 every phase is a few microseconds of HBM traffic
+// (25 MB QKV, 8 MB out-proj, 9-17 MB of context per layer), so separate
+// kernels spend most of their time ramping up and draining.  Here every byte
+// that does not depend on the running activations -- all weights and all
+// context K/V -- is streamed by a dedicated producer warp with bulk-async
+// copies (TMA 1-D, mbarrier completion) into a 3-stage shared-memory ring, in
+// exactly the order the consumer warps will use it, across phase and layer
+// boundaries.  The producer never waits on the grid barriers, so HBM keeps
+// streaming while the consumers synchronise.  Only the small dynamic data
+// (x, q, the user rows, partials) moves through L2 with ld.global.cg.
+//
+// Work split (static, identical on every CTA): P1 rows [c*3h/G, (c+1)*3h/G),
+// P3 rows [c*h/G, ...); P2 splits the flattened (head, 16-row unit) space of
+// context ++ user rows evenly, so a CTA touches at most two heads; each head's
+// partials (m, l, o) are merged by the last CTA to finish it (atomic counter).
+#include <math_constants.h>
+
+#include "ekv_common.cuh"
+#include "ekv_kernels.h"
+#include "ekv_mega.h"
+
+namespace ekv {
+
+namespace mk {
+
+constexpr int NCW = 16;                 // consumer warps
+constexpr int THREADS = (NCW + 1) * 32; // + 1 producer warp
+constexpr int NST = 3;                  // ring stages
+constexpr int STAGE = 64 * 1024;        // bytes per stage
+constexpr int UNIT = 16;                // attention rows per partition unit
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(saddr(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 4000000000ll) __trap();
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
+}
+
+// Sense-reversing grid barrier over the consumer warps of every CTA.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G) {
+    consumers_sync();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned my = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == G - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            const long long t0 = clock64();
+            while (*gen == my) {
+                __nanosleep(32);
+                if (clock64() - t0 > 4000000000ll) __trap();
+            }
+        }
+        __threadfence();
+    }
+    consumers_sync();
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic schedule shared by producer and consumers.
+// ---------------------------------------------------------------------------
+struct Split {
+    int r0, r1;
+};
+__device__ __forceinline__ Split rows_of(int c, int G, int N) {
+    return Split{(int)((long long)c * N / G), (int)((long long)(c + 1) * N / G)};
+}
+
+// One CTA's attention work for one head: context rows [c0, c1) (through the
+// ring) and user rows [u0, u1) (direct loads).
+struct Piece {
+    int head, c0, c1, u0, u1, slot;
+};
+
+struct AttnPlan {
+    int n;
+    Piece p[2];
+};
+
+__device__ __forceinline__ int ctx_units(int S) { return (S + UNIT - 1) / UNIT; }
+
+__device__ __forceinline__ AttnPlan plan_attention(int c, int G, int H, int S, int nuser) {
+    const int cu = ctx_units(S), uu = (nuser + UNIT - 1) / UNIT, per = cu + uu;
+    const long long TU = (long long)H * per;
+    const long long a = (long long)c * TU / G, b = (long long)(c + 1) * TU / G;
+    AttnPlan pl;
+    pl.n = 0;
+    for (long long u = a; u < b;) {
+        const int h = (int)(u / per);
+        const long long hend = (long long)(h + 1) * per;
+        const long long e = b < hend ? b : hend;
+        const int lo = (int)(u - (long long)h * per), hi = (int)(e - (long long)h * per);  // units
+        Piece pc;
+        pc.head = h;
+        pc.c0 = min(lo, cu) * UNIT;
+        pc.c1 = min(min(hi, cu) * UNIT, S);
+        pc.u0 = max(lo - cu, 0) * UNIT;
+        pc.u1 = min(max(hi - cu, 0) * UNIT, nuser);
+        pc.slot = pl.n;
+        pl.p[pl.n++] = pc;
+        u = e;
+    }
+    return pl;
+}
+
+// number of CTAs whose unit range intersects head h (the merge fan-in)
+__device__ __forceinline__ int owner(long long unit, int G, long long TU) {
+    // largest c with floor(c*TU/G) <= unit
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((long long)mid * TU / G <= unit) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int D, int FMT>
+struct Fmt {
+    static constexpr int ROW = FMT == 16 ? D * 2 : (FMT == 8 ? D : D / 2);  // bytes per row
+    static constexpr int LPR = ROW / 16;
+    static constexpr int EPL = D / LPR;
+    static constexpr int RPP = 32 / LPR;
+};
+
+__device__ __forceinline__ int att_stage_rows(int row_bytes, int ng) {
+    const int per = 2 * (row_bytes + ng * 4);
+    int r = STAGE / per;
+    r -= r % UNIT;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// expand 16 bytes of K/V into floats (same encoding as k_attn.cu)
+// ---------------------------------------------------------------------------
+template <int FMT>
+__device__ __forceinline__ void expand16(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (FMT == 16) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            f[2 * k] = bf16_lo(w[k]);
+            f[2 * k + 1] = bf16_hi(w[k]);
+        }
+    } else if constexpr (FMT == 8) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t u = w[k] ^ 0x80808080u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                f[4 * k + b] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7440 + b)) - 8388736.0f;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t lo = (w[k] & 0x0F0F0F0Fu) ^ 0x08080808u;
+            const uint32_t hi = ((w[k] >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                f[8 * k + 2 * b] = __uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7440 + b)) - 8388616.0f;
+                f[8 * k + 2 * b + 1] = __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7440 + b)) - 8388616.0f;
+            }
+        }
+    }
+}
+
+// Online-softmax state of one lane group (the LPR lanes of one row subgroup).
+template <int EPL>
+struct OState {
+    float m, l, o[EPL];
+};
+
+template <int EPL>
+__device__ __forceinline__ void ostate_init(OState<EPL>& s) {
+    s.m = -CUDART_INF_F;
+    s.l = 0.0f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) s.o[e] = 0.0f;
+}
+
+// absorb one row: logit x, value row f (already scaled by its dequant scale)
+template <int EPL>
+__device__ __forceinline__ void ostate_add(OState<EPL>& s, float x, const float* f, float vscale) {
+    const float mn = fmaxf(s.m, x);
+    const float corr = exp2f((s.m - mn) * kLog2e);  // exp(-inf) = 0 on the first row
+    const float p = exp2f((x - mn) * kLog2e);
+    s.l = s.l * corr + p;
+    const float pv = p * vscale;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) s.o[e] = fmaf(pv, f[e], s.o[e] * corr);
+    s.m = mn;
+}
+
+template <int EPL>
+__device__ __forceinline__ void ostate_merge_from(OState<EPL>& s, float m2, float l2, const float* o2) {
+    const float mn = fmaxf(s.m, m2);
+    if (mn == -CUDART_INF_F) return;
+    const float a = exp2f((s.m - mn) * kLog2e), b = exp2f((m2 - mn) * kLog2e);
+    s.l = s.l * a + l2 * b;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) s.o[e] = s.o[e] * a + o2[e] * b;
+    s.m = mn;
+}
+
+// ---------------------------------------------------------------------------
+// The kernel
+// ---------------------------------------------------------------------------
+template <int D>
+struct Smem {
+    uint8_t ring[NST][STAGE];
+    uint64_t full[NST];
+    uint64_t empty[NST];
+    float red_m[NCW][32 / 1];  // per warp, per row-subgroup m (max 32 subgroups)
+    float red_l[NCW][32];
+    float red_o[NCW][D];
+    float red_wm[NCW], red_wl[NCW];
+    int s_last;
+};
+
+template <int D>
+__device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int nuser) {
+    int stage = 0;
+    uint32_t phase = 0;
+    const int h = a.H * D;
+    auto next = [&](int bytes_total) {
+        mbar_wait(&sm.empty[stage], phase ^ 1);
+        mbar_expect(&sm.full[stage], (uint32_t)bytes_total);
+    };
+    auto advance = [&] {
+        if (++stage == NST) {
+            stage = 0;
+            phase ^= 1;
+        }
+    };
+    const Split q = rows_of(c, G, 3 * h), o = rows_of(c, G, h);
+    const AttnPlan pl = plan_attention(c, G, a.H, a.S, nuser);
+    const int rows_per_w = STAGE / (h * 2);  // weight rows per stage
+    for (int l = 0; l < a.L; ++l) {
+        const MegaLayer& ly = a.layer[l];
+        for (int r = q.r0; r < q.r1; r += rows_per_w) {
+            const int n = min(rows_per_w, q.r1 - r);
+            next(n * h * 2);
+            bulk_g2s(sm.ring[stage], ly.wqkv + (size_t)r * h, n * h * 2, &sm.full[stage]);
+            advance();
+        }
+        const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
+        const int ng = ly.fmt == 16 ? 0 : D / ly.group;
+        const int cap = att_stage_rows(row_b, ng);
+        for (int i = 0; i < pl.n; ++i) {
+            const Piece& pc = pl.p[i];
+            for (int r = pc.c0; r < pc.c1; r += cap) {
+                const int n = min(cap, pc.c1 - r);
+                const size_t base = (size_t)pc.head * a.S + r;
+                const int kb = n * row_b, sb = n * ng * 4;
+                next(2 * (kb + sb));
+                uint8_t* dst = sm.ring[stage];
+                bulk_g2s(dst, ly.ck + base * row_b, kb, &sm.full[stage]);
+                bulk_g2s(dst + kb, ly.cv + base * row_b, kb, &sm.full[stage]);
+                if (ng) {
+                    bulk_g2s(dst + 2 * kb, ly.cks + base * ng, sb, &sm.full[stage]);
+                    bulk_g2s(dst + 2 * kb + sb, ly.cvs + base * ng, sb, &sm.full[stage]);
+                }
+                advance();
+            }
+        }
+        for (int r = o.r0; r < o.r1; r += rows_per_w) {
+            const int n = min(rows_per_w, o.r1 - r);
+            next(n * h * 2);
+            bulk_g2s(sm.ring[stage], ly.wo + (size_t)r * h, n * h * 2, &sm.full[stage]);
+            advance();
+        }
+    }
+}
+
+// consumer-side ring cursor
+struct Cursor {
+    int stage = 0;
+    uint32_t phase = 0;
+};
+
+template <int D>
+__device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, Cursor& cu) {
+    mbar_wait(&sm.full[cu.stage], cu.phase);
+    return sm.ring[cu.stage];
+}
+template <int D>
+__device__ __forceinline__ void ring_release(Smem<D>& sm, Cursor& cu) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[cu.stage]);
+    if (++cu.stage == NST) {
+        cu.stage = 0;
+        cu.phase ^= 1;
+    }
+}
+
+// y[n] = sum_k x[k] W[n][k] for the CTA's rows, weights from the ring.
+// x is in registers: lane holds x[c*256 + lane*8 + e].
+template <int D, int KC, class Epi>
+__device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, int h,
+                                          const float* xr, Epi epi) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows_per_w = STAGE / (h * 2);
+    for (int r = rows.r0; r < rows.r1; r += rows_per_w) {
+        const int n = min(rows_per_w, rows.r1 - r);
+        const uint8_t* st = ring_acquire(sm, cu);
+        for (int i = warp; i < n; i += NCW) {
+            const uint16_t* w = (const uint16_t*)(st + (size_t)i * h * 2);
+            float acc = 0.0f;
+#pragma unroll
+            for (int c = 0; c < KC; ++c) {
+                const uint4 v = *reinterpret_cast<const uint4*>(w + c * 256 + lane * 8);
+                const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    acc = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], acc);
+                    acc = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], acc);
+                }
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) epi(r + i, acc);
+        }
+        ring_release(sm, cu);
+    }
+}
+
+// Attention of q over rows held in a ring stage (context) or in global memory
+// (user rows), accumulated into this lane's online-softmax state.
+template <int D, int FMT>
+__device__ __forceinline__ void attend_stage(const uint8_t* kb, const uint8_t* vb, const float* ks,
+                                             const float* vs, int ng, int group, int n,
+                                             const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
+                                             bool global_src) {
+    using F = Fmt<D, FMT>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane % F::LPR, rsub = lane / F::LPR;
+    const int grp = FMT == 16 ? 0 : (sub * F::EPL) / group;
+    for (int base = warp * F::RPP; base < n; base += NCW * F::RPP) {
+        const int row = base + rsub;
+        const bool ok = row < n;
+        uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+        float ksc = 1.0f, vsc = 1.0f;
+        if (ok) {
+            const uint8_t* kp = kb + (size_t)row * F::ROW + sub * 16;
+            const uint8_t* vp = vb + (size_t)row * F::ROW + sub * 16;
+            if (global_src) {
+                kv = __ldcg(reinterpret_cast<const uint4*>(kp));
+                vv = __ldcg(reinterpret_cast<const uint4*>(vp));
+            } else {
+                kv = *reinterpret_cast<const uint4*>(kp);
+                vv = *reinterpret_cast<const uint4*>(vp);
+            }
+            if constexpr (FMT != 16) {
+                ksc = ks[(size_t)row * ng + grp];
+                vsc = vs[(size_t)row * ng + grp];
+            }
+        }
+        float f[F::EPL];
+        expand16<FMT>(kv, f);
+        float dot = 0.0f;
+#pragma unroll
+        for (int e = 0; e < F::EPL; ++e) dot = fmaf(qreg[e], f[e], dot);
+        dot *= ksc;
+#pragma unroll
+        for (int o = F::LPR >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (ok) {
+            expand16<FMT>(vv, f);
+            ostate_add<F::EPL>(st, dot, f, vsc);
+        }
+    }
+}
+
+// Combine the lane-group states of all consumer warps into one partial
+// (m, l, o[D]) and write it to the workspace slot.
+template <int D, int FMT>
+__device__ __forceinline__ void finish_piece(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& st, float* out) {
+    using F = Fmt<D, FMT>;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sub = lane % F::LPR;
+    // merge the row subgroups inside the warp (xor over the subgroup lane bits)
+    for (int off = F::LPR; off < 32; off <<= 1) {
+        float o2[F::EPL];
+        const float m2 = __shfl_xor_sync(0xffffffffu, st.m, off);
+        const float l2 = __shfl_xor_sync(0xffffffffu, st.l, off);
+#pragma unroll
+        for (int e = 0; e < F::EPL; ++e) o2[e] = __shfl_xor_sync(0xffffffffu, st.o[e], off);
+        ostate_merge_from<F::EPL>(st, m2, l2, o2);
+    }
+    if (lane < F::LPR) {
+#pragma unroll
+        for (int e = 0; e < F::EPL; ++e) sm.red_o[warp][sub * F::EPL + e] = st.o[e];
+        if (lane == 0) {
+            sm.red_wm[warp] = st.m;
+            sm.red_wl[warp] = st.l;
+        }
+    }
+    consumers_sync();
+    if (threadIdx.x < D) {
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < NCW; ++w) M = fmaxf(M, sm.red_wm[w]);
+        float Ls = 0.0f, O = 0.0f;
+        if (M != -CUDART_INF_F) {
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) {
+                const float s = exp2f((sm.red_wm[w] - M) * kLog2e);
+                Ls += sm.red_wl[w] * s;
+                O += sm.red_o[w][threadIdx.x] * s;
+            }
+        }
+        out[2 + threadIdx.x] = O;
+        if (threadIdx.x == 0) {
+            out[0] = M;
+            out[1] = Ls;
+        }
+    }
+    consumers_sync();
+}
+
+template <int D, int FMT>
+__device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
+                                                Cursor& cu, const AttnPlan& pl, int c, int G,
+                                                int nuser) {
+    using F = Fmt<D, FMT>;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % F::LPR;
+    const int ng = FMT == 16 ? 0 : D / ly.group;
+    const int cap = att_stage_rows(F::ROW, ng);
+    for (int i = 0; i < pl.n; ++i) {
+        const Piece& pc = pl.p[i];
+        float qreg[F::EPL];
+#pragma unroll
+        for (int e = 0; e < F::EPL; ++e) qreg[e] = __ldcg(a.q + pc.head * D + sub * F::EPL + e);
+        OState<F::EPL> st;
+        ostate_init<F::EPL>(st);
+        for (int r = pc.c0; r < pc.c1; r += cap) {
+            const int n = min(cap, pc.c1 - r);
+            const uint8_t* s = ring_acquire(sm, cu);
+            const int kbytes = n * F::ROW;
+            attend_stage<D, FMT>(s, s + kbytes, (const float*)(s + 2 * kbytes),
+                                 (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n, qreg,
+                                 st, false);
+            ring_release(sm, cu);
+        }
+        if (pc.u1 > pc.u0) {
+            // user rows: bf16, written by P1 of this layer -> coherent loads
+            using FU = Fmt<D, 16>;
+            float qu[FU::EPL];
+            const int subu = lane % FU::LPR;
+#pragma unroll
+            for (int e = 0; e < FU::EPL; ++e) qu[e] = __ldcg(a.q + pc.head * D + subu * FU::EPL + e);
+            OState<FU::EPL> su;
+            ostate_init<FU::EPL>(su);
+            const uint8_t* kbase = (const uint8_t*)(ly.uk + ((size_t)pc.head * a.cap + pc.u0) * D);
+            const uint8_t* vbase = (const uint8_t*)(ly.uv + ((size_t)pc.head * a.cap + pc.u0) * D);
+            attend_stage<D, 16>(kbase, vbase, nullptr, nullptr, 0, D, pc.u1 - pc.u0, qu, su, true);
+            // fold the user state into the context state through the workspace
+            float* tmp = a.ws + ((size_t)c * 4 + 2 + i) * (D + 2);
+            finish_piece<D, 16>(sm, su, tmp);
+            // merge the context partial with the user partial
+            float* outp = a.ws + ((size_t)c * 4 + i) * (D + 2);
+            finish_piece<D, FMT>(sm, st, outp);
+            if (threadIdx.x < D) {
+                const float m1 = outp[0], l1 = outp[1], m2 = tmp[0], l2 = tmp[1];
+                const float M = fmaxf(m1, m2);
+                const float s1 = (l1 > 0.0f) ? exp2f((m1 - M) * kLog2e) : 0.0f;
+                const float s2 = (l2 > 0.0f) ? exp2f((m2 - M) * kLog2e) : 0.0f;
+                const float o = outp[2 + threadIdx.x] * s1 + tmp[2 + threadIdx.x] * s2;
+                consumers_sync();
+                outp[2 + threadIdx.x] = o;
+                if (threadIdx.x == 0) {
+                    outp[0] = M;
+                    outp[1] = l1 * s1 + l2 * s2;
+                }
+            } else {
+                consumers_sync();
+            }
+        } else {
+            finish_piece<D, FMT>(sm, st, a.ws + ((size_t)c * 4 + i) * (D + 2));
+        }
+    }
+    // publish partials; the last CTA to finish a head merges it into concat
+    consumers_sync();
+    const int cuu = ctx_units(a.S), uu = (nuser + UNIT - 1) / UNIT, per = cuu + uu;
+    const long long TU = (long long)a.H * per;
+    for (int i = 0; i < pl.n; ++i) {
+        const int hh = pl.p[i].head;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int first = owner((long long)hh * per, G, TU);
+            const int last = owner((long long)(hh + 1) * per - 1, G, TU);
+            unsigned expect = 0;  // CTAs with a non-empty unit range inside [first, last]
+            for (int cc = first; cc <= last; ++cc)
+                expect += ((long long)cc * TU / G) < ((long long)(cc + 1) * TU / G);
+            const unsigned prev = atomicAdd(&a.head_ctr[hh], 1u);
+            sm.s_last = (prev == expect - 1) ? (first + 1) : 0;  // 1 + first owner
+            if (prev == expect - 1) atomicExch(&a.head_ctr[hh], 0u);
+        }
+        consumers_sync();
+        const int last_flag = sm.s_last;
+        if (last_flag) {
+            __threadfence();
+            const int first = last_flag - 1;
+            const int lastc = owner((long long)(hh + 1) * per - 1, G, TU);
+            if (threadIdx.x < D) {
+                float M = -CUDART_INF_F;
+                for (int cc = first; cc <= lastc; ++cc) {
+                    const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
+                    if (po.n == 0) continue;
+                    const int slot = po.p[0].head == hh ? 0 : 1;
+                    const float* pp = a.ws + ((size_t)cc * 4 + slot) * (D + 2);
+                    if (__ldcg(pp + 1) > 0.0f) M = fmaxf(M, __ldcg(pp));
+                }
+                float Ls = 0.0f, O = 0.0f;
+                for (int cc = first; cc <= lastc; ++cc) {
+                    const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
+                    if (po.n == 0) continue;
+                    const int slot = po.p[0].head == hh ? 0 : 1;
+                    const float* pp = a.ws + ((size_t)cc * 4 + slot) * (D + 2);
+                    const float li = __ldcg(pp + 1);
+                    if (li > 0.0f) {
+                        const float s = exp2f((__ldcg(pp) - M) * kLog2e);
+                        Ls += li * s;
+                        O += __ldcg(pp + 2 + threadIdx.x) * s;
+                    }
+                }
+                a.concat[hh * D + threadIdx.x] = O / Ls;
+            }
+        }
+        consumers_sync();
+    }
+}
+
+template <int D, int KC>
+__global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_constant__ MegaArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    const int c = blockIdx.x, G = gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = a.H * D;
+    const int user_len = a.state->user_len;  // rows before this token
+    const int step = a.state->step;
+    const int nuser = user_len + 1;           // visible user rows incl. this token
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == NCW) {  // producer
+        if (lane == 0) produce<D>(a, sm, c, G, nuser);
+        return;
+    }
+    Cursor cu;
+    const Split qrows = rows_of(c, G, 3 * h), orows = rows_of(c, G, h);
+    const AttnPlan pl = plan_attention(c, G, a.H, a.S, nuser);
+    float xr[KC * 8];
+    for (int l = 0; l < a.L; ++l) {
+        const MegaLayer& ly = a.layer[l];
+        // ---- P1: QKV ----
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int k = cc * 256 + lane * 8 + e;
+                float v = __ldcg(a.x + k);
+                if (l == 0) {
+                    const float pe =
+                        __uint_as_float((uint32_t)a.pos[(size_t)(a.S + user_len) * h + k] << 16);
+                    v = a.gamma[k] * (v + pe) + a.bias[k];
+                }
+                xr[cc * 8 + e] = v;
+            }
+        proj_rows<D, KC>(sm, cu, qrows, h, xr, [&](int n, float v) {
+            const int part = n / h, rem = n - part * h;
+            if (part == 0) {
+                a.q[rem] = v;
+            } else {
+                const int head = rem / D, cix = rem - head * D;
+                uint16_t* dst = part == 1 ? ly.uk : ly.uv;
+                dst[((size_t)head * a.cap + user_len) * D + cix] = f32_to_bf16_bits(v);
+            }
+        });
+        grid_sync(a.bar, G);
+        // ---- P2: attention ----
+        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, nuser);
+        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, nuser);
+        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, nuser);
+        grid_sync(a.bar, G);
+        // ---- P3: output projection ----
+#pragma unroll
+        for (int cc = 0; cc < KC; ++cc)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) xr[cc * 8 + e] = __ldcg(a.concat + cc * 256 + lane * 8 + e);
+        const bool last = l == a.L - 1;
+        proj_rows<D, KC>(sm, cu, orows, h, xr, [&](int n, float v) {
+            a.x[n] = v;
+            if (last) a.hist[(size_t)step * h + n] = v;
+        });
+        grid_sync(a.bar, G);
+    }
+    if (c == 0 && threadIdx.x == 0) {
+        a.state->user_len = user_len + 1;
+        a.state->step = step + 1;
+    }
+}
+
+}  // namespace mk
+
+size_t mega_smem_bytes(int D) {
+    switch (D) {
+        case 32: return sizeof(mk::Smem<32>) + 128;
+        case 64: return sizeof(mk::Smem<64>) + 128;
+        default: return sizeof(mk::Smem<128>) + 128;
+    }
+}
+
+bool mega_supported(int L, int H, int D, int S, int h) {
+    if (L > kMegaMaxLayers || H > 148 || S % mk::UNIT != 0) return false;
+    if (!(D == 32 || D == 64 || D == 128)) return false;
+    if (h % 256 != 0 || h > 2048) return false;  // x held in registers (KC <= 8)
+    if (mk::STAGE / (h * 2) < 1) return false;
+    return true;
+}
+
+template <int D, int KC>
+static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
+    auto fn = mk::decode_step_kernel<D, KC>;
+    const size_t smem = mega_smem_bytes(D);
+    static bool set = false;
+    if (!set) {
+        EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        set = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(mk::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EKV_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
+}
+
+template <int D>
+static void launch_d(const MegaArgs& a, int grid, int kc, cudaStream_t st) {
+    switch (kc) {
+        case 1: launch_dk<D, 1>(a, grid, st); break;
+        case 2: launch_dk<D, 2>(a, grid, st); break;
+        case 4: launch_dk<D, 4>(a, grid, st); break;
+        case 8: launch_dk<D, 8>(a, grid, st); break;
+        default: require(false, "decode megakernel: hidden size must be 256/512/1024/2048",
+                         EKV_EUNSUPPORTED);
+    }
+}
+
+void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st) {
+    const int kc = a.H * a.D / 256;
+    switch (a.D) {
+        case 32: launch_d<32>(a, num_sms, kc, st); break;
+        case 64: launch_d<64>(a, num_sms, kc, st); break;
+        case 128: launch_d<128>(a, num_sms, kc, st); break;
+        default: require(false, "decode megakernel: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
+    }
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+}  // namespace ekv

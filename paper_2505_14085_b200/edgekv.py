@@ -359,15 +359,22 @@ class Session:
             self.model.ctx.synchronize()
         return out
 
+    def set_decode_path(self, path: str) -> str:
+        """'mega' (one persistent kernel per step, default) or 'graph' (per-layer kernels in a
+        CUDA graph).  Returns the path that will actually run."""
+        act = C.c_int()
+        call("ekv_session_set_decode_path", self.hnd, 0 if path == "mega" else 1, C.byref(act))
+        return "mega" if act.value == 0 else "graph"
+
     def profile_step(self) -> np.ndarray:
-        """One real decode step, kernel by kernel, with CUDA-event times (ms):
-        [3l] QKV projection, [3l+1] attention, [3l+2] output projection, [3L] advance."""
+        """One real decode step with CUDA-event times (ms).  Graph path: [3l] QKV projection,
+        [3l+1] attention, [3l+2] output projection, [3L] advance; persistent path: [0] = step."""
         n = 3 * self.model.L + 1
         out = np.zeros(n, dtype=np.float32)
         got = C.c_int()
         call("ekv_session_profile_step", self.hnd, out.ctypes.data_as(C.POINTER(C.c_float)), n,
              C.byref(got))
-        return out
+        return out[:got.value]
 
     def user_kv(self, layer: int):
         k = C.c_void_p(); v = C.c_void_p(); cap = C.c_int()

@@ -106,15 +106,23 @@ def make_context(ek, ctx, oracle, model, S, formats, seed, d_c=None):
 EKV_INT8, EKV_INT4 = 8, 4
 
 
-@pytest.mark.parametrize("formats,S,U,T", [([16, 8, 8], 300, 5, 6), ([16, 16], 0, 3, 4),
-                                           ([16, 4], 257, 9, 3), ([8, 8], 128, 0, 3)])
-def test_collaborative_decode_matches_oracle(ek, ctx, oracle, formats, S, U, T):
-    L, H, d = len(formats), 4, 64
+@pytest.mark.parametrize("path", ["mega", "graph"])
+@pytest.mark.parametrize("formats,S,U,T,H,d", [([16, 8, 8], 320, 5, 6, 4, 64),
+                                               ([16, 16], 0, 3, 4, 4, 64),
+                                               ([16, 4], 256, 9, 3, 4, 64),
+                                               ([8, 8], 128, 0, 3, 4, 64),
+                                               ([16, 8], 300, 4, 3, 4, 64),
+                                               ([16, 8, 4], 512, 7, 5, 8, 32),
+                                               ([8, 16], 256, 3, 4, 4, 128)])
+def test_collaborative_decode_matches_oracle(ek, ctx, oracle, formats, S, U, T, H, d, path):
+    L = len(formats)
     h, max_pos = H * d, 1024
     bits, f64 = host_bf16_model(oracle, L, H, d, max_pos, seed=7 + S)
     model = upload_model(ek, ctx, bits, L, H, d, max_pos)
     kvc, ck, cv = make_context(ek, ctx, oracle, model, S, formats, seed=11 + S)
     sess = ek.Session(model, kvc, U + T)
+    got_path = sess.set_decode_path(path)
+    assert got_path == ("graph" if (path == "graph" or S % 16) else "mega")
     ue = oracle.generate_embeddings(43, max(U, 1), h)[:U]
     ue32 = ue.astype(np.float32)
     pre, steps = ek.collaborative_decode(sess, ue32, T)
@@ -238,9 +246,11 @@ def test_full_ce_lslm_path_config1(ek, ctx, oracle):
     sess = ek.Session(edge, kvc, U + T)
     useed = oracle.mix(42, 0x55E20000)
     ue = oracle.generate_embeddings(useed, U, he).astype(np.float32)
-    pre, steps = ek.collaborative_decode(sess, ue, T)
-    teacher = np.vstack([pre[-1:], steps[:-1]]).astype(np.float64)
-    wp, ws_ = oracle.collaborative_decode(ef, ck, cv, ue.astype(np.float64), T, teacher=teacher,
-                                          user_kv_bf16=True)
-    assert max(normwise(pre[r], wp[r]) for r in range(U)) <= TOL
-    assert max(normwise(steps[t], ws_[t]) for t in range(T)) <= TOL
+    for path in ("mega", "graph"):
+        assert sess.set_decode_path(path) == path
+        pre, steps = ek.collaborative_decode(sess, ue, T)
+        teacher = np.vstack([pre[-1:], steps[:-1]]).astype(np.float64)
+        wp, ws_ = oracle.collaborative_decode(ef, ck, cv, ue.astype(np.float64), T, teacher=teacher,
+                                              user_kv_bf16=True)
+        assert max(normwise(pre[r], wp[r]) for r in range(U)) <= TOL
+        assert max(normwise(steps[t], ws_[t]) for t in range(T)) <= TOL, path
