@@ -251,6 +251,11 @@ int ekv_session_decode(ekv_session_t s, int steps, float* out_dev);
  * 1 = the per-layer kernels (K5, K4, K5) replayed from a CUDA graph.
  * active (optional) receives the path that will actually run. */
 int ekv_session_set_decode_path(ekv_session_t s, int path, int* active);
+/* Diagnostics of the persistent path: one real decode step with %globaltimer
+ * stamps (ns) of every grid barrier: out[(3l+k)*2G + g] = arrival of CTA g at
+ * barrier k of layer l, out[(3l+k)*2G + G + g] = its release; out[6L*G + g] =
+ * CTA start.  Needs capacity >= (6L+1)*G. */
+int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_out);
 /* One decode step launched kernel by kernel with CUDA events between the
  * launches (diagnostics / roofline attribution; the step is real and advances
  * the session).  Graph path: kernel_ms[3l+0] = layer l QKV projection,

@@ -79,6 +79,7 @@ PROTOS = {
     "ekv_session_forward": [_vp, _vp, _i, _vp],
     "ekv_session_decode": [_vp, _i, _vp],
     "ekv_session_set_decode_path": [_vp, _i, _ip],
+    "ekv_session_trace_step": [_vp, C.POINTER(C.c_uint64), _i, _ip],
     "ekv_session_profile_step": [_vp, _fp, _i, _ip],
     "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
     "ekv_collaborative_decode": [_vp, _vp, _i, _i, _vp, _vp],

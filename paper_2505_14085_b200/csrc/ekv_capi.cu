@@ -1073,6 +1073,29 @@ int ekv_session_destroy(ekv_session_t s) {
     });
 }
 
+int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_out) {
+    return guard([&] {
+        require(s && out && n_out, "null argument");
+        require(use_mega(s), "trace: the persistent decode kernel is not active");
+        const int G = s->model->ctx->num_sms, L = s->model->cfg.num_layers;
+        const int n = (6 * L + 1) * G;
+        require(capacity >= n, "trace: need " + std::to_string(n) + " entries");
+        check_overflow(s, 1);
+        set_dev(s->model->ctx);
+        cudaStream_t st = s->model->ctx->stream;
+        unsigned long long* d = dalloc<unsigned long long>(n);
+        MegaArgs a = s->mega;
+        a.trace = d;
+        launch_decode_mega(a, G, st);
+        EKV_CUDA(cudaMemcpyAsync(out, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+        cudaFree(d);
+        s->user_len += 1;
+        s->steps += 1;
+        *n_out = n;
+    });
+}
+
 int ekv_session_set_decode_path(ekv_session_t s, int path, int* active) {
     return guard([&] {
         require(s != nullptr, "null session");

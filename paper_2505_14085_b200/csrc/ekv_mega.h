@@ -35,6 +35,7 @@ struct MegaArgs {
     float* ws;             // [G][4][D+2] attention partials
     unsigned* head_ctr;    // [H], zero
     unsigned* bar;         // grid barrier {count, generation}, zero
+    unsigned long long* trace;  // optional [3L][2][G] barrier arrival/release + [G] start (ns)
     MegaLayer layer[kMegaMaxLayers];
 };
 

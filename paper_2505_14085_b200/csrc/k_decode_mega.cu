@@ -79,10 +79,19 @@ __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Sense-reversing grid barrier over the consumer warps of every CTA.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G) {
+// trace (optional): [2][G] arrival / release timestamps of this barrier.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G,
+                                          unsigned long long* trace = nullptr) {
     consumers_sync();
     if (threadIdx.x == 0) {
+        if (trace) trace[blockIdx.x] = gtimer();
         volatile unsigned* gen = bar + 1;
         const unsigned my = *gen;
         __threadfence();
@@ -98,6 +107,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G) {
             }
         }
         __threadfence();
+        if (trace) trace[G + blockIdx.x] = gtimer();
     }
     consumers_sync();
 }
@@ -586,6 +596,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     const int user_len = a.state->user_len;  // rows before this token
     const int step = a.state->step;
     const int nuser = user_len + 1;           // visible user rows incl. this token
+    if (a.trace && threadIdx.x == 0) a.trace[(size_t)a.L * 6 * G + c] = gtimer();  // start
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
@@ -628,12 +639,13 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
                 dst[((size_t)head * a.cap + user_len) * D + cix] = f32_to_bf16_bits(v);
             }
         });
-        grid_sync(a.bar, G);
+        unsigned long long* tr = a.trace ? a.trace + (size_t)(3 * l) * 2 * G : nullptr;
+        grid_sync(a.bar, G, tr);
         // ---- P2: attention ----
         if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, nuser);
         else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, nuser);
         else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, nuser);
-        grid_sync(a.bar, G);
+        grid_sync(a.bar, G, tr ? tr + 2 * G : nullptr);
         // ---- P3: output projection ----
 #pragma unroll
         for (int cc = 0; cc < KC; ++cc)
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
             a.x[n] = v;
             if (last) a.hist[(size_t)step * h + n] = v;
         });
-        grid_sync(a.bar, G);
+        grid_sync(a.bar, G, tr ? tr + 4 * G : nullptr);
     }
     if (c == 0 && threadIdx.x == 0) {
         a.state->user_len = user_len + 1;

@@ -366,6 +366,15 @@ class Session:
         call("ekv_session_set_decode_path", self.hnd, 0 if path == "mega" else 1, C.byref(act))
         return "mega" if act.value == 0 else "graph"
 
+    def trace_step(self, num_sms: int) -> np.ndarray:
+        """Persistent path: %globaltimer stamps of one step, [(6L+1)*G] (see ekv_capi.h)."""
+        n = (6 * self.model.L + 1) * num_sms
+        out = np.zeros(n, dtype=np.uint64)
+        got = C.c_int()
+        call("ekv_session_trace_step", self.hnd, out.ctypes.data_as(C.POINTER(C.c_uint64)), n,
+             C.byref(got))
+        return out
+
     def profile_step(self) -> np.ndarray:
         """One real decode step with CUDA-event times (ms).  Graph path: [3l] QKV projection,
         [3l+1] attention, [3l+2] output projection, [3L] advance; persistent path: [0] = step."""
