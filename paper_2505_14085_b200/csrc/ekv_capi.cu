@@ -249,9 +249,9 @@ void session_alloc(ekv_session_s* s) {
         s->mega_ok = mega_supported(L, H, D, s->kv->S, m->h);
         if (s->mega_ok) {
             const int G = m->ctx->num_sms;
-            s->mega_ws = dalloc<float>((size_t)G * 4 * (D + 2));
-            s->mega_sync = dalloc<unsigned>((size_t)H + 2);
-            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * (H + 2)));
+            s->mega_ws = dalloc<float>((size_t)G * 2 * (D + 2));
+            s->mega_sync = dalloc<unsigned>((size_t)H + 8);
+            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * (H + 8)));
             MegaArgs& a = s->mega;
             a.L = L;
             a.H = H;
@@ -268,7 +268,7 @@ void session_alloc(ekv_session_s* s) {
             a.hist = s->hist;
             a.ws = s->mega_ws;
             a.head_ctr = s->mega_sync;
-            a.bar = s->mega_sync + H;
+            a.sync = (unsigned long long*)(s->mega_sync + ((H + 1) & ~1));
             for (int l = 0; l < L; ++l) {
                 const ekv_segment& sg = s->kv->seg[l];
                 MegaLayer& ly = a.layer[l];

@@ -32,9 +32,9 @@ struct MegaArgs {
     float* q;              // [h]
     float* concat;         // [h]
     float* hist;           // [cap][h] step outputs
-    float* ws;             // [G][4][D+2] attention partials
+    float* ws;             // [G][2][D+2] attention partials
     unsigned* head_ctr;    // [H], zero
-    unsigned* bar;         // grid barrier {count, generation}, zero
+    unsigned long long* sync;  // grid barrier {count, count at launch start}, zero
     unsigned long long* trace;  // optional [3L][2][G] barrier arrival/release + [G] start (ns)
     MegaLayer layer[kMegaMaxLayers];
 };

@@ -23,6 +23,10 @@
 // P3 rows [c*h/G, ...); P2 splits the flattened (head, 16-row unit) space of
 // context ++ user rows evenly, so a CTA touches at most two heads; each head's
 // partials (m, l, o) are merged by the last CTA to finish it (atomic counter).
+// User rows written by earlier steps are static during a step, so they are
+// streamed through the ring like the context; only this step's row is read
+// directly.  The activations a phase consumes (x, the attention output, q)
+// are staged once per phase into shared memory with 16-byte loads.
 #include <math_constants.h>
 
 #include "ekv_common.cuh"
@@ -33,7 +37,7 @@ namespace ekv {
 
 namespace mk {
 
-constexpr int NCW = 16;                 // consumer warps
+constexpr int NCW = 8;                  // consumer warps
 constexpr int THREADS = (NCW + 1) * 32; // + 1 producer warp
 constexpr int NST = 3;                  // ring stages
 constexpr int STAGE = 64 * 1024;        // bytes per stage
@@ -85,29 +89,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// Sense-reversing grid barrier over the consumer warps of every CTA.
+// Grid barrier over the consumer warps of every CTA: one 64-bit counter that
+// only grows; barrier k of a launch completes when it reaches base + (k+1)*G,
+// where base (= the counter value when the launch started) is published by
+// CTA 0 at the end of the previous launch.  One red.release + acquire polling,
+// no reset on the critical path.
 // trace (optional): [2][G] arrival / release timestamps of this barrier.
-__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned G,
+__device__ __forceinline__ void grid_sync(unsigned long long* count, unsigned long long target,
                                           unsigned long long* trace = nullptr) {
     consumers_sync();
     if (threadIdx.x == 0) {
         if (trace) trace[blockIdx.x] = gtimer();
-        volatile unsigned* gen = bar + 1;
-        const unsigned my = *gen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == G - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            const long long t0 = clock64();
-            while (*gen == my) {
-                __nanosleep(32);
-                if (clock64() - t0 > 4000000000ll) __trap();
-            }
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+        const long long t0 = clock64();
+        unsigned long long v;
+        while (true) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
+            if (v >= target) break;
+            if (clock64() - t0 > 4000000000ll) __trap();
         }
-        __threadfence();
-        if (trace) trace[G + blockIdx.x] = gtimer();
+        if (trace) trace[gridDim.x + blockIdx.x] = gtimer();
     }
     consumers_sync();
 }
@@ -266,15 +267,21 @@ struct Smem {
     uint8_t ring[NST][STAGE];
     uint64_t full[NST];
     uint64_t empty[NST];
-    float red_m[NCW][32 / 1];  // per warp, per row-subgroup m (max 32 subgroups)
-    float red_l[NCW][32];
-    float red_o[NCW][D];
-    float red_wm[NCW], red_wl[NCW];
+    float xs[2048];            // phase input (x or the attention output)
+    float qs[2][D];            // q of the (<= 2) heads of this CTA's attention pieces
+    float red_o[NCW][D];       // per-warp partial outputs
+    float red_m[NCW], red_l[NCW];
+    float fin_m[2], fin_l[2];  // CTA-level (context, user) states of one piece
+    float fin_o[2][D];
     int s_last;
 };
 
+// Per-piece schedule pieces that go through the ring: context rows [c0, c1) and
+// the static user rows [u0, min(u1, ulen)) (written by earlier steps).
+__device__ __forceinline__ int user_static_end(const Piece& pc, int ulen) { return min(pc.u1, ulen); }
+
 template <int D>
-__device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int nuser) {
+__device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen) {
     int stage = 0;
     uint32_t phase = 0;
     const int h = a.H * D;
@@ -289,8 +296,9 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int nuser)
         }
     };
     const Split q = rows_of(c, G, 3 * h), o = rows_of(c, G, h);
-    const AttnPlan pl = plan_attention(c, G, a.H, a.S, nuser);
+    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
     const int rows_per_w = STAGE / (h * 2);  // weight rows per stage
+    const int ucap = att_stage_rows(D * 2, 0);
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
         for (int r = q.r0; r < q.r1; r += rows_per_w) {
@@ -316,6 +324,17 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int nuser)
                     bulk_g2s(dst + 2 * kb, ly.cks + base * ng, sb, &sm.full[stage]);
                     bulk_g2s(dst + 2 * kb + sb, ly.cvs + base * ng, sb, &sm.full[stage]);
                 }
+                advance();
+            }
+            const int ue = user_static_end(pc, ulen);
+            for (int r = pc.u0; r < ue; r += ucap) {
+                const int n = min(ucap, ue - r);
+                const size_t base = (size_t)pc.head * a.cap + r;
+                const int kb = n * D * 2;
+                next(2 * kb);
+                uint8_t* dst = sm.ring[stage];
+                bulk_g2s(dst, ly.uk + base * D, kb, &sm.full[stage]);
+                bulk_g2s(dst + kb, ly.uv + base * D, kb, &sm.full[stage]);
                 advance();
             }
         }
@@ -349,12 +368,41 @@ __device__ __forceinline__ void ring_release(Smem<D>& sm, Cursor& cu) {
     }
 }
 
-// y[n] = sum_k x[k] W[n][k] for the CTA's rows, weights from the ring.
-// x is in registers: lane holds x[c*256 + lane*8 + e].
+// Stage a phase input vector (h floats, in global, written by other CTAs) into
+// shared memory with 16-byte coherent loads; optional layer-0 input transform.
+template <int D>
+__device__ __forceinline__ void stage_vector(Smem<D>& sm, const float* src, int h,
+                                             const float* gamma, const float* bias,
+                                             const uint16_t* pos_row) {
+    for (int i = threadIdx.x; i < h / 4; i += NCW * 32) {
+        float4 v = __ldcg(reinterpret_cast<const float4*>(src) + i);
+        if (pos_row) {
+            const float4 g = reinterpret_cast<const float4*>(gamma)[i];
+            const float4 b = reinterpret_cast<const float4*>(bias)[i];
+            const uint2 p = reinterpret_cast<const uint2*>(pos_row)[i];
+            v.x = g.x * (v.x + bf16_lo(p.x)) + b.x;
+            v.y = g.y * (v.y + bf16_hi(p.x)) + b.y;
+            v.z = g.z * (v.z + bf16_lo(p.y)) + b.z;
+            v.w = g.w * (v.w + bf16_hi(p.y)) + b.w;
+        }
+        reinterpret_cast<float4*>(sm.xs)[i] = v;
+    }
+    consumers_sync();
+}
+
+// y[n] = sum_k x[k] W[n][k] for the CTA's rows, weights from the ring, x from
+// shared memory into registers once (lane holds x[c*256 + lane*8 + e]).
 template <int D, int KC, class Epi>
-__device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, int h,
-                                          const float* xr, Epi epi) {
+__device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, int h, Epi epi) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float xr[KC * 8];
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+        const float4 a0 = *reinterpret_cast<const float4*>(sm.xs + c * 256 + lane * 8);
+        const float4 a1 = *reinterpret_cast<const float4*>(sm.xs + c * 256 + lane * 8 + 4);
+        xr[c * 8 + 0] = a0.x; xr[c * 8 + 1] = a0.y; xr[c * 8 + 2] = a0.z; xr[c * 8 + 3] = a0.w;
+        xr[c * 8 + 4] = a1.x; xr[c * 8 + 5] = a1.y; xr[c * 8 + 6] = a1.z; xr[c * 8 + 7] = a1.w;
+    }
     const int rows_per_w = STAGE / (h * 2);
     for (int r = rows.r0; r < rows.r1; r += rows_per_w) {
         const int n = min(rows_per_w, rows.r1 - r);
@@ -379,13 +427,12 @@ __device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, i
     }
 }
 
-// Attention of q over rows held in a ring stage (context) or in global memory
-// (user rows), accumulated into this lane's online-softmax state.
+// Attention of q over n rows (ring stage or global), into this lane's state.
 template <int D, int FMT>
-__device__ __forceinline__ void attend_stage(const uint8_t* kb, const uint8_t* vb, const float* ks,
-                                             const float* vs, int ng, int group, int n,
-                                             const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
-                                             bool global_src) {
+__device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t* vb, const float* ks,
+                                               const float* vs, int ng, int group, int n,
+                                               const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
+                                               bool global_src) {
     using F = Fmt<D, FMT>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = lane % F::LPR, rsub = lane / F::LPR;
@@ -425,14 +472,12 @@ __device__ __forceinline__ void attend_stage(const uint8_t* kb, const uint8_t* v
     }
 }
 
-// Combine the lane-group states of all consumer warps into one partial
-// (m, l, o[D]) and write it to the workspace slot.
+// Fold every lane-group state of the CTA into sm.fin_*[which] (m, l, o[D]).
 template <int D, int FMT>
-__device__ __forceinline__ void finish_piece(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& st, float* out) {
+__device__ __forceinline__ void fold_cta(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& st, int which) {
     using F = Fmt<D, FMT>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = lane % F::LPR;
-    // merge the row subgroups inside the warp (xor over the subgroup lane bits)
     for (int off = F::LPR; off < 32; off <<= 1) {
         float o2[F::EPL];
         const float m2 = __shfl_xor_sync(0xffffffffu, st.m, off);
@@ -445,28 +490,28 @@ __device__ __forceinline__ void finish_piece(Smem<D>& sm, OState<Fmt<D, FMT>::EP
 #pragma unroll
         for (int e = 0; e < F::EPL; ++e) sm.red_o[warp][sub * F::EPL + e] = st.o[e];
         if (lane == 0) {
-            sm.red_wm[warp] = st.m;
-            sm.red_wl[warp] = st.l;
+            sm.red_m[warp] = st.m;
+            sm.red_l[warp] = st.l;
         }
     }
     consumers_sync();
-    if (threadIdx.x < D) {
+    for (int t = threadIdx.x; t < D; t += NCW * 32) {
         float M = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) M = fmaxf(M, sm.red_wm[w]);
+        for (int w = 0; w < NCW; ++w) M = fmaxf(M, sm.red_m[w]);
         float Ls = 0.0f, O = 0.0f;
         if (M != -CUDART_INF_F) {
 #pragma unroll
             for (int w = 0; w < NCW; ++w) {
-                const float s = exp2f((sm.red_wm[w] - M) * kLog2e);
-                Ls += sm.red_wl[w] * s;
-                O += sm.red_o[w][threadIdx.x] * s;
+                const float sc = exp2f((sm.red_m[w] - M) * kLog2e);
+                Ls += sm.red_l[w] * sc;
+                O += sm.red_o[w][t] * sc;
             }
         }
-        out[2 + threadIdx.x] = O;
-        if (threadIdx.x == 0) {
-            out[0] = M;
-            out[1] = Ls;
+        sm.fin_o[which][t] = O;
+        if (t == 0) {
+            sm.fin_m[which] = M;
+            sm.fin_l[which] = Ls;
         }
     }
     consumers_sync();
@@ -475,67 +520,77 @@ __device__ __forceinline__ void finish_piece(Smem<D>& sm, OState<Fmt<D, FMT>::EP
 template <int D, int FMT>
 __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
                                                 Cursor& cu, const AttnPlan& pl, int c, int G,
-                                                int nuser) {
+                                                int ulen) {
     using F = Fmt<D, FMT>;
+    using FU = Fmt<D, 16>;
     const int lane = threadIdx.x & 31;
-    const int sub = lane % F::LPR;
+    const int nuser = ulen + 1;
     const int ng = FMT == 16 ? 0 : D / ly.group;
     const int cap = att_stage_rows(F::ROW, ng);
+    const int ucap = att_stage_rows(D * 2, 0);
+    // q of the heads this CTA attends (written by P1 on other CTAs)
+    for (int i = 0; i < pl.n; ++i)
+        for (int t = threadIdx.x; t < D / 4; t += NCW * 32)
+            reinterpret_cast<float4*>(sm.qs[i])[t] =
+                __ldcg(reinterpret_cast<const float4*>(a.q + pl.p[i].head * D) + t);
+    consumers_sync();
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
-        float qreg[F::EPL];
+        {   // context rows (ring)
+            float qreg[F::EPL];
+            const int sub = lane % F::LPR;
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) qreg[e] = __ldcg(a.q + pc.head * D + sub * F::EPL + e);
-        OState<F::EPL> st;
-        ostate_init<F::EPL>(st);
-        for (int r = pc.c0; r < pc.c1; r += cap) {
-            const int n = min(cap, pc.c1 - r);
-            const uint8_t* s = ring_acquire(sm, cu);
-            const int kbytes = n * F::ROW;
-            attend_stage<D, FMT>(s, s + kbytes, (const float*)(s + 2 * kbytes),
-                                 (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n, qreg,
-                                 st, false);
-            ring_release(sm, cu);
+            for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
+            OState<F::EPL> st;
+            ostate_init<F::EPL>(st);
+            for (int r = pc.c0; r < pc.c1; r += cap) {
+                const int n = min(cap, pc.c1 - r);
+                const uint8_t* s = ring_acquire(sm, cu);
+                const int kbytes = n * F::ROW;
+                attend_rows_mk<D, FMT>(s, s + kbytes, (const float*)(s + 2 * kbytes),
+                                       (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n,
+                                       qreg, st, false);
+                ring_release(sm, cu);
+            }
+            fold_cta<D, FMT>(sm, st, 0);
         }
-        if (pc.u1 > pc.u0) {
-            // user rows: bf16, written by P1 of this layer -> coherent loads
-            using FU = Fmt<D, 16>;
-            float qu[FU::EPL];
-            const int subu = lane % FU::LPR;
+        {   // user rows: earlier steps through the ring, this step's row directly
+            float qreg[FU::EPL];
+            const int sub = lane % FU::LPR;
 #pragma unroll
-            for (int e = 0; e < FU::EPL; ++e) qu[e] = __ldcg(a.q + pc.head * D + subu * FU::EPL + e);
+            for (int e = 0; e < FU::EPL; ++e) qreg[e] = sm.qs[i][sub * FU::EPL + e];
             OState<FU::EPL> su;
             ostate_init<FU::EPL>(su);
-            const uint8_t* kbase = (const uint8_t*)(ly.uk + ((size_t)pc.head * a.cap + pc.u0) * D);
-            const uint8_t* vbase = (const uint8_t*)(ly.uv + ((size_t)pc.head * a.cap + pc.u0) * D);
-            attend_stage<D, 16>(kbase, vbase, nullptr, nullptr, 0, D, pc.u1 - pc.u0, qu, su, true);
-            // fold the user state into the context state through the workspace
-            float* tmp = a.ws + ((size_t)c * 4 + 2 + i) * (D + 2);
-            finish_piece<D, 16>(sm, su, tmp);
-            // merge the context partial with the user partial
-            float* outp = a.ws + ((size_t)c * 4 + i) * (D + 2);
-            finish_piece<D, FMT>(sm, st, outp);
-            if (threadIdx.x < D) {
-                const float m1 = outp[0], l1 = outp[1], m2 = tmp[0], l2 = tmp[1];
-                const float M = fmaxf(m1, m2);
-                const float s1 = (l1 > 0.0f) ? exp2f((m1 - M) * kLog2e) : 0.0f;
-                const float s2 = (l2 > 0.0f) ? exp2f((m2 - M) * kLog2e) : 0.0f;
-                const float o = outp[2 + threadIdx.x] * s1 + tmp[2 + threadIdx.x] * s2;
-                consumers_sync();
-                outp[2 + threadIdx.x] = o;
-                if (threadIdx.x == 0) {
-                    outp[0] = M;
-                    outp[1] = l1 * s1 + l2 * s2;
-                }
-            } else {
-                consumers_sync();
+            const int ue = user_static_end(pc, ulen);
+            for (int r = pc.u0; r < ue; r += ucap) {
+                const int n = min(ucap, ue - r);
+                const uint8_t* s = ring_acquire(sm, cu);
+                attend_rows_mk<D, 16>(s, s + n * D * 2, nullptr, nullptr, 0, D, n, qreg, su, false);
+                ring_release(sm, cu);
             }
-        } else {
-            finish_piece<D, FMT>(sm, st, a.ws + ((size_t)c * 4 + i) * (D + 2));
+            if (ulen >= pc.u0 && ulen < pc.u1) {
+                const size_t row = (size_t)pc.head * a.cap + ulen;
+                attend_rows_mk<D, 16>((const uint8_t*)(ly.uk + row * D), (const uint8_t*)(ly.uv + row * D),
+                                      nullptr, nullptr, 0, D, 1, qreg, su, true);
+            }
+            fold_cta<D, 16>(sm, su, 1);
         }
+        // combine (context, user) and publish this CTA's partial for the head
+        float* outp = a.ws + ((size_t)c * 2 + i) * (D + 2);
+        for (int t = threadIdx.x; t < D; t += NCW * 32) {
+            const float m1 = sm.fin_m[0], l1 = sm.fin_l[0], m2 = sm.fin_m[1], l2 = sm.fin_l[1];
+            const float M = fmaxf(m1, m2);
+            const float s1 = (l1 > 0.0f) ? exp2f((m1 - M) * kLog2e) : 0.0f;
+            const float s2 = (l2 > 0.0f) ? exp2f((m2 - M) * kLog2e) : 0.0f;
+            outp[2 + t] = sm.fin_o[0][t] * s1 + sm.fin_o[1][t] * s2;
+            if (t == 0) {
+                outp[0] = M;
+                outp[1] = l1 * s1 + l2 * s2;
+            }
+        }
+        consumers_sync();
     }
-    // publish partials; the last CTA to finish a head merges it into concat
-    consumers_sync();
+    // the last CTA to finish a head merges its partials into the attention output
     const int cuu = ctx_units(a.S), uu = (nuser + UNIT - 1) / UNIT, per = cuu + uu;
     const long long TU = (long long)a.H * per;
     for (int i = 0; i < pl.n; ++i) {
@@ -548,7 +603,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             for (int cc = first; cc <= last; ++cc)
                 expect += ((long long)cc * TU / G) < ((long long)(cc + 1) * TU / G);
             const unsigned prev = atomicAdd(&a.head_ctr[hh], 1u);
-            sm.s_last = (prev == expect - 1) ? (first + 1) : 0;  // 1 + first owner
+            sm.s_last = (prev == expect - 1) ? (first + 1) : 0;
             if (prev == expect - 1) atomicExch(&a.head_ctr[hh], 0u);
         }
         consumers_sync();
@@ -557,29 +612,27 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             __threadfence();
             const int first = last_flag - 1;
             const int lastc = owner((long long)(hh + 1) * per - 1, G, TU);
-            if (threadIdx.x < D) {
+            for (int t = threadIdx.x; t < D; t += NCW * 32) {
                 float M = -CUDART_INF_F;
                 for (int cc = first; cc <= lastc; ++cc) {
                     const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
                     if (po.n == 0) continue;
-                    const int slot = po.p[0].head == hh ? 0 : 1;
-                    const float* pp = a.ws + ((size_t)cc * 4 + slot) * (D + 2);
+                    const float* pp = a.ws + ((size_t)cc * 2 + (po.p[0].head == hh ? 0 : 1)) * (D + 2);
                     if (__ldcg(pp + 1) > 0.0f) M = fmaxf(M, __ldcg(pp));
                 }
                 float Ls = 0.0f, O = 0.0f;
                 for (int cc = first; cc <= lastc; ++cc) {
                     const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
                     if (po.n == 0) continue;
-                    const int slot = po.p[0].head == hh ? 0 : 1;
-                    const float* pp = a.ws + ((size_t)cc * 4 + slot) * (D + 2);
+                    const float* pp = a.ws + ((size_t)cc * 2 + (po.p[0].head == hh ? 0 : 1)) * (D + 2);
                     const float li = __ldcg(pp + 1);
                     if (li > 0.0f) {
-                        const float s = exp2f((__ldcg(pp) - M) * kLog2e);
-                        Ls += li * s;
-                        O += __ldcg(pp + 2 + threadIdx.x) * s;
+                        const float sc = exp2f((__ldcg(pp) - M) * kLog2e);
+                        Ls += li * sc;
+                        O += __ldcg(pp + 2 + t) * sc;
                     }
                 }
-                a.concat[hh * D + threadIdx.x] = O / Ls;
+                a.concat[hh * D + t] = O / Ls;
             }
         }
         consumers_sync();
@@ -593,9 +646,9 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     const int c = blockIdx.x, G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = a.H * D;
-    const int user_len = a.state->user_len;  // rows before this token
+    const int ulen = a.state->user_len;  // user rows before this token
     const int step = a.state->step;
-    const int nuser = user_len + 1;           // visible user rows incl. this token
+    const unsigned long long base = a.sync[1];  // barrier counter value at launch
     if (a.trace && threadIdx.x == 0) a.trace[(size_t)a.L * 6 * G + c] = gtimer();  // start
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
@@ -606,61 +659,48 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     }
     __syncthreads();
     if (warp == NCW) {  // producer
-        if (lane == 0) produce<D>(a, sm, c, G, nuser);
+        if (lane == 0) produce<D>(a, sm, c, G, ulen);
         return;
     }
     Cursor cu;
     const Split qrows = rows_of(c, G, 3 * h), orows = rows_of(c, G, h);
-    const AttnPlan pl = plan_attention(c, G, a.H, a.S, nuser);
-    float xr[KC * 8];
+    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
+    unsigned long long nb = 0;  // barriers passed in this launch
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
-        // ---- P1: QKV ----
-#pragma unroll
-        for (int cc = 0; cc < KC; ++cc)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int k = cc * 256 + lane * 8 + e;
-                float v = __ldcg(a.x + k);
-                if (l == 0) {
-                    const float pe =
-                        __uint_as_float((uint32_t)a.pos[(size_t)(a.S + user_len) * h + k] << 16);
-                    v = a.gamma[k] * (v + pe) + a.bias[k];
-                }
-                xr[cc * 8 + e] = v;
-            }
-        proj_rows<D, KC>(sm, cu, qrows, h, xr, [&](int n, float v) {
+        unsigned long long* tr = a.trace ? a.trace + (size_t)(3 * l) * 2 * G : nullptr;
+        // ---- P1: QKV (input transform fused at layer 0) ----
+        stage_vector<D>(sm, a.x, h, a.gamma, a.bias,
+                        l == 0 ? a.pos + (size_t)(a.S + ulen) * h : nullptr);
+        proj_rows<D, KC>(sm, cu, qrows, h, [&](int n, float v) {
             const int part = n / h, rem = n - part * h;
             if (part == 0) {
                 a.q[rem] = v;
             } else {
                 const int head = rem / D, cix = rem - head * D;
                 uint16_t* dst = part == 1 ? ly.uk : ly.uv;
-                dst[((size_t)head * a.cap + user_len) * D + cix] = f32_to_bf16_bits(v);
+                dst[((size_t)head * a.cap + ulen) * D + cix] = f32_to_bf16_bits(v);
             }
         });
-        unsigned long long* tr = a.trace ? a.trace + (size_t)(3 * l) * 2 * G : nullptr;
-        grid_sync(a.bar, G, tr);
+        grid_sync(a.sync, base + (++nb) * G, tr);
         // ---- P2: attention ----
-        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, nuser);
-        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, nuser);
-        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, nuser);
-        grid_sync(a.bar, G, tr ? tr + 2 * G : nullptr);
+        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, ulen);
+        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, ulen);
+        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, ulen);
+        grid_sync(a.sync, base + (++nb) * G, tr ? tr + 2 * G : nullptr);
         // ---- P3: output projection ----
-#pragma unroll
-        for (int cc = 0; cc < KC; ++cc)
-#pragma unroll
-            for (int e = 0; e < 8; ++e) xr[cc * 8 + e] = __ldcg(a.concat + cc * 256 + lane * 8 + e);
+        stage_vector<D>(sm, a.concat, h, nullptr, nullptr, nullptr);
         const bool last = l == a.L - 1;
-        proj_rows<D, KC>(sm, cu, orows, h, xr, [&](int n, float v) {
+        proj_rows<D, KC>(sm, cu, orows, h, [&](int n, float v) {
             a.x[n] = v;
             if (last) a.hist[(size_t)step * h + n] = v;
         });
-        grid_sync(a.bar, G, tr ? tr + 4 * G : nullptr);
+        grid_sync(a.sync, base + (++nb) * G, tr ? tr + 4 * G : nullptr);
     }
     if (c == 0 && threadIdx.x == 0) {
-        a.state->user_len = user_len + 1;
+        a.state->user_len = ulen + 1;
         a.state->step = step + 1;
+        a.sync[1] = base + nb * G;  // every CTA read `base` before the first barrier
     }
 }
 
