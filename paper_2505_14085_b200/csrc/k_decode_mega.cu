@@ -39,8 +39,8 @@ namespace mk {
 
 constexpr int NCW = 8;                  // consumer warps
 constexpr int THREADS = (NCW + 1) * 32; // + 1 producer warp
-constexpr int NST = 3;                  // ring stages
-constexpr int STAGE = 64 * 1024;        // bytes per stage
+constexpr int NST = 12;                 // ring stages
+constexpr int STAGE = 16 * 1024;        // bytes per stage
 constexpr int UNIT = 16;                // attention rows per partition unit
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -272,6 +272,7 @@ struct Smem {
     float red_o[NCW][D];       // per-warp partial outputs
     float red_m[NCW], red_l[NCW];
     float fin_m[2], fin_l[2];  // CTA-level (context, user) states of one piece
+    float mw[160], lw[160];    // merge of one head: per contributing CTA (m, l) then weight
     float fin_o[2][D];
     int s_last;
 };
@@ -612,27 +613,50 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             __threadfence();
             const int first = last_flag - 1;
             const int lastc = owner((long long)(hh + 1) * per - 1, G, TU);
-            for (int t = threadIdx.x; t < D; t += NCW * 32) {
-                float M = -CUDART_INF_F;
-                for (int cc = first; cc <= lastc; ++cc) {
-                    const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
-                    if (po.n == 0) continue;
-                    const float* pp = a.ws + ((size_t)cc * 2 + (po.p[0].head == hh ? 0 : 1)) * (D + 2);
-                    if (__ldcg(pp + 1) > 0.0f) M = fmaxf(M, __ldcg(pp));
+            const int nc = lastc - first + 1;  // <= G
+            // (m, l) of every contributing CTA -> shared memory, then weights
+            for (int j = threadIdx.x; j < nc; j += NCW * 32) {
+                const int cc = first + j;
+                const long long u0 = (long long)cc * TU / G, u1 = (long long)(cc + 1) * TU / G;
+                float m = -CUDART_INF_F, l = 0.0f;
+                if (u0 < u1) {
+                    const int slot = (int)(u0 / per) == hh ? 0 : 1;
+                    const float* pp = a.ws + ((size_t)cc * 2 + slot) * (D + 2);
+                    m = __ldcg(pp);
+                    l = __ldcg(pp + 1);
+                    if (!(l > 0.0f)) m = -CUDART_INF_F;
                 }
-                float Ls = 0.0f, O = 0.0f;
-                for (int cc = first; cc <= lastc; ++cc) {
-                    const AttnPlan po = plan_attention(cc, G, a.H, a.S, nuser);
-                    if (po.n == 0) continue;
-                    const float* pp = a.ws + ((size_t)cc * 2 + (po.p[0].head == hh ? 0 : 1)) * (D + 2);
-                    const float li = __ldcg(pp + 1);
-                    if (li > 0.0f) {
-                        const float sc = exp2f((__ldcg(pp) - M) * kLog2e);
-                        Ls += li * sc;
-                        O += __ldcg(pp + 2 + t) * sc;
+                sm.mw[j] = m;
+                sm.lw[j] = l;
+            }
+            consumers_sync();
+            if (threadIdx.x < 32) {
+                float M = -CUDART_INF_F;
+                for (int j = threadIdx.x; j < nc; j += 32) M = fmaxf(M, sm.mw[j]);
+                M = warp_max(M);
+                float Ls = 0.0f;
+                for (int j = threadIdx.x; j < nc; j += 32) {
+                    const float w = sm.mw[j] == -CUDART_INF_F ? 0.0f : exp2f((sm.mw[j] - M) * kLog2e);
+                    sm.mw[j] = w;
+                    Ls += sm.lw[j] * w;
+                }
+                Ls = warp_sum(Ls);
+                if (threadIdx.x == 0) sm.fin_l[0] = Ls;
+            }
+            consumers_sync();
+            const float inv = 1.0f / sm.fin_l[0];
+            for (int t = threadIdx.x; t < D; t += NCW * 32) {
+                float O = 0.0f;
+#pragma unroll 4
+                for (int j = 0; j < nc; ++j) {
+                    const float w = sm.mw[j];
+                    if (w != 0.0f) {
+                        const int cc = first + j;
+                        const int slot = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
+                        O += __ldcg(a.ws + ((size_t)cc * 2 + slot) * (D + 2) + 2 + t) * w;
                     }
                 }
-                a.concat[hh * D + t] = O / Ls;
+                a.concat[hh * D + t] = O * inv;
             }
         }
         consumers_sync();
