@@ -39,10 +39,11 @@ namespace mk {
 
 constexpr int NCW = 8;                  // consumer warps
 constexpr int THREADS = (NCW + 1) * 32; // + 1 producer warp
-constexpr int NST = 12;                 // ring stages
-constexpr int STAGE = 16 * 1024;        // bytes per stage
+constexpr int NST = 16;                 // ring stages (a multiple of NCW: see the ring protocol)
+constexpr int STAGE = 12 * 1024;        // bytes per stage
 constexpr int UNIT = 16;                // attention rows per partition unit
 constexpr float kLog2e = 1.4426950408889634f;
+static_assert(NST % NCW == 0, "ring slots must map to a fixed consumer warp");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -348,25 +349,26 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen) 
     }
 }
 
-// consumer-side ring cursor
+// Ring protocol.  Producer and consumers walk the same global sequence of
+// stages; stage k lives in slot k % NST (phase bit (k / NST) & 1) and is owned
+// by consumer warp k % NCW, which alone waits for it, uses it and releases it
+// (empty barriers count one arrival), so up to NCW stages are worked on
+// concurrently while the producer refills the rest.  NST % NCW == 0 makes every
+// slot belong to one warp forever: a warp waits for round r of a slot only
+// after it released round r-1 itself, so the parity wait cannot alias.
 struct Cursor {
-    int stage = 0;
-    uint32_t phase = 0;
+    long long k = 0;  // global index of the first stage of the current phase
 };
 
 template <int D>
-__device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, Cursor& cu) {
-    mbar_wait(&sm.full[cu.stage], cu.phase);
-    return sm.ring[cu.stage];
+__device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, long long k) {
+    mbar_wait(&sm.full[k % NST], (uint32_t)((k / NST) & 1));
+    return sm.ring[k % NST];
 }
 template <int D>
-__device__ __forceinline__ void ring_release(Smem<D>& sm, Cursor& cu) {
+__device__ __forceinline__ void ring_release(Smem<D>& sm, long long k) {
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[cu.stage]);
-    if (++cu.stage == NST) {
-        cu.stage = 0;
-        cu.phase ^= 1;
-    }
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[k % NST]);
 }
 
 // Stage a phase input vector (h floats, in global, written by other CTAs) into
@@ -405,27 +407,34 @@ __device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, i
         xr[c * 8 + 4] = a1.x; xr[c * 8 + 5] = a1.y; xr[c * 8 + 6] = a1.z; xr[c * 8 + 7] = a1.w;
     }
     const int rows_per_w = STAGE / (h * 2);
-    for (int r = rows.r0; r < rows.r1; r += rows_per_w) {
+    const int nst = (rows.r1 - rows.r0 + rows_per_w - 1) / rows_per_w;
+    for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
+        const int r = rows.r0 + j * rows_per_w;
         const int n = min(rows_per_w, rows.r1 - r);
-        const uint8_t* st = ring_acquire(sm, cu);
-        for (int i = warp; i < n; i += NCW) {
+        const uint8_t* st = ring_acquire(sm, cu.k + j);
+        for (int i = 0; i < n; ++i) {
             const uint16_t* w = (const uint16_t*)(st + (size_t)i * h * 2);
-            float acc = 0.0f;
+            float acc[KC];
 #pragma unroll
             for (int c = 0; c < KC; ++c) {
                 const uint4 v = *reinterpret_cast<const uint4*>(w + c * 256 + lane * 8);
                 const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
+                float a0 = 0.0f;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    acc = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], acc);
-                    acc = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], acc);
+                    a0 = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], a0);
+                    a0 = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], a0);
                 }
+                acc[c] = a0;
             }
-            acc = warp_sum(acc);
-            if (lane == 0) epi(r + i, acc);
+#pragma unroll
+            for (int c = 1; c < KC; ++c) acc[0] += acc[c];
+            const float v = warp_sum(acc[0]);
+            if (lane == 0) epi(r + i, v);
         }
-        ring_release(sm, cu);
+        ring_release(sm, cu.k + j);
     }
+    cu.k += nst;
 }
 
 // Attention of q over n rows (ring stage or global), into this lane's state.
@@ -435,10 +444,10 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
                                                const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
                                                bool global_src) {
     using F = Fmt<D, FMT>;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31;
     const int sub = lane % F::LPR, rsub = lane / F::LPR;
     const int grp = FMT == 16 ? 0 : (sub * F::EPL) / group;
-    for (int base = warp * F::RPP; base < n; base += NCW * F::RPP) {
+    for (int base = 0; base < n; base += F::RPP) {  // the calling warp owns all n rows
         const int row = base + rsub;
         const bool ok = row < n;
         uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
@@ -544,15 +553,19 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
             OState<F::EPL> st;
             ostate_init<F::EPL>(st);
-            for (int r = pc.c0; r < pc.c1; r += cap) {
+            const int warp = threadIdx.x >> 5;
+            const int nst = (pc.c1 - pc.c0 + cap - 1) / cap;
+            for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
+                const int r = pc.c0 + j * cap;
                 const int n = min(cap, pc.c1 - r);
-                const uint8_t* s = ring_acquire(sm, cu);
+                const uint8_t* s = ring_acquire(sm, cu.k + j);
                 const int kbytes = n * F::ROW;
                 attend_rows_mk<D, FMT>(s, s + kbytes, (const float*)(s + 2 * kbytes),
                                        (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n,
                                        qreg, st, false);
-                ring_release(sm, cu);
+                ring_release(sm, cu.k + j);
             }
+            cu.k += nst;
             fold_cta<D, FMT>(sm, st, 0);
         }
         {   // user rows: earlier steps through the ring, this step's row directly
@@ -563,13 +576,17 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             OState<FU::EPL> su;
             ostate_init<FU::EPL>(su);
             const int ue = user_static_end(pc, ulen);
-            for (int r = pc.u0; r < ue; r += ucap) {
+            const int warp = threadIdx.x >> 5;
+            const int nst = ue > pc.u0 ? (ue - pc.u0 + ucap - 1) / ucap : 0;
+            for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
+                const int r = pc.u0 + j * ucap;
                 const int n = min(ucap, ue - r);
-                const uint8_t* s = ring_acquire(sm, cu);
+                const uint8_t* s = ring_acquire(sm, cu.k + j);
                 attend_rows_mk<D, 16>(s, s + n * D * 2, nullptr, nullptr, 0, D, n, qreg, su, false);
-                ring_release(sm, cu);
+                ring_release(sm, cu.k + j);
             }
-            if (ulen >= pc.u0 && ulen < pc.u1) {
+            cu.k += nst;
+            if (ulen >= pc.u0 && ulen < pc.u1 && warp == NCW - 1) {
                 const size_t row = (size_t)pc.head * a.cap + ulen;
                 attend_rows_mk<D, 16>((const uint8_t*)(ly.uk + row * D), (const uint8_t*)(ly.uv + row * D),
                                       nullptr, nullptr, 0, D, 1, qreg, su, true);
@@ -677,7 +694,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
-            mbar_init(&sm.empty[i], NCW);
+            mbar_init(&sm.empty[i], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
