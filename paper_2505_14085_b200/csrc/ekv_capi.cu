@@ -1078,12 +1078,13 @@ int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_
         require(s && out && n_out, "null argument");
         require(use_mega(s), "trace: the persistent decode kernel is not active");
         const int G = s->model->ctx->num_sms, L = s->model->cfg.num_layers;
-        const int n = (6 * L + 1) * G;
+        const int n = (6 * L + 1) * G + 16 * G;
         require(capacity >= n, "trace: need " + std::to_string(n) + " entries");
         check_overflow(s, 1);
         set_dev(s->model->ctx);
         cudaStream_t st = s->model->ctx->stream;
         unsigned long long* d = dalloc<unsigned long long>(n);
+        EKV_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long) * n, st));
         MegaArgs a = s->mega;
         a.trace = d;
         launch_decode_mega(a, G, st);

@@ -273,9 +273,9 @@ struct Smem {
     float red_o[NCW][D];       // per-warp partial outputs
     float red_m[NCW], red_l[NCW];
     float fin_m[2], fin_l[2];  // CTA-level (context, user) states of one piece
-    float mw[160], lw[160];    // merge of one head: per contributing CTA (m, l) then weight
     float fin_o[2][D];
-    int s_last;
+    float pm[160][2], pl[160][2];  // head merge: per (CTA, slot) max / sum, then weight
+    int hfirst[160], hlast[160];   // head merge: contributing CTA range per head
 };
 
 // Per-piece schedule pieces that go through the ring: context rows [c0, c1) and
@@ -531,6 +531,14 @@ template <int D, int FMT>
 __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
                                                 Cursor& cu, const AttnPlan& pl, int c, int G,
                                                 int ulen) {
+    unsigned long long* sub =
+        (a.trace && &ly == &a.layer[a.L - 1]) ? a.trace + (size_t)(6 * a.L + 1) * G + (size_t)c * 16 : nullptr;
+    int si = 0;
+    auto stamp = [&] {
+        if (sub && threadIdx.x == 0 && si < 16) sub[si] = gtimer();
+        ++si;
+    };
+    stamp();
     using F = Fmt<D, FMT>;
     using FU = Fmt<D, 16>;
     const int lane = threadIdx.x & 31;
@@ -544,6 +552,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             reinterpret_cast<float4*>(sm.qs[i])[t] =
                 __ldcg(reinterpret_cast<const float4*>(a.q + pl.p[i].head * D) + t);
     consumers_sync();
+    stamp();
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
         {   // context rows (ring)
@@ -566,7 +575,9 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                 ring_release(sm, cu.k + j);
             }
             cu.k += nst;
+            stamp();
             fold_cta<D, FMT>(sm, st, 0);
+            stamp();
         }
         {   // user rows: earlier steps through the ring, this step's row directly
             float qreg[FU::EPL];
@@ -592,6 +603,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                                       nullptr, nullptr, 0, D, 1, qreg, su, true);
             }
             fold_cta<D, 16>(sm, su, 1);
+            stamp();
         }
         // combine (context, user) and publish this CTA's partial for the head
         float* outp = a.ws + ((size_t)c * 2 + i) * (D + 2);
@@ -608,76 +620,68 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
         }
         consumers_sync();
     }
-    // the last CTA to finish a head merges its partials into the attention output
-    const int cuu = ctx_units(a.S), uu = (nuser + UNIT - 1) / UNIT, per = cuu + uu;
+}
+
+// P3 prologue: merge every head's partials (Eq. 5 generalised to the CTAs that
+// attended the head) straight into sm.xs, the input of the output projection.
+// Every CTA does this redundantly from L2 (~50 KB), which replaces a serial
+// last-CTA merge on the attention phase's critical path.
+template <int D>
+__device__ __forceinline__ void merge_heads(const MegaArgs& a, Smem<D>& sm, int G, int nuser) {
+    const int per = ctx_units(a.S) + (nuser + UNIT - 1) / UNIT;
     const long long TU = (long long)a.H * per;
-    for (int i = 0; i < pl.n; ++i) {
-        const int hh = pl.p[i].head;
-        if (threadIdx.x == 0) {
-            __threadfence();
-            const int first = owner((long long)hh * per, G, TU);
-            const int last = owner((long long)(hh + 1) * per - 1, G, TU);
-            unsigned expect = 0;  // CTAs with a non-empty unit range inside [first, last]
-            for (int cc = first; cc <= last; ++cc)
-                expect += ((long long)cc * TU / G) < ((long long)(cc + 1) * TU / G);
-            const unsigned prev = atomicAdd(&a.head_ctr[hh], 1u);
-            sm.s_last = (prev == expect - 1) ? (first + 1) : 0;
-            if (prev == expect - 1) atomicExch(&a.head_ctr[hh], 0u);
+    for (int cc = threadIdx.x; cc < G; cc += NCW * 32) {
+        const long long u0 = (long long)cc * TU / G, u1 = (long long)(cc + 1) * TU / G;
+        for (int sl = 0; sl < 2; ++sl) {
+            float m = -CUDART_INF_F, l = 0.0f;
+            const bool has = u0 < u1 && (sl == 0 || (u1 - 1) / per != u0 / per);
+            if (has) {
+                const float* pp = a.ws + ((size_t)cc * 2 + sl) * (D + 2);
+                m = __ldcg(pp);
+                l = __ldcg(pp + 1);
+                if (!(l > 0.0f)) m = -CUDART_INF_F;
+            }
+            sm.pm[cc][sl] = m;
+            sm.pl[cc][sl] = l;
         }
-        consumers_sync();
-        const int last_flag = sm.s_last;
-        if (last_flag) {
-            __threadfence();
-            const int first = last_flag - 1;
-            const int lastc = owner((long long)(hh + 1) * per - 1, G, TU);
-            const int nc = lastc - first + 1;  // <= G
-            // (m, l) of every contributing CTA -> shared memory, then weights
-            for (int j = threadIdx.x; j < nc; j += NCW * 32) {
-                const int cc = first + j;
-                const long long u0 = (long long)cc * TU / G, u1 = (long long)(cc + 1) * TU / G;
-                float m = -CUDART_INF_F, l = 0.0f;
-                if (u0 < u1) {
-                    const int slot = (int)(u0 / per) == hh ? 0 : 1;
-                    const float* pp = a.ws + ((size_t)cc * 2 + slot) * (D + 2);
-                    m = __ldcg(pp);
-                    l = __ldcg(pp + 1);
-                    if (!(l > 0.0f)) m = -CUDART_INF_F;
-                }
-                sm.mw[j] = m;
-                sm.lw[j] = l;
-            }
-            consumers_sync();
-            if (threadIdx.x < 32) {
-                float M = -CUDART_INF_F;
-                for (int j = threadIdx.x; j < nc; j += 32) M = fmaxf(M, sm.mw[j]);
-                M = warp_max(M);
-                float Ls = 0.0f;
-                for (int j = threadIdx.x; j < nc; j += 32) {
-                    const float w = sm.mw[j] == -CUDART_INF_F ? 0.0f : exp2f((sm.mw[j] - M) * kLog2e);
-                    sm.mw[j] = w;
-                    Ls += sm.lw[j] * w;
-                }
-                Ls = warp_sum(Ls);
-                if (threadIdx.x == 0) sm.fin_l[0] = Ls;
-            }
-            consumers_sync();
-            const float inv = 1.0f / sm.fin_l[0];
-            for (int t = threadIdx.x; t < D; t += NCW * 32) {
-                float O = 0.0f;
-#pragma unroll 4
-                for (int j = 0; j < nc; ++j) {
-                    const float w = sm.mw[j];
-                    if (w != 0.0f) {
-                        const int cc = first + j;
-                        const int slot = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
-                        O += __ldcg(a.ws + ((size_t)cc * 2 + slot) * (D + 2) + 2 + t) * w;
-                    }
-                }
-                a.concat[hh * D + t] = O * inv;
-            }
-        }
-        consumers_sync();
     }
+    consumers_sync();
+    for (int hh = threadIdx.x; hh < a.H; hh += NCW * 32) {
+        const int first = owner((long long)hh * per, G, TU);
+        const int last = owner((long long)(hh + 1) * per - 1, G, TU);
+        float M = -CUDART_INF_F;
+        for (int cc = first; cc <= last; ++cc) {
+            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
+            M = fmaxf(M, sm.pm[cc][sl]);
+        }
+        float Ls = 0.0f;
+        for (int cc = first; cc <= last; ++cc) {
+            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
+            const float w = sm.pm[cc][sl] == -CUDART_INF_F ? 0.0f : exp2f((sm.pm[cc][sl] - M) * kLog2e);
+            sm.pm[cc][sl] = w;  // becomes the merge weight (normalised below)
+            Ls += sm.pl[cc][sl] * w;
+        }
+        const float inv = 1.0f / Ls;
+        for (int cc = first; cc <= last; ++cc) {
+            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
+            sm.pm[cc][sl] *= inv;
+        }
+        sm.hfirst[hh] = first;
+        sm.hlast[hh] = last;
+    }
+    consumers_sync();
+    const int h = a.H * D;
+    for (int e = threadIdx.x; e < h; e += NCW * 32) {
+        const int hh = e / D, c = e - hh * D;
+        float O = 0.0f;
+        for (int cc = sm.hfirst[hh]; cc <= sm.hlast[hh]; ++cc) {
+            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
+            const float w = sm.pm[cc][sl];
+            if (w != 0.0f) O += w * __ldcg(a.ws + ((size_t)cc * 2 + sl) * (D + 2) + 2 + c);
+        }
+        sm.xs[e] = O;
+    }
+    consumers_sync();
 }
 
 template <int D, int KC>
@@ -730,7 +734,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
         else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, ulen);
         grid_sync(a.sync, base + (++nb) * G, tr ? tr + 2 * G : nullptr);
         // ---- P3: output projection ----
-        stage_vector<D>(sm, a.concat, h, nullptr, nullptr, nullptr);
+        merge_heads<D>(a, sm, G, ulen + 1);
         const bool last = l == a.L - 1;
         proj_rows<D, KC>(sm, cu, orows, h, [&](int n, float v) {
             a.x[n] = v;
@@ -798,6 +802,7 @@ static void launch_d(const MegaArgs& a, int grid, int kc, cudaStream_t st) {
 }
 
 void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st) {
+    require(num_sms <= 160, "decode megakernel: at most 160 SMs", EKV_EUNSUPPORTED);
     const int kc = a.H * a.D / 256;
     switch (a.D) {
         case 32: launch_d<32>(a, num_sms, kc, st); break;

@@ -29,3 +29,10 @@ for b in range(3 * L):
     tot[names[b % 3]] += (rel.max() - prev_rel.min()) / 1e3
     prev_rel = rel
 print("phase totals us", {k: round(v, 1) for k, v in tot.items()}, "step us", (bars[-1, 1].max() - t0) / 1e3)
+
+sub = t[(6 * L + 1) * G:].reshape(G, 16)
+rel_p1 = bars[3 * (L - 1), 1]
+for cta in list(np.argsort(-(bars[3 * (L - 1) + 1, 0] - rel_p1))[:4]) + [0, 70]:
+    row = sub[cta]
+    row = row[row > 0]
+    print("cta", cta, "P2 sub-phase us:", np.round(np.diff(np.concatenate([[rel_p1[cta]], row])) / 1e3, 2))
