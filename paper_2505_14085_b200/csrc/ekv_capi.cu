@@ -1078,7 +1078,7 @@ int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_
         require(s && out && n_out, "null argument");
         require(use_mega(s), "trace: the persistent decode kernel is not active");
         const int G = s->model->ctx->num_sms, L = s->model->cfg.num_layers;
-        const int n = (6 * L + 1) * G + 16 * G;
+        const int n = (6 * L + 1) * G + 32 * G;
         require(capacity >= n, "trace: need " + std::to_string(n) + " entries");
         check_overflow(s, 1);
         set_dev(s->model->ctx);

@@ -80,6 +80,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(saddr(bar))
         : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
 }
@@ -161,6 +164,17 @@ __device__ __forceinline__ AttnPlan plan_attention(int c, int G, int H, int S, i
     return pl;
 }
 
+// largest c with floor(c*TU/G) <= unit (32-bit: TU * G < 2^31)
+__device__ __forceinline__ int owner32(int unit, int G, int TU) {
+    int lo = 0, hi = G - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (mid * TU / G <= unit) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 // number of CTAs whose unit range intersects head h (the merge fan-in)
 __device__ __forceinline__ int owner(long long unit, int G, long long TU) {
     // largest c with floor(c*TU/G) <= unit
@@ -181,11 +195,14 @@ struct Fmt {
     static constexpr int RPP = 32 / LPR;
 };
 
+// Rows per attention stage: what fits a slot, capped at ATT_ROWS so a head's
+// chunk spreads over several consumer warps.
+constexpr int ATT_ROWS = 64;
 __device__ __forceinline__ int att_stage_rows(int row_bytes, int ng) {
     const int per = 2 * (row_bytes + ng * 4);
     int r = STAGE / per;
     r -= r % UNIT;
-    return r;
+    return r < ATT_ROWS ? r : ATT_ROWS;
 }
 
 // ---------------------------------------------------------------------------
@@ -270,13 +287,26 @@ struct Smem {
     uint64_t empty[NST];
     float xs[2048];            // phase input (x or the attention output)
     float qs[2][D];            // q of the (<= 2) heads of this CTA's attention pieces
-    float red_o[NCW][D];       // per-warp partial outputs
-    float red_m[NCW], red_l[NCW];
-    float fin_m[2], fin_l[2];  // CTA-level (context, user) states of one piece
-    float fin_o[2][D];
-    float pm[160][2], pl[160][2];  // head merge: per (CTA, slot) max / sum, then weight
+    uint16_t nk[2][D], nv[2][D];  // this step's user K/V row of those heads (bf16)
+    float ws_o[2][2][NCW][D];  // per (piece, context/user, warp) partial output
+    float ws_m[2][2][NCW], ws_l[2][2][NCW];
+    int merge_heads_n;         // heads this CTA must merge (last to finish them)
+    int merge_head[2];
     int hfirst[160], hlast[160];   // head merge: contributing CTA range per head
+    int hcount[160];               // head merge: number of contributing (non-idle) CTAs
+    int ch0[160];                  // head merge: first head of each CTA (-1: idle CTA)
+    int trace_on;
+    int phase_id;
+    unsigned long long wait_cycles[4];
 };
+
+// Diagnostics: %globaltimer stamps of sub-phases of the last layer
+// (trace region [(6L+1)G + 32c + idx]).
+template <int D>
+__device__ __forceinline__ void stamp(const MegaArgs& a, Smem<D>& sm, int idx) {
+    if (a.trace && sm.trace_on && threadIdx.x == 0)
+        a.trace[(size_t)(6 * a.L + 1) * gridDim.x + (size_t)blockIdx.x * 32 + idx] = gtimer();
+}
 
 // Per-piece schedule pieces that go through the ring: context rows [c0, c1) and
 // the static user rows [u0, min(u1, ulen)) (written by earlier steps).
@@ -301,8 +331,38 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen) 
     const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
     const int rows_per_w = STAGE / (h * 2);  // weight rows per stage
     const int ucap = att_stage_rows(D * 2, 0);
+    // HBM -> L2 prefetch of one layer's stream of this CTA.  Issued a layer
+    // ahead, it keeps HBM busy while the consumers sit in grid barriers and the
+    // ring is full; the ring then refills from L2.
+    auto prefetch_layer = [&](int l) {
+        if (l >= a.L) return;
+        const MegaLayer& ly = a.layer[l];
+        prefetch_l2(ly.wqkv + (size_t)q.r0 * h, (uint32_t)(q.r1 - q.r0) * h * 2);
+        const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
+        const int ng = ly.fmt == 16 ? 0 : D / ly.group;
+        for (int i = 0; i < pl.n; ++i) {
+            const Piece& pc = pl.p[i];
+            const size_t base = (size_t)pc.head * a.S + pc.c0;
+            const uint32_t n = pc.c1 - pc.c0;
+            prefetch_l2(ly.ck + base * row_b, n * row_b);
+            prefetch_l2(ly.cv + base * row_b, n * row_b);
+            if (ng) {
+                prefetch_l2(ly.cks + base * ng, n * ng * 4);
+                prefetch_l2(ly.cvs + base * ng, n * ng * 4);
+            }
+            const int ue = user_static_end(pc, ulen);
+            if (ue > pc.u0) {
+                const size_t ub = (size_t)pc.head * a.cap + pc.u0;
+                prefetch_l2(ly.uk + ub * D, (uint32_t)(ue - pc.u0) * D * 2);
+                prefetch_l2(ly.uv + ub * D, (uint32_t)(ue - pc.u0) * D * 2);
+            }
+        }
+        prefetch_l2(ly.wo + (size_t)o.r0 * h, (uint32_t)(o.r1 - o.r0) * h * 2);
+    };
+    prefetch_layer(0);
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
+        prefetch_layer(l + 1);
         for (int r = q.r0; r < q.r1; r += rows_per_w) {
             const int n = min(rows_per_w, q.r1 - r);
             next(n * h * 2);
@@ -362,7 +422,9 @@ struct Cursor {
 
 template <int D>
 __device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, long long k) {
+    const long long t0 = clock64();
     mbar_wait(&sm.full[k % NST], (uint32_t)((k / NST) & 1));
+    if (sm.trace_on && (threadIdx.x & 31) == 0) atomicAdd(&sm.wait_cycles[sm.phase_id], (unsigned long long)(clock64() - t0));
     return sm.ring[k % NST];
 }
 template <int D>
@@ -437,54 +499,87 @@ __device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, i
     cu.k += nst;
 }
 
-// Attention of q over n rows (ring stage or global), into this lane's state.
+// Attention of q over n <= ATT_ROWS rows (a ring stage, or global memory for
+// this step's user row) owned by the calling warp, into this lane's state.
+// Two passes per stage: all logits of the lane-group's rows first (registers),
+// then one rescale of the running state and one exp per row.
 template <int D, int FMT>
 __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t* vb, const float* ks,
                                                const float* vs, int ng, int group, int n,
                                                const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
                                                bool global_src) {
     using F = Fmt<D, FMT>;
+    constexpr int MAXR = (ATT_ROWS + F::RPP - 1) / F::RPP;  // rows per lane group per stage
     const int lane = threadIdx.x & 31;
     const int sub = lane % F::LPR, rsub = lane / F::LPR;
     const int grp = FMT == 16 ? 0 : (sub * F::EPL) / group;
-    for (int base = 0; base < n; base += F::RPP) {  // the calling warp owns all n rows
-        const int row = base + rsub;
-        const bool ok = row < n;
-        uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-        float ksc = 1.0f, vsc = 1.0f;
-        if (ok) {
+    // pass 1: lane-partial dots of every row (independent LDS + FMA chains),
+    // then the LPR-lane reductions of all rows together (independent shuffles)
+    float lg[MAXR];
+#pragma unroll
+    for (int p = 0; p < MAXR; ++p) {
+        const int row = p * F::RPP + rsub;
+        lg[p] = 0.0f;
+        if (p * F::RPP < n && row < n) {
             const uint8_t* kp = kb + (size_t)row * F::ROW + sub * 16;
-            const uint8_t* vp = vb + (size_t)row * F::ROW + sub * 16;
-            if (global_src) {
-                kv = __ldcg(reinterpret_cast<const uint4*>(kp));
-                vv = __ldcg(reinterpret_cast<const uint4*>(vp));
-            } else {
-                kv = *reinterpret_cast<const uint4*>(kp);
-                vv = *reinterpret_cast<const uint4*>(vp);
+            const uint4 kv = global_src ? __ldcg(reinterpret_cast<const uint4*>(kp))
+                                        : *reinterpret_cast<const uint4*>(kp);
+            float f[F::EPL];
+            expand16<FMT>(kv, f);
+            float d0 = 0.0f, d1 = 0.0f;
+#pragma unroll
+            for (int e = 0; e < F::EPL; e += 2) {
+                d0 = fmaf(qreg[e], f[e], d0);
+                d1 = fmaf(qreg[e + 1], f[e + 1], d1);
             }
-            if constexpr (FMT != 16) {
-                ksc = ks[(size_t)row * ng + grp];
-                vsc = vs[(size_t)row * ng + grp];
-            }
+            float dot = d0 + d1;
+            if constexpr (FMT != 16) dot *= ks[(size_t)row * ng + grp];
+            lg[p] = dot;
         }
-        float f[F::EPL];
-        expand16<FMT>(kv, f);
-        float dot = 0.0f;
+    }
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) dot = fmaf(qreg[e], f[e], dot);
-        dot *= ksc;
+    for (int o = F::LPR >> 1; o > 0; o >>= 1)
 #pragma unroll
-        for (int o = F::LPR >> 1; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (ok) {
+        for (int p = 0; p < MAXR; ++p)
+            if (p * F::RPP < n) lg[p] += __shfl_xor_sync(0xffffffffu, lg[p], o);
+    float mx = -CUDART_INF_F;
+#pragma unroll
+    for (int p = 0; p < MAXR; ++p) {
+        const int row = p * F::RPP + rsub;
+        if (p * F::RPP < n && row < n) mx = fmaxf(mx, lg[p]);
+    }
+    if (mx == -CUDART_INF_F) return;  // no rows for this lane group
+    const float mn = fmaxf(st.m, mx);
+    const float corr = exp2f((st.m - mn) * kLog2e);
+    st.l *= corr;
+#pragma unroll
+    for (int e = 0; e < F::EPL; ++e) st.o[e] *= corr;
+    st.m = mn;
+#pragma unroll
+    for (int p = 0; p < MAXR; ++p) {
+        const int row = p * F::RPP + rsub;
+        if (p * F::RPP < n && row < n) {
+            const float pr = exp2f((lg[p] - mn) * kLog2e);
+            const uint8_t* vp = vb + (size_t)row * F::ROW + sub * 16;
+            const uint4 vv = global_src ? __ldcg(reinterpret_cast<const uint4*>(vp))
+                                        : *reinterpret_cast<const uint4*>(vp);
+            float vsc = 1.0f;
+            if constexpr (FMT != 16) vsc = vs[(size_t)row * ng + grp];
+            float f[F::EPL];
             expand16<FMT>(vv, f);
-            ostate_add<F::EPL>(st, dot, f, vsc);
+            st.l += pr;
+            const float pv = pr * vsc;
+#pragma unroll
+            for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
         }
     }
 }
 
-// Fold every lane-group state of the CTA into sm.fin_*[which] (m, l, o[D]).
+// Fold the lane-group states of this warp (xor over the row-subgroup lane
+// bits) and park the warp's (m, l, o[D]) in shared memory slot [piece][kind].
 template <int D, int FMT>
-__device__ __forceinline__ void fold_cta(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& st, int which) {
+__device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& st, int piece,
+                                                int kind) {
     using F = Fmt<D, FMT>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = lane % F::LPR;
@@ -498,61 +593,94 @@ __device__ __forceinline__ void fold_cta(Smem<D>& sm, OState<Fmt<D, FMT>::EPL>& 
     }
     if (lane < F::LPR) {
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) sm.red_o[warp][sub * F::EPL + e] = st.o[e];
-        if (lane == 0) {
-            sm.red_m[warp] = st.m;
-            sm.red_l[warp] = st.l;
-        }
+        for (int e = 0; e < F::EPL; ++e) sm.ws_o[piece][kind][warp][sub * F::EPL + e] = st.o[e];
     }
-    consumers_sync();
-    for (int t = threadIdx.x; t < D; t += NCW * 32) {
-        float M = -CUDART_INF_F;
+    if (lane == 0) {
+        sm.ws_m[piece][kind][warp] = st.m;
+        sm.ws_l[piece][kind][warp] = st.l;
+    }
+}
+
+// Merge of one head's partials by one warp (Eq. 5 generalised to the CTAs
+// that attended the head): every load issued before any use, shuffle-free
+// per-lane math (each lane owns D/32 output columns), result to a.concat.
+template <int D>
+__device__ __forceinline__ void merge_one_head(const MegaArgs& a, Smem<D>& sm, int hh) {
+    constexpr int MAXC = 8;
+    constexpr int VPL = (D + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    const int first = sm.hfirst[hh], last = sm.hlast[hh];
+    float M = -CUDART_INF_F, Ls = 0.0f, O[VPL];
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) M = fmaxf(M, sm.red_m[w]);
-        float Ls = 0.0f, O = 0.0f;
-        if (M != -CUDART_INF_F) {
+    for (int t = 0; t < VPL; ++t) O[t] = 0.0f;
+    for (int c0 = first; c0 <= last; c0 += MAXC) {
+        float m[MAXC], l[MAXC], v[MAXC][VPL];
 #pragma unroll
-            for (int w = 0; w < NCW; ++w) {
-                const float sc = exp2f((sm.red_m[w] - M) * kLog2e);
-                Ls += sm.red_l[w] * sc;
-                O += sm.red_o[w][t] * sc;
+        for (int j = 0; j < MAXC; ++j) {
+            const int cc = c0 + j;
+            const bool ok = cc <= last && sm.ch0[cc] >= 0;
+            const int sl = ok && sm.ch0[cc] == hh ? 0 : 1;
+            const float* pp = a.ws + ((size_t)(ok ? cc : first) * 2 + sl) * (D + 2);
+            m[j] = ok ? __ldcg(pp) : -CUDART_INF_F;
+            l[j] = ok ? __ldcg(pp + 1) : 0.0f;
+#pragma unroll
+            for (int t = 0; t < VPL; ++t) {
+                const int cix = lane + 32 * t;
+                v[j][t] = (ok && cix < D) ? __ldcg(pp + 2 + cix) : 0.0f;
             }
         }
-        sm.fin_o[which][t] = O;
-        if (t == 0) {
-            sm.fin_m[which] = M;
-            sm.fin_l[which] = Ls;
+        float Mn = M;
+#pragma unroll
+        for (int j = 0; j < MAXC; ++j)
+            if (l[j] > 0.0f) Mn = fmaxf(Mn, m[j]);
+        const float corr = M == -CUDART_INF_F ? 0.0f : exp2f((M - Mn) * kLog2e);
+        Ls *= corr;
+#pragma unroll
+        for (int t = 0; t < VPL; ++t) O[t] *= corr;
+#pragma unroll
+        for (int j = 0; j < MAXC; ++j) {
+            const float w = l[j] > 0.0f ? exp2f((m[j] - Mn) * kLog2e) : 0.0f;
+            Ls += l[j] * w;
+#pragma unroll
+            for (int t = 0; t < VPL; ++t) O[t] += w * v[j][t];
         }
+        M = Mn;
     }
-    consumers_sync();
+    const float inv = 1.0f / Ls;
+#pragma unroll
+    for (int t = 0; t < VPL; ++t) {
+        const int cix = lane + 32 * t;
+        if (cix < D) a.concat[hh * D + cix] = O[t] * inv;
+    }
 }
 
 template <int D, int FMT>
 __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
                                                 Cursor& cu, const AttnPlan& pl, int c, int G,
                                                 int ulen) {
-    unsigned long long* sub =
-        (a.trace && &ly == &a.layer[a.L - 1]) ? a.trace + (size_t)(6 * a.L + 1) * G + (size_t)c * 16 : nullptr;
-    int si = 0;
-    auto stamp = [&] {
-        if (sub && threadIdx.x == 0 && si < 16) sub[si] = gtimer();
-        ++si;
-    };
-    stamp();
+    stamp(a, sm, 10);
     using F = Fmt<D, FMT>;
     using FU = Fmt<D, 16>;
-    const int lane = threadIdx.x & 31;
-    const int nuser = ulen + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ng = FMT == 16 ? 0 : D / ly.group;
     const int cap = att_stage_rows(F::ROW, ng);
     const int ucap = att_stage_rows(D * 2, 0);
-    // q of the heads this CTA attends (written by P1 on other CTAs)
-    for (int i = 0; i < pl.n; ++i)
+    // q and this step's user K/V row of the heads this CTA attends (written by
+    // P1 on other CTAs): one round of coherent loads into shared memory
+    for (int i = 0; i < pl.n; ++i) {
         for (int t = threadIdx.x; t < D / 4; t += NCW * 32)
             reinterpret_cast<float4*>(sm.qs[i])[t] =
                 __ldcg(reinterpret_cast<const float4*>(a.q + pl.p[i].head * D) + t);
+        if (ulen >= pl.p[i].u0 && ulen < pl.p[i].u1) {
+            const size_t row = ((size_t)pl.p[i].head * a.cap + ulen) * D;
+            for (int t = threadIdx.x; t < D / 8; t += NCW * 32) {
+                reinterpret_cast<uint4*>(sm.nk[i])[t] = __ldcg(reinterpret_cast<const uint4*>(ly.uk + row) + t);
+                reinterpret_cast<uint4*>(sm.nv[i])[t] = __ldcg(reinterpret_cast<const uint4*>(ly.uv + row) + t);
+            }
+        }
+    }
     consumers_sync();
-    stamp();
+    stamp(a, sm, 11);
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
         {   // context rows (ring)
@@ -562,7 +690,6 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
             OState<F::EPL> st;
             ostate_init<F::EPL>(st);
-            const int warp = threadIdx.x >> 5;
             const int nst = (pc.c1 - pc.c0 + cap - 1) / cap;
             for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
                 const int r = pc.c0 + j * cap;
@@ -575,9 +702,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                 ring_release(sm, cu.k + j);
             }
             cu.k += nst;
-            stamp();
-            fold_cta<D, FMT>(sm, st, 0);
-            stamp();
+            park_warp_state<D, FMT>(sm, st, i, 0);
         }
         {   // user rows: earlier steps through the ring, this step's row directly
             float qreg[FU::EPL];
@@ -587,7 +712,6 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             OState<FU::EPL> su;
             ostate_init<FU::EPL>(su);
             const int ue = user_static_end(pc, ulen);
-            const int warp = threadIdx.x >> 5;
             const int nst = ue > pc.u0 ? (ue - pc.u0 + ucap - 1) / ucap : 0;
             for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
                 const int r = pc.u0 + j * ucap;
@@ -597,89 +721,86 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                 ring_release(sm, cu.k + j);
             }
             cu.k += nst;
-            if (ulen >= pc.u0 && ulen < pc.u1 && warp == NCW - 1) {
-                const size_t row = (size_t)pc.head * a.cap + ulen;
-                attend_rows_mk<D, 16>((const uint8_t*)(ly.uk + row * D), (const uint8_t*)(ly.uv + row * D),
-                                      nullptr, nullptr, 0, D, 1, qreg, su, true);
-            }
-            fold_cta<D, 16>(sm, su, 1);
-            stamp();
+            if (ulen >= pc.u0 && ulen < pc.u1 && warp == (int)((cu.k + i) % NCW))
+                attend_rows_mk<D, 16>((const uint8_t*)sm.nk[i], (const uint8_t*)sm.nv[i], nullptr,
+                                      nullptr, 0, D, 1, qreg, su, false);
+            park_warp_state<D, 16>(sm, su, i, 1);
         }
-        // combine (context, user) and publish this CTA's partial for the head
-        float* outp = a.ws + ((size_t)c * 2 + i) * (D + 2);
-        for (int t = threadIdx.x; t < D; t += NCW * 32) {
-            const float m1 = sm.fin_m[0], l1 = sm.fin_l[0], m2 = sm.fin_m[1], l2 = sm.fin_l[1];
-            const float M = fmaxf(m1, m2);
-            const float s1 = (l1 > 0.0f) ? exp2f((m1 - M) * kLog2e) : 0.0f;
-            const float s2 = (l2 > 0.0f) ? exp2f((m2 - M) * kLog2e) : 0.0f;
-            outp[2 + t] = sm.fin_o[0][t] * s1 + sm.fin_o[1][t] * s2;
-            if (t == 0) {
-                outp[0] = M;
-                outp[1] = l1 * s1 + l2 * s2;
-            }
-        }
-        consumers_sync();
     }
+    consumers_sync();
+    stamp(a, sm, 12);
+    // one CTA-level fold of every (piece, kind, warp) state -> this CTA's partials
+    for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
+        const int i = t / D, cix = t - i * D;
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int w = 0; w < NCW; ++w)
+                if (sm.ws_l[i][k][w] > 0.0f) M = fmaxf(M, sm.ws_m[i][k][w]);
+        float Ls = 0.0f, O = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) {
+                const float l = sm.ws_l[i][k][w];
+                if (l > 0.0f) {
+                    const float sc = exp2f((sm.ws_m[i][k][w] - M) * kLog2e);
+                    Ls += l * sc;
+                    O += sm.ws_o[i][k][w][cix] * sc;
+                }
+            }
+        float* outp = a.ws + ((size_t)c * 2 + i) * (D + 2);
+        outp[2 + cix] = O;
+        if (cix == 0) {
+            outp[0] = M;
+            outp[1] = Ls;
+        }
+    }
+    consumers_sync();
+    // publish; the last CTA to finish a head merges it (one warp per head, every
+    // load of the merge in flight at once) into the attention output
+    if (threadIdx.x == 0) {
+        int nm = 0;
+        for (int i = 0; i < pl.n; ++i) {
+            const int hh = pl.p[i].head;
+            unsigned prev;
+            // release: this CTA's partials (ordered by the bar.sync above);
+            // acquire: every other contributor's partials for the merger
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                         : "=r"(prev) : "l"(&a.head_ctr[hh]) : "memory");
+            if (prev == (unsigned)sm.hcount[hh] - 1) {
+                a.head_ctr[hh] = 0u;  // re-arm (next use is after a grid barrier)
+                sm.merge_head[nm++] = hh;
+            }
+        }
+        sm.merge_heads_n = nm;
+    }
+    consumers_sync();
+    stamp(a, sm, 13);
+    if (warp < sm.merge_heads_n) merge_one_head<D>(a, sm, sm.merge_head[warp]);
+    consumers_sync();
+    stamp(a, sm, 14);
 }
 
-// P3 prologue: merge every head's partials (Eq. 5 generalised to the CTAs that
-// attended the head) straight into sm.xs, the input of the output projection.
-// Every CTA does this redundantly from L2 (~50 KB), which replaces a serial
-// last-CTA merge on the attention phase's critical path.
+// Per-step merge topology (depends only on the step's user length): the first
+// head of every CTA's unit range and the contiguous CTA range attending each head.
 template <int D>
-__device__ __forceinline__ void merge_heads(const MegaArgs& a, Smem<D>& sm, int G, int nuser) {
+__device__ __forceinline__ void plan_merge(const MegaArgs& a, Smem<D>& sm, int G, int nuser) {
     const int per = ctx_units(a.S) + (nuser + UNIT - 1) / UNIT;
-    const long long TU = (long long)a.H * per;
+    const int TU = a.H * per;  // < 2^31 / G for every supported shape (checked at launch)
     for (int cc = threadIdx.x; cc < G; cc += NCW * 32) {
-        const long long u0 = (long long)cc * TU / G, u1 = (long long)(cc + 1) * TU / G;
-        for (int sl = 0; sl < 2; ++sl) {
-            float m = -CUDART_INF_F, l = 0.0f;
-            const bool has = u0 < u1 && (sl == 0 || (u1 - 1) / per != u0 / per);
-            if (has) {
-                const float* pp = a.ws + ((size_t)cc * 2 + sl) * (D + 2);
-                m = __ldcg(pp);
-                l = __ldcg(pp + 1);
-                if (!(l > 0.0f)) m = -CUDART_INF_F;
-            }
-            sm.pm[cc][sl] = m;
-            sm.pl[cc][sl] = l;
-        }
+        const int u0 = cc * TU / G, u1 = (cc + 1) * TU / G;
+        sm.ch0[cc] = u0 < u1 ? u0 / per : -1;
     }
     consumers_sync();
     for (int hh = threadIdx.x; hh < a.H; hh += NCW * 32) {
-        const int first = owner((long long)hh * per, G, TU);
-        const int last = owner((long long)(hh + 1) * per - 1, G, TU);
-        float M = -CUDART_INF_F;
-        for (int cc = first; cc <= last; ++cc) {
-            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
-            M = fmaxf(M, sm.pm[cc][sl]);
-        }
-        float Ls = 0.0f;
-        for (int cc = first; cc <= last; ++cc) {
-            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
-            const float w = sm.pm[cc][sl] == -CUDART_INF_F ? 0.0f : exp2f((sm.pm[cc][sl] - M) * kLog2e);
-            sm.pm[cc][sl] = w;  // becomes the merge weight (normalised below)
-            Ls += sm.pl[cc][sl] * w;
-        }
-        const float inv = 1.0f / Ls;
-        for (int cc = first; cc <= last; ++cc) {
-            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
-            sm.pm[cc][sl] *= inv;
-        }
-        sm.hfirst[hh] = first;
-        sm.hlast[hh] = last;
-    }
-    consumers_sync();
-    const int h = a.H * D;
-    for (int e = threadIdx.x; e < h; e += NCW * 32) {
-        const int hh = e / D, c = e - hh * D;
-        float O = 0.0f;
-        for (int cc = sm.hfirst[hh]; cc <= sm.hlast[hh]; ++cc) {
-            const int sl = (int)(((long long)cc * TU / G) / per) == hh ? 0 : 1;
-            const float w = sm.pm[cc][sl];
-            if (w != 0.0f) O += w * __ldcg(a.ws + ((size_t)cc * 2 + sl) * (D + 2) + 2 + c);
-        }
-        sm.xs[e] = O;
+        const int f = owner32(hh * per, G, TU), l = owner32((hh + 1) * per - 1, G, TU);
+        int n = 0;
+        for (int cc = f; cc <= l; ++cc) n += sm.ch0[cc] >= 0;
+        sm.hfirst[hh] = f;
+        sm.hlast[hh] = l;
+        sm.hcount[hh] = n;
     }
     consumers_sync();
 }
@@ -710,13 +831,22 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     Cursor cu;
     const Split qrows = rows_of(c, G, 3 * h), orows = rows_of(c, G, h);
     const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
+    plan_merge<D>(a, sm, G, ulen + 1);
     unsigned long long nb = 0;  // barriers passed in this launch
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
         unsigned long long* tr = a.trace ? a.trace + (size_t)(3 * l) * 2 * G : nullptr;
         // ---- P1: QKV (input transform fused at layer 0) ----
+        if (threadIdx.x == 0) {
+            sm.trace_on = (l == a.L - 1);
+            sm.phase_id = 0;
+            for (int i = 0; i < 4; ++i) sm.wait_cycles[i] = 0;
+        }
+        consumers_sync();
+        stamp(a, sm, 0);
         stage_vector<D>(sm, a.x, h, a.gamma, a.bias,
                         l == 0 ? a.pos + (size_t)(a.S + ulen) * h : nullptr);
+        stamp(a, sm, 1);
         proj_rows<D, KC>(sm, cu, qrows, h, [&](int n, float v) {
             const int part = n / h, rem = n - part * h;
             if (part == 0) {
@@ -727,19 +857,29 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
                 dst[((size_t)head * a.cap + ulen) * D + cix] = f32_to_bf16_bits(v);
             }
         });
+        stamp(a, sm, 3);
         grid_sync(a.sync, base + (++nb) * G, tr);
+        if (threadIdx.x == 0) sm.phase_id = 1;
         // ---- P2: attention ----
         if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, ulen);
         else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, ulen);
         else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, ulen);
         grid_sync(a.sync, base + (++nb) * G, tr ? tr + 2 * G : nullptr);
         // ---- P3: output projection ----
-        merge_heads<D>(a, sm, G, ulen + 1);
+        if (threadIdx.x == 0) sm.phase_id = 2;
+        stamp(a, sm, 20);
+        stage_vector<D>(sm, a.concat, h, nullptr, nullptr, nullptr);
+        stamp(a, sm, 21);
         const bool last = l == a.L - 1;
         proj_rows<D, KC>(sm, cu, orows, h, [&](int n, float v) {
             a.x[n] = v;
             if (last) a.hist[(size_t)step * h + n] = v;
         });
+        stamp(a, sm, 22);
+        if (sm.trace_on && threadIdx.x == 0 && a.trace)
+            for (int i = 0; i < 3; ++i)
+                a.trace[(size_t)(6 * a.L + 1) * G + (size_t)c * 32 + 28 + i] = sm.wait_cycles[i];
+
         grid_sync(a.sync, base + (++nb) * G, tr ? tr + 4 * G : nullptr);
     }
     if (c == 0 && threadIdx.x == 0) {

@@ -30,9 +30,16 @@ for b in range(3 * L):
     prev_rel = rel
 print("phase totals us", {k: round(v, 1) for k, v in tot.items()}, "step us", (bars[-1, 1].max() - t0) / 1e3)
 
-sub = t[(6 * L + 1) * G:].reshape(G, 16)
-rel_p1 = bars[3 * (L - 1), 1]
-for cta in list(np.argsort(-(bars[3 * (L - 1) + 1, 0] - rel_p1))[:4]) + [0, 70]:
+sub = t[(6 * L + 1) * G:].reshape(G, 32).astype(np.int64)
+names = {0: "P1 start", 1: "x staged", 3: "qkv done", 10: "P2 start", 11: "q staged", 12: "rows done",
+         13: "partials+atomics", 14: "merge", 20: "P3 start", 21: "concat staged", 22: "out proj done"}
+for cta in [0, 18, 70, 120]:
     row = sub[cta]
-    row = row[row > 0]
-    print("cta", cta, "P2 sub-phase us:", np.round(np.diff(np.concatenate([[rel_p1[cta]], row])) / 1e3, 2))
+    out = []
+    prev = None
+    for k in sorted(names):
+        if row[k] > 0:
+            if prev is not None:
+                out.append(f"{names[k]} +{(row[k] - prev) / 1e3:.2f}")
+            prev = row[k]
+    print("cta", cta, "| ".join(out), "| ring-wait cycles (sum over warps) P1/P2/P3:", row[28:31])
