@@ -72,6 +72,14 @@ int ekv_ctx_synchronize(ekv_ctx_t ctx);
  * count every kernel node). */
 int ekv_ctx_kernel_launches(ekv_ctx_t ctx, int64_t* count);
 
+/* Device memory helpers for hosts that do not link the CUDA runtime (the C++
+ * mirror): allocation on the context's device, and synchronous copies on the
+ * context stream.  kind: 0 host->device, 1 device->host, 2 device->device. */
+int ekv_device_alloc(ekv_ctx_t ctx, size_t bytes, void** out);
+int ekv_device_free(ekv_ctx_t ctx, void* p);
+int ekv_memset(ekv_ctx_t ctx, void* dst_dev, int value, size_t bytes);
+int ekv_copy(ekv_ctx_t ctx, void* dst, const void* src, size_t bytes, int kind);
+
 /* Counter-hash synthetic data (bit-identical to oracle ekvo_fill_uniform_bf16):
  * dst[i] = bf16_rn(lo + (hi-lo) * ((mix(mix(seed,stream_id), i) >> 11) * 2^-53)),
  * mix = Rng::mix (rng.hpp:35-40). */
@@ -127,6 +135,11 @@ int ekv_match_layers(const double* edge_outs, int me, int ce, const double* clou
  * src dev bf16 [rows][d_c], kept dev int32 [d_e], dst dev bf16 [rows][d_e]. */
 int ekv_kv_gather(ekv_ctx_t ctx, const void* src_dev, int64_t rows, int d_c,
                   const int* kept_dev, int d_e, void* dst_dev);
+
+/* The same column gather for 2-, 4- or 8-byte elements (e.g. fp64 caches of
+ * the C++ mirror, where prune_cache must stay an exact copy). */
+int ekv_gather_columns(ekv_ctx_t ctx, const void* src_dev, int64_t rows, int d_c,
+                       const int* kept_dev, int d_e, int elem_bytes, void* dst_dev);
 
 /* K3: gather kept channels, quantise, pack (no reference -- SPEC.md:281, 488;
  * contract in DESIGN.md section 3, restated in oracle/ekv_oracle.c):

@@ -47,6 +47,10 @@ PROTOS = {
     "ekv_ctx_stream": [_vp, _pp],
     "ekv_ctx_synchronize": [_vp],
     "ekv_ctx_kernel_launches": [_vp, C.POINTER(C.c_int64)],
+    "ekv_device_alloc": [_vp, C.c_size_t, _pp],
+    "ekv_device_free": [_vp, _vp],
+    "ekv_memset": [_vp, _vp, _i, C.c_size_t],
+    "ekv_copy": [_vp, _vp, _vp, C.c_size_t, _i],
     "ekv_fill_uniform_bf16": [_vp, _vp, _i64, _u64, _u64, _d, _d],
     "ekv_prune_retained": [_d, _i, _ip],
     "ekv_align_qnorm": [_vp, _vp, _vp, _i, _i, _i, _i, _vp],
@@ -54,6 +58,7 @@ PROTOS = {
     "ekv_rank_channels": [_dp, _dp, _i, _i, _ip, _dp],
     "ekv_match_layers": [_dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
     "ekv_kv_gather": [_vp, _vp, _i64, _i, _vp, _i, _vp],
+    "ekv_gather_columns": [_vp, _vp, _i64, _i, _vp, _i, _i, _vp],
     "ekv_kv_compress": [_vp, _vp, _i64, _i, _vp, _i, _i, _i, _vp, _vp],
     "ekv_kv_compress_batched": [_vp, _i, _pp, _i64, _i, _vp, _i, _i, _i, _pp, _pp],
     "ekv_kv_dequant": [_vp, _vp, _vp, _i64, _i, _i, _i, _vp],

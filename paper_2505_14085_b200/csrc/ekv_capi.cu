@@ -460,6 +460,43 @@ int ekv_ctx_kernel_launches(ekv_ctx_t c, int64_t* count) {
     });
 }
 
+int ekv_device_alloc(ekv_ctx_t c, size_t bytes, void** out) {
+    return guard([&] {
+        require(c && out, "ekv_device_alloc: null argument");
+        set_dev(c);
+        *out = dalloc<uint8_t>(bytes);
+    });
+}
+
+int ekv_device_free(ekv_ctx_t c, void* p) {
+    return guard([&] {
+        require(c != nullptr, "null context");
+        set_dev(c);
+        EKV_CUDA(cudaFree(p));
+    });
+}
+
+int ekv_memset(ekv_ctx_t c, void* dst, int value, size_t bytes) {
+    return guard([&] {
+        require(c && (dst || bytes == 0), "ekv_memset: null argument");
+        set_dev(c);
+        EKV_CUDA(cudaMemsetAsync(dst, value, bytes, c->stream));
+        EKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int ekv_copy(ekv_ctx_t c, void* dst, const void* src, size_t bytes, int kind) {
+    return guard([&] {
+        require(c && ((dst && src) || bytes == 0), "ekv_copy: null argument");
+        require(kind >= 0 && kind <= 2, "ekv_copy: kind must be 0, 1 or 2");
+        set_dev(c);
+        const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                           : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+        EKV_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c->stream));
+        EKV_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
 int ekv_fill_uniform_bf16(ekv_ctx_t c, void* dst, int64_t n, uint64_t seed, uint64_t stream_id,
                           double lo, double hi) {
     return guard([&] {
@@ -659,6 +696,15 @@ int ekv_kv_gather(ekv_ctx_t c, const void* src, int64_t rows, int d_c, const int
         check_rows_args(c, src, dst, rows, d_c, kept, d_e, "ekv_kv_gather");
         set_dev(c);
         launch_kv_gather(src, rows, d_c, kept, d_e, dst, c->stream);
+    });
+}
+
+int ekv_gather_columns(ekv_ctx_t c, const void* src, int64_t rows, int d_c, const int* kept,
+                       int d_e, int elem_bytes, void* dst) {
+    return guard([&] {
+        check_rows_args(c, src, dst, rows, d_c, kept, d_e, "ekv_gather_columns");
+        set_dev(c);
+        launch_gather_columns(src, rows, d_c, kept, d_e, elem_bytes, dst, c->stream);
     });
 }
 

@@ -31,6 +31,8 @@ void launch_kv_compress(const void* src, int64_t rows, int d_c, const int* kept,
                         int group, void* codes, float* scales, cudaStream_t st);
 void launch_kv_gather(const void* src, int64_t rows, int d_c, const int* kept, int d_e, void* dst,
                       cudaStream_t st);
+void launch_gather_columns(const void* src, int64_t rows, int d_c, const int* kept, int d_e,
+                           int elem_bytes, void* dst, cudaStream_t st);
 void launch_kv_dequant(const void* codes, const float* scales, int64_t rows, int d_e, int bits,
                        int group, void* dst, cudaStream_t st);
 void launch_kv_colnorm(const void* K, int64_t rows, int d_c, double* colsq, cudaStream_t st);

@@ -293,6 +293,30 @@ __global__ void kv_gather_kernel(const uint16_t* __restrict__ src, int64_t rows,
     }
 }
 
+template <class T>
+__global__ void gather_columns_kernel(const T* __restrict__ src, int64_t rows, int d_c,
+                                      const int* __restrict__ kept, int d_e, T* __restrict__ dst) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * d_e;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = t / d_e;
+        dst[t] = src[row * d_c + kept[t - row * d_e]];
+    }
+}
+
+void launch_gather_columns(const void* src, int64_t rows, int d_c, const int* kept, int d_e,
+                           int elem_bytes, void* dst, cudaStream_t st) {
+    if (rows <= 0) return;
+    const int g = grid_for(rows * d_e, 256);
+    switch (elem_bytes) {
+        case 2: gather_columns_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)src, rows, d_c, kept, d_e, (uint16_t*)dst); break;
+        case 4: gather_columns_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)src, rows, d_c, kept, d_e, (uint32_t*)dst); break;
+        case 8: gather_columns_kernel<uint64_t><<<g, 256, 0, st>>>((const uint64_t*)src, rows, d_c, kept, d_e, (uint64_t*)dst); break;
+        default: require(false, "gather_columns: element size must be 2, 4 or 8 bytes");
+    }
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
 void launch_kv_gather(const void* src, int64_t rows, int d_c, const int* kept, int d_e, void* dst,
                       cudaStream_t st) {
     if (rows <= 0) return;
