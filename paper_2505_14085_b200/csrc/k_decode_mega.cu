@@ -312,99 +312,126 @@ __device__ __forceinline__ void stamp(const MegaArgs& a, Smem<D>& sm, int idx) {
 // the static user rows [u0, min(u1, ulen)) (written by earlier steps).
 __device__ __forceinline__ int user_static_end(const Piece& pc, int ulen) { return min(pc.u1, ulen); }
 
+// The producer's stage sequence as a generator (the consumers walk the same
+// sequence implicitly).  A stage is up to 4 contiguous global ranges copied
+// back to back into one ring slot.
+struct StageDesc {
+    int n = 0;
+    const void* src[4];
+    uint32_t bytes[4];
+    uint32_t total = 0;
+    __device__ void add(const void* p, uint32_t b) {
+        src[n] = p;
+        bytes[n++] = b;
+        total += b;
+    }
+};
+
+template <int D>
+struct StageGen {
+    const MegaArgs* a;
+    Split q, o;
+    AttnPlan pl;
+    int h, ulen, rows_per_w, ucap;
+    // cursor: layer, section (0 qkv, 1 attention, 2 out), piece, part (0 ctx, 1 user), row
+    int l = 0, sec = 0, piece = 0, part = 0, r = -1;
+
+    __device__ StageGen(const MegaArgs& args, int c, int G, int ul)
+        : a(&args), q(rows_of(c, G, 3 * args.H * D)), o(rows_of(c, G, args.H * D)),
+          pl(plan_attention(c, G, args.H, args.S, ul + 1)), h(args.H * D), ulen(ul),
+          rows_per_w(STAGE / (args.H * D * 2)), ucap(att_stage_rows(D * 2, 0)) {}
+
+    __device__ bool next(StageDesc& d) {
+        d = StageDesc{};
+        while (l < a->L) {
+            const MegaLayer& ly = a->layer[l];
+            if (sec == 0 || sec == 2) {
+                const Split sp = sec == 0 ? q : o;
+                if (r < 0) r = sp.r0;
+                if (r < sp.r1) {
+                    const int n = min(rows_per_w, sp.r1 - r);
+                    d.add((sec == 0 ? ly.wqkv : ly.wo) + (size_t)r * h, (uint32_t)n * h * 2);
+                    r += n;
+                    return true;
+                }
+                r = -1;
+                if (sec == 0) {
+                    sec = 1;
+                    piece = 0;
+                    part = 0;
+                } else {
+                    sec = 0;
+                    ++l;
+                }
+                continue;
+            }
+            // attention section
+            if (piece >= pl.n) {
+                sec = 2;
+                r = -1;
+                continue;
+            }
+            const Piece& pc = pl.p[piece];
+            if (part == 0) {
+                const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
+                const int ng = ly.fmt == 16 ? 0 : D / ly.group;
+                const int cap = att_stage_rows(row_b, ng);
+                if (r < 0) r = pc.c0;
+                if (r < pc.c1) {
+                    const int n = min(cap, pc.c1 - r);
+                    const size_t base = (size_t)pc.head * a->S + r;
+                    const uint32_t kb = n * row_b, sb = n * ng * 4;
+                    d.add(ly.ck + base * row_b, kb);
+                    d.add(ly.cv + base * row_b, kb);
+                    if (ng) {
+                        d.add(ly.cks + base * ng, sb);
+                        d.add(ly.cvs + base * ng, sb);
+                    }
+                    r += n;
+                    return true;
+                }
+                part = 1;
+                r = -1;
+                continue;
+            }
+            const int ue = user_static_end(pc, ulen);
+            if (r < 0) r = pc.u0;
+            if (r < ue) {
+                const int n = min(ucap, ue - r);
+                const size_t base = (size_t)pc.head * a->cap + r;
+                d.add(ly.uk + base * D, (uint32_t)n * D * 2);
+                d.add(ly.uv + base * D, (uint32_t)n * D * 2);
+                r += n;
+                return true;
+            }
+            ++piece;
+            part = 0;
+            r = -1;
+        }
+        return false;
+    }
+};
+
 template <int D>
 __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen) {
     int stage = 0;
     uint32_t phase = 0;
-    const int h = a.H * D;
-    auto next = [&](int bytes_total) {
+    // (an HBM->L2 prefetch cursor running ahead of this one was measured to
+    // slow the step down -- profiles/r01_megakernel_experiments.txt -- so the
+    // ring is fed straight from HBM)
+    StageGen<D> main(a, c, G, ulen);
+    StageDesc d;
+    while (main.next(d)) {
         mbar_wait(&sm.empty[stage], phase ^ 1);
-        mbar_expect(&sm.full[stage], (uint32_t)bytes_total);
-    };
-    auto advance = [&] {
+        mbar_expect(&sm.full[stage], d.total);
+        uint32_t off = 0;
+        for (int i = 0; i < d.n; ++i) {
+            bulk_g2s(sm.ring[stage] + off, d.src[i], d.bytes[i], &sm.full[stage]);
+            off += d.bytes[i];
+        }
         if (++stage == NST) {
             stage = 0;
             phase ^= 1;
-        }
-    };
-    const Split q = rows_of(c, G, 3 * h), o = rows_of(c, G, h);
-    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
-    const int rows_per_w = STAGE / (h * 2);  // weight rows per stage
-    const int ucap = att_stage_rows(D * 2, 0);
-    // HBM -> L2 prefetch of one layer's stream of this CTA.  Issued a layer
-    // ahead, it keeps HBM busy while the consumers sit in grid barriers and the
-    // ring is full; the ring then refills from L2.
-    auto prefetch_layer = [&](int l) {
-        if (l >= a.L) return;
-        const MegaLayer& ly = a.layer[l];
-        prefetch_l2(ly.wqkv + (size_t)q.r0 * h, (uint32_t)(q.r1 - q.r0) * h * 2);
-        const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
-        const int ng = ly.fmt == 16 ? 0 : D / ly.group;
-        for (int i = 0; i < pl.n; ++i) {
-            const Piece& pc = pl.p[i];
-            const size_t base = (size_t)pc.head * a.S + pc.c0;
-            const uint32_t n = pc.c1 - pc.c0;
-            prefetch_l2(ly.ck + base * row_b, n * row_b);
-            prefetch_l2(ly.cv + base * row_b, n * row_b);
-            if (ng) {
-                prefetch_l2(ly.cks + base * ng, n * ng * 4);
-                prefetch_l2(ly.cvs + base * ng, n * ng * 4);
-            }
-            const int ue = user_static_end(pc, ulen);
-            if (ue > pc.u0) {
-                const size_t ub = (size_t)pc.head * a.cap + pc.u0;
-                prefetch_l2(ly.uk + ub * D, (uint32_t)(ue - pc.u0) * D * 2);
-                prefetch_l2(ly.uv + ub * D, (uint32_t)(ue - pc.u0) * D * 2);
-            }
-        }
-        prefetch_l2(ly.wo + (size_t)o.r0 * h, (uint32_t)(o.r1 - o.r0) * h * 2);
-    };
-    prefetch_layer(0);
-    for (int l = 0; l < a.L; ++l) {
-        const MegaLayer& ly = a.layer[l];
-        prefetch_layer(l + 1);
-        for (int r = q.r0; r < q.r1; r += rows_per_w) {
-            const int n = min(rows_per_w, q.r1 - r);
-            next(n * h * 2);
-            bulk_g2s(sm.ring[stage], ly.wqkv + (size_t)r * h, n * h * 2, &sm.full[stage]);
-            advance();
-        }
-        const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
-        const int ng = ly.fmt == 16 ? 0 : D / ly.group;
-        const int cap = att_stage_rows(row_b, ng);
-        for (int i = 0; i < pl.n; ++i) {
-            const Piece& pc = pl.p[i];
-            for (int r = pc.c0; r < pc.c1; r += cap) {
-                const int n = min(cap, pc.c1 - r);
-                const size_t base = (size_t)pc.head * a.S + r;
-                const int kb = n * row_b, sb = n * ng * 4;
-                next(2 * (kb + sb));
-                uint8_t* dst = sm.ring[stage];
-                bulk_g2s(dst, ly.ck + base * row_b, kb, &sm.full[stage]);
-                bulk_g2s(dst + kb, ly.cv + base * row_b, kb, &sm.full[stage]);
-                if (ng) {
-                    bulk_g2s(dst + 2 * kb, ly.cks + base * ng, sb, &sm.full[stage]);
-                    bulk_g2s(dst + 2 * kb + sb, ly.cvs + base * ng, sb, &sm.full[stage]);
-                }
-                advance();
-            }
-            const int ue = user_static_end(pc, ulen);
-            for (int r = pc.u0; r < ue; r += ucap) {
-                const int n = min(ucap, ue - r);
-                const size_t base = (size_t)pc.head * a.cap + r;
-                const int kb = n * D * 2;
-                next(2 * kb);
-                uint8_t* dst = sm.ring[stage];
-                bulk_g2s(dst, ly.uk + base * D, kb, &sm.full[stage]);
-                bulk_g2s(dst + kb, ly.uv + base * D, kb, &sm.full[stage]);
-                advance();
-            }
-        }
-        for (int r = o.r0; r < o.r1; r += rows_per_w) {
-            const int n = min(rows_per_w, o.r1 - r);
-            next(n * h * 2);
-            bulk_g2s(sm.ring[stage], ly.wo + (size_t)r * h, n * h * 2, &sm.full[stage]);
-            advance();
         }
     }
 }
