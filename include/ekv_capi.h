@@ -265,9 +265,14 @@ int ekv_session_decode(ekv_session_t s, int steps, float* out_dev);
  * active (optional) receives the path that will actually run. */
 int ekv_session_set_decode_path(ekv_session_t s, int path, int* active);
 /* Diagnostics of the persistent path: one real decode step with %globaltimer
- * stamps (ns) of every grid barrier: out[(3l+k)*2G + g] = arrival of CTA g at
- * barrier k of layer l, out[(3l+k)*2G + G + g] = its release; out[6L*G + g] =
- * CTA start.  Needs capacity >= (6L+1)*G. */
+ * stamps (ns) of its phases: out[(l*G + g)*16 + k] = CTA g in layer l at k =
+ * 0 layer start, 1 input ready, 2 QKV rows done, 3 q/k/v of its heads ready,
+ * 4 attention partials published, 5 head merge done, 6 output-projection
+ * partials published, 7 layer output reduced; k = 8..10: ring-wait cycles of
+ * the consumer warps in the QKV, attention and output-projection phases.
+ * out[(L*G + g)*16 + k]: 0 CTA start, 1/2 producer start/end (ns), 3 stages
+ * issued, 4 producer cycles waiting for free ring slots, 5 producer cycles.
+ * Needs capacity >= 16*(L+1)*G. */
 int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_out);
 /* One decode step launched kernel by kernel with CUDA events between the
  * launches (diagnostics / roofline attribution; the step is real and advances

@@ -112,8 +112,8 @@ struct ekv_session_s {
     // persistent decode-step kernel (k_decode_mega.cu)
     int path = 0;                  // 0 = megakernel when supported, 1 = per-layer graph
     bool mega_ok = false;
-    float* mega_ws = nullptr;
-    unsigned* mega_sync = nullptr;  // [H] head counters + 2 barrier words
+    uint64_t* mega_ll = nullptr;     // tagged words of the dataflow (MegaArgs::ll_*)
+    unsigned* mega_sync = nullptr;   // [0] launch epoch
     MegaArgs mega{};
     size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
 };
@@ -246,12 +246,19 @@ void session_alloc(ekv_session_s* s) {
         const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = m->cfg.head_dim;
         const char* env = getenv("EKV_DECODE_PATH");
         if (env && std::string(env) == "graph") s->path = 1;
-        s->mega_ok = mega_supported(L, H, D, s->kv->S, m->h);
+        {
+            const int G = m->ctx->num_sms;
+            s->mega_ok = mega_supported(L, H, D, s->kv->S, m->h) && m->h >= G &&
+                         H * ((m->h + G - 1) / G) <= 1024;
+        }
         if (s->mega_ok) {
             const int G = m->ctx->num_sms;
-            s->mega_ws = dalloc<float>((size_t)G * 2 * (D + 2));
-            s->mega_sync = dalloc<unsigned>((size_t)H + 8);
-            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * (H + 8)));
+            const int h = m->h;
+            const size_t words = (size_t)h + (size_t)H * h + 3 * (size_t)h + (size_t)G * 2 * (D + 2);
+            s->mega_ll = dalloc<uint64_t>(words);
+            EKV_CUDA(cudaMemset(s->mega_ll, 0, sizeof(uint64_t) * words));
+            s->mega_sync = dalloc<unsigned>(8);
+            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * 8));
             MegaArgs& a = s->mega;
             a.L = L;
             a.H = H;
@@ -263,17 +270,25 @@ void session_alloc(ekv_session_s* s) {
             a.pos = m->pos;
             a.state = s->state;
             a.x = s->xa;
-            a.q = s->q;
-            a.concat = s->xb;
             a.hist = s->hist;
-            a.ws = s->mega_ws;
-            a.head_ctr = s->mega_sync;
-            a.sync = (unsigned long long*)(s->mega_sync + ((H + 1) & ~1));
+            a.ll_x = s->mega_ll;
+            a.ll_xpart = a.ll_x + h;
+            a.ll_qkv = a.ll_xpart + (size_t)H * h;
+            a.ll_part = a.ll_qkv + 3 * (size_t)h;
+            a.sync = s->mega_sync;
+            a.trace = nullptr;
+            // W_o of layer l = rows [l*4h + 3h, l*4h + 4h) of the weight buffer
+            a.wo_map = make_map_2d_bf16(m->weights, (uint64_t)h, (uint64_t)L * 4 * h, (uint32_t)D,
+                                        (uint32_t)mega_wo_box_rows(D));
+            a.wo_row0 = 3 * h;
+            a.wo_layer_rows = 4 * h;
+            a.prefetch_stages = 0;
+            if (const char* e = getenv("EKV_MEGA_PREFETCH")) a.prefetch_stages = atoi(e);
+            if (a.prefetch_stages > 0 && a.prefetch_stages < 4) a.prefetch_stages = 4;
             for (int l = 0; l < L; ++l) {
                 const ekv_segment& sg = s->kv->seg[l];
                 MegaLayer& ly = a.layer[l];
                 ly.wqkv = m->wqkvT(l);
-                ly.wo = m->woT(l);
                 ly.fmt = sg.S > 0 ? sg.format : EKV_KV_BF16;
                 ly.group = sg.group > 0 ? sg.group : D;
                 ly.ck = (const uint8_t*)sg.k;
@@ -1113,7 +1128,7 @@ int ekv_session_destroy(ekv_session_t s) {
         if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
         for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                         (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
-                        (void*)s->ws, (void*)s->counters, (void*)s->mega_ws, (void*)s->mega_sync})
+                        (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync})
             cudaFree(p);
         delete s;
     });
@@ -1124,7 +1139,7 @@ int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_
         require(s && out && n_out, "null argument");
         require(use_mega(s), "trace: the persistent decode kernel is not active");
         const int G = s->model->ctx->num_sms, L = s->model->cfg.num_layers;
-        const int n = (6 * L + 1) * G + 32 * G;
+        const int n = 16 * (L + 1) * G;
         require(capacity >= n, "trace: need " + std::to_string(n) + " entries");
         check_overflow(s, 1);
         set_dev(s->model->ctx);

@@ -328,6 +328,24 @@ static CUtensorMap make_map_3d(const void* base, uint64_t inner, uint64_t rows, 
     return m;
 }
 
+// 2-D bf16 map without swizzle (row-major [rows][inner]); used by the decode
+// kernel to gather head column blocks of the output projection.
+CUtensorMap make_map_2d_bf16(const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                             uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {inner * 2};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (2-D) failed (" + std::to_string((int)r) + ")",
+            EKV_ECUDA);
+    return m;
+}
+
 void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
                                 int n_cols, double* colsq, int num_sms, cudaStream_t st) {
     using namespace k1;

@@ -1,32 +1,39 @@
 // The decode step as ONE persistent kernel (batch-1 collaborative decode).
 //
-// merged_forward (cache_merge.cpp:156-226) for one new row, all layers:
-//   P1  QKV projection of the layer input (input transform fused at layer 0),
-//       K/V appended to the session's user cache
-//   P2  segment attention over the reused context + causal user segment,
-//       merged by the Eq. 5 normaliser rule (cache_merge.cpp:12-80)
-//   P3  output projection -> next layer's input (history row at the last layer)
-// separated by grid-wide barriers (one CTA per SM, cooperative launch).
+// merged_forward (cache_merge.cpp:156-226) for one new row, all layers, as a
+// dataflow over four phases per layer, with no grid-wide barrier:
+//   A  QKV projection of the layer input (input transform fused at layer 0);
+//      K/V appended to the session's user cache
+//   B  segment attention of each head over the reused context + causal user
+//      segment, split over CTAs; per-CTA partials (m, l, o)
+//   C  per head: merge of the partials by the Eq. 5 normaliser rule
+//      (cache_merge.cpp:12-80), then that head's column block of the output
+//      projection (split-K over heads): W_o[:, head] . o_head
+//   R  per output element: sum of the per-head partials in head order
+//      (deterministic) -> next layer's input
+// Dependencies are carried by tagged 64-bit words (value | tag, one 8-byte
+// store, polled by the reader), so a phase waits only for the few CTAs that
+// produce its inputs: B(h) for the A rows of head h, C(h) for the B pieces of
+// head h, R for every head's C rows of its elements, A for every element of R.
+// One of those waits (A on R) is the per-layer all-to-all of the
+// computation itself; nothing else is global.
 //
 // Why one kernel: at batch 1 every phase is a few microseconds of HBM traffic
 // (25 MB QKV, 8 MB out-proj, 9-17 MB of context per layer), so separate
-// kernels spend most of their time ramping up and draining.  Here every byte
-// that does not depend on the running activations -- all weights and all
-// context K/V -- is streamed by a dedicated producer warp with bulk-async
-// copies (TMA 1-D, mbarrier completion) into a 3-stage shared-memory ring, in
-// exactly the order the consumer warps will use it, across phase and layer
-// boundaries.  The producer never waits on the grid barriers, so HBM keeps
-// streaming while the consumers synchronise.  Only the small dynamic data
-// (x, q, the user rows, partials) moves through L2 with ld.global.cg.
+// kernels spend most of their time ramping up and draining.  Every byte that
+// does not depend on the running activations -- all weights and all context
+// K/V -- is streamed by a dedicated producer warp (TMA: 1-D bulk copies for
+// rows, a 2-D tensor map for the W_o head column blocks) into a 16-stage
+// shared-memory ring, in exactly the order the consumer warps use it, across
+// phase and layer boundaries.  The producer never waits on the dataflow, so
+// HBM keeps streaming while the consumers wait for their inputs.
 //
-// Work split (static, identical on every CTA): P1 rows [c*3h/G, (c+1)*3h/G),
-// P3 rows [c*h/G, ...); P2 splits the flattened (head, 16-row unit) space of
-// context ++ user rows evenly, so a CTA touches at most two heads; each head's
-// partials (m, l, o) are merged by the last CTA to finish it (atomic counter).
-// User rows written by earlier steps are static during a step, so they are
-// streamed through the ring like the context; only this step's row is read
-// directly.  The activations a phase consumes (x, the attention output, q)
-// are staged once per phase into shared memory with 16-byte loads.
+// Work split (static, proportional, identical on every CTA): A covers virtual
+// rows [c*3h/G, (c+1)*3h/G) of the head-major (head, q|k|v, d) order; B splits
+// the flattened (head, 16-row unit) space of context ++ user rows; C splits
+// the (head, output row) space; R splits the h output elements.  The three
+// head-ordered splits line up, so the CTAs producing and consuming one head's
+// data are neighbours, and each CTA touches at most two heads per phase.
 #include <math_constants.h>
 
 #include "ekv_common.cuh"
@@ -38,7 +45,8 @@ namespace ekv {
 namespace mk {
 
 constexpr int NCW = 8;                  // consumer warps
-constexpr int THREADS = (NCW + 1) * 32; // + 1 producer warp
+constexpr int NPW = 2;                  // producer warps (one issuing thread each)
+constexpr int THREADS = (NCW + NPW + 1) * 32;  // + 1 L2-prefetch warp
 constexpr int NST = 16;                 // ring stages (a multiple of NCW: see the ring protocol)
 constexpr int STAGE = 12 * 1024;        // bytes per stage
 constexpr int UNIT = 16;                // attention rows per partition unit
@@ -55,8 +63,13 @@ __device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes)
                  : "memory");
 }
+// Slot release.  Relaxed, not release: a consumer has used every value it
+// loaded from the slot before it arrives (the loads feed its arithmetic), and a
+// release would also wait for the consumer's outstanding global stores (the
+// tagged words written from the slot's results) to reach L2 -- a round trip
+// per stage on the critical path.
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     uint32_t done = 0;
@@ -80,8 +93,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(saddr(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(saddr(dst)),
+        "l"(map), "r"(saddr(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(saddr(p)));
+    return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void prefetch_tile_l2(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0),
+                 "r"(c1)
+                 : "memory");
 }
 __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
@@ -93,28 +125,31 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// Grid barrier over the consumer warps of every CTA: one 64-bit counter that
-// only grows; barrier k of a launch completes when it reaches base + (k+1)*G,
-// where base (= the counter value when the launch started) is published by
-// CTA 0 at the end of the previous launch.  One red.release + acquire polling,
-// no reset on the critical path.
-// trace (optional): [2][G] arrival / release timestamps of this barrier.
-__device__ __forceinline__ void grid_sync(unsigned long long* count, unsigned long long target,
-                                          unsigned long long* trace = nullptr) {
-    consumers_sync();
-    if (threadIdx.x == 0) {
-        if (trace) trace[blockIdx.x] = gtimer();
-        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(count) : "memory");
+// ---------------------------------------------------------------------------
+// Tagged words.  A word is {float bits (low 32), tag (high 32)}; writers use
+// one 8-byte relaxed store, readers one 8-byte relaxed load (single-copy
+// atomic), so a matching tag implies the value.  Tags are unique per (launch,
+// layer) and never 0, so zero-initialised buffers read as "not ready".
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ll_st(uint64_t* p, float v, uint32_t tag) {
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ll_ld(const uint64_t* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+// finish a word whose first load is w: spin until its tag matches
+__device__ __forceinline__ float ll_spin(const uint64_t* p, unsigned long long w, uint32_t tag) {
+    if ((uint32_t)(w >> 32) != tag) {
         const long long t0 = clock64();
-        unsigned long long v;
-        while (true) {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(count) : "memory");
-            if (v >= target) break;
+        do {
+            w = ll_ld(p);
             if (clock64() - t0 > 4000000000ll) __trap();
-        }
-        if (trace) trace[gridDim.x + blockIdx.x] = gtimer();
+        } while ((uint32_t)(w >> 32) != tag);
     }
-    consumers_sync();
+    return __uint_as_float((uint32_t)w);
 }
 
 // ---------------------------------------------------------------------------
@@ -127,8 +162,8 @@ __device__ __forceinline__ Split rows_of(int c, int G, int N) {
     return Split{(int)((long long)c * N / G), (int)((long long)(c + 1) * N / G)};
 }
 
-// One CTA's attention work for one head: context rows [c0, c1) (through the
-// ring) and user rows [u0, u1) (direct loads).
+// One CTA's attention work for one head: context rows [c0, c1) and user rows
+// [u0, u1); slot = its index in the CTA's plan (0 or 1).
 struct Piece {
     int head, c0, c1, u0, u1, slot;
 };
@@ -164,24 +199,40 @@ __device__ __forceinline__ AttnPlan plan_attention(int c, int G, int H, int S, i
     return pl;
 }
 
+// One CTA's output-projection work for one head: rows [n0, n1) of W_o[:, head].
+struct OPiece {
+    int head, n0, n1;
+};
+struct OPlan {
+    int n;
+    OPiece p[2];
+};
+__device__ __forceinline__ OPlan plan_outproj(int c, int G, int H, int h) {
+    const long long TW = (long long)H * h;
+    const long long a = (long long)c * TW / G, b = (long long)(c + 1) * TW / G;
+    OPlan pl;
+    pl.n = 0;
+    for (long long w = a; w < b;) {
+        const int hd = (int)(w / h);
+        const long long e = b < (long long)(hd + 1) * h ? b : (long long)(hd + 1) * h;
+        pl.p[pl.n++] = OPiece{hd, (int)(w - (long long)hd * h), (int)(e - (long long)hd * h)};
+        w = e;
+    }
+    return pl;
+}
+
+// virtual (head, part, d) QKV row -> physical row of W_qkv ([q | k | v] x h)
+__device__ __forceinline__ int qkv_phys(int v, int D, int h) {
+    const int head = v / (3 * D), rem = v - head * 3 * D, part = rem / D;
+    return part * h + head * D + (rem - part * D);
+}
+
 // largest c with floor(c*TU/G) <= unit (32-bit: TU * G < 2^31)
 __device__ __forceinline__ int owner32(int unit, int G, int TU) {
     int lo = 0, hi = G - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (mid * TU / G <= unit) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
-}
-
-// number of CTAs whose unit range intersects head h (the merge fan-in)
-__device__ __forceinline__ int owner(long long unit, int G, long long TU) {
-    // largest c with floor(c*TU/G) <= unit
-    int lo = 0, hi = G - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((long long)mid * TU / G <= unit) lo = mid;
         else hi = mid - 1;
     }
     return lo;
@@ -253,19 +304,6 @@ __device__ __forceinline__ void ostate_init(OState<EPL>& s) {
     for (int e = 0; e < EPL; ++e) s.o[e] = 0.0f;
 }
 
-// absorb one row: logit x, value row f (already scaled by its dequant scale)
-template <int EPL>
-__device__ __forceinline__ void ostate_add(OState<EPL>& s, float x, const float* f, float vscale) {
-    const float mn = fmaxf(s.m, x);
-    const float corr = exp2f((s.m - mn) * kLog2e);  // exp(-inf) = 0 on the first row
-    const float p = exp2f((x - mn) * kLog2e);
-    s.l = s.l * corr + p;
-    const float pv = p * vscale;
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) s.o[e] = fmaf(pv, f[e], s.o[e] * corr);
-    s.m = mn;
-}
-
 template <int EPL>
 __device__ __forceinline__ void ostate_merge_from(OState<EPL>& s, float m2, float l2, const float* o2) {
     const float mn = fmaxf(s.m, m2);
@@ -278,161 +316,190 @@ __device__ __forceinline__ void ostate_merge_from(OState<EPL>& s, float m2, floa
 }
 
 // ---------------------------------------------------------------------------
-// The kernel
+// Shared memory and diagnostics
 // ---------------------------------------------------------------------------
 template <int D>
 struct Smem {
     uint8_t ring[NST][STAGE];
     uint64_t full[NST];
     uint64_t empty[NST];
-    float xs[2048];            // phase input (x or the attention output)
-    float qs[2][D];            // q of the (<= 2) heads of this CTA's attention pieces
+    float xs[2048];               // phase input x (A) / per-head partial sums (R)
+    float qs[2][D];               // q of the (<= 2) heads of this CTA's attention pieces
     uint16_t nk[2][D], nv[2][D];  // this step's user K/V row of those heads (bf16)
-    float ws_o[2][2][NCW][D];  // per (piece, context/user, warp) partial output
+    float os[2][D];               // merged attention output of this CTA's W_o heads
+    float ws_o[2][2][NCW][D];     // per (piece, context/user, warp) partial output
     float ws_m[2][2][NCW], ws_l[2][2][NCW];
-    int merge_heads_n;         // heads this CTA must merge (last to finish them)
-    int merge_head[2];
-    int hfirst[160], hlast[160];   // head merge: contributing CTA range per head
-    int hcount[160];               // head merge: number of contributing (non-idle) CTAs
-    int ch0[160];                  // head merge: first head of each CTA (-1: idle CTA)
-    int trace_on;
-    int phase_id;
-    unsigned long long wait_cycles[4];
+    int hfirst[160], hlast[160];  // contributing CTA range of each head's attention
+    int ch0[160];                 // first attention head of each CTA (-1: idle CTA)
+    volatile long long prod_k[2]; // stages issued so far by each producer (for the prefetcher)
+    int tphase;                   // diagnostics: phase of the ring waits being counted
+    unsigned long long twait[3];  // diagnostics: ring-wait cycles of A, B, C (sum over warps)
 };
 
-// Diagnostics: %globaltimer stamps of sub-phases of the last layer
-// (trace region [(6L+1)G + 32c + idx]).
-template <int D>
-__device__ __forceinline__ void stamp(const MegaArgs& a, Smem<D>& sm, int idx) {
-    if (a.trace && sm.trace_on && threadIdx.x == 0)
-        a.trace[(size_t)(6 * a.L + 1) * gridDim.x + (size_t)blockIdx.x * 32 + idx] = gtimer();
+// Diagnostics (a.trace != nullptr): trace[(l*G + c)*16 + k], k = 0 layer start,
+// 1 x ready, 2 A done, 3 q/k/v ready, 4 B done, 5 partials merged, 6 C done,
+// 7 R done (%globaltimer ns); 8..10 = consumer ring-wait cycles in A, B, C.
+// trace[(L*G + c)*16 + k]: 0 CTA start, 1/2 producer start/end (ns), 3 stages
+// issued, 4 producer cycles waiting for free slots, 5 producer cycles total.
+__device__ __forceinline__ void stamp(const MegaArgs& a, int l, int k) {
+    if (a.trace && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + k] = gtimer();
+}
+template <class SM>
+__device__ __forceinline__ void set_tphase(const MegaArgs& a, SM& sm, int ph) {
+    if (a.trace && threadIdx.x == 0) sm.tphase = ph;
 }
 
 // Per-piece schedule pieces that go through the ring: context rows [c0, c1) and
 // the static user rows [u0, min(u1, ulen)) (written by earlier steps).
 __device__ __forceinline__ int user_static_end(const Piece& pc, int ulen) { return min(pc.u1, ulen); }
 
-// The producer's stage sequence as a generator (the consumers walk the same
-// sequence implicitly).  A stage is up to 4 contiguous global ranges copied
-// back to back into one ring slot.
-struct StageDesc {
-    int n = 0;
-    const void* src[4];
-    uint32_t bytes[4];
-    uint32_t total = 0;
-    __device__ void add(const void* p, uint32_t b) {
-        src[n] = p;
-        bytes[n++] = b;
-        total += b;
+// The producer: one thread walks the stage sequence the consumers use, as
+// plain nested loops (layer -> QKV rows, attention pieces, W_o pieces), with
+// every index in registers: per stage one wait for the slot, one expect_tx and
+// 1-4 bulk copies (or one 2-D tensor box).
+template <bool PF>
+struct Prod {
+    uint64_t* full;
+    uint64_t* empty;
+    uint8_t* ring;
+    volatile long long* prod_k;
+    const CUtensorMap* map;
+    int sel = 0;          // producer: issues the stages with k % NPW == sel
+    int dist = 0;         // prefetcher: stays at most `dist` stages ahead of the producers
+    long long k = 0;      // global stage index
+    long long waited = 0, count = 0;
+    bool trace = false;
+
+    __device__ __forceinline__ bool mine() const { return PF || (int)(k % NPW) == sel; }
+    __device__ __forceinline__ uint8_t* acquire(uint32_t bytes) {
+        if constexpr (PF) {
+            const long long t0 = clock64();
+            while (min(prod_k[0], prod_k[1]) + dist < k) {
+                __nanosleep(64);
+                if (clock64() - t0 > 4000000000ll) __trap();
+            }
+            return nullptr;
+        } else {
+            const int slot = (int)(k % NST);
+            const uint32_t par = (uint32_t)((k / NST) & 1) ^ 1u;
+            if (trace) {
+                const long long w0 = clock64();
+                mbar_wait(&empty[slot], par);
+                waited += clock64() - w0;
+                ++count;
+            } else {
+                mbar_wait(&empty[slot], par);
+            }
+            mbar_expect(&full[slot], bytes);
+            return ring + (size_t)slot * STAGE;
+        }
+    }
+    __device__ __forceinline__ void copy(uint8_t* dst, const void* src, uint32_t bytes) {
+        if constexpr (PF) prefetch_l2(src, bytes);
+        else bulk_g2s(dst, src, bytes, &full[k % NST]);
+    }
+    __device__ __forceinline__ void tile(uint8_t* dst, int x, int y) {
+        if constexpr (PF) prefetch_tile_l2(map, x, y);
+        else tma_2d(dst, map, x, y, &full[k % NST]);
+    }
+    __device__ __forceinline__ void advance() {
+        if constexpr (!PF) {
+            if ((int)(k % NPW) == sel) prod_k[sel] = k + 1;
+        }
+        ++k;
     }
 };
 
-template <int D>
-struct StageGen {
-    const MegaArgs* a;
-    Split q, o;
-    AttnPlan pl;
-    int h, ulen, rows_per_w, ucap;
-    // cursor: layer, section (0 qkv, 1 attention, 2 out), piece, part (0 ctx, 1 user), row
-    int l = 0, sec = 0, piece = 0, part = 0, r = -1;
-
-    __device__ StageGen(const MegaArgs& args, int c, int G, int ul)
-        : a(&args), q(rows_of(c, G, 3 * args.H * D)), o(rows_of(c, G, args.H * D)),
-          pl(plan_attention(c, G, args.H, args.S, ul + 1)), h(args.H * D), ulen(ul),
-          rows_per_w(STAGE / (args.H * D * 2)), ucap(att_stage_rows(D * 2, 0)) {}
-
-    __device__ bool next(StageDesc& d) {
-        d = StageDesc{};
-        while (l < a->L) {
-            const MegaLayer& ly = a->layer[l];
-            if (sec == 0 || sec == 2) {
-                const Split sp = sec == 0 ? q : o;
-                if (r < 0) r = sp.r0;
-                if (r < sp.r1) {
-                    const int n = min(rows_per_w, sp.r1 - r);
-                    d.add((sec == 0 ? ly.wqkv : ly.wo) + (size_t)r * h, (uint32_t)n * h * 2);
-                    r += n;
-                    return true;
-                }
-                r = -1;
-                if (sec == 0) {
-                    sec = 1;
-                    piece = 0;
-                    part = 0;
-                } else {
-                    sec = 0;
-                    ++l;
-                }
-                continue;
+template <int D, bool PF>
+__device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, int sel) {
+    const long long p0 = clock64();
+    const unsigned long long g0 = gtimer();
+    Prod<PF> pr;
+    pr.prod_k = sm.prod_k;
+    pr.map = &a.wo_map;
+    pr.dist = a.prefetch_stages;
+    pr.full = sm.full;
+    pr.empty = sm.empty;
+    pr.ring = &sm.ring[0][0];
+    pr.trace = a.trace != nullptr;
+    pr.sel = sel;
+    const int h = a.H * D;
+    const Split q = rows_of(c, G, 3 * h);
+    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
+    const OPlan op = plan_outproj(c, G, a.H, h);
+    const int rpw = STAGE / (h * 2);
+    const int ucap = att_stage_rows(D * 2, 0);
+    constexpr int RPS = STAGE / (2 * D);
+    for (int l = 0; l < a.L; ++l) {
+        const MegaLayer& ly = a.layer[l];
+        // A: QKV rows in virtual head-major order; a stage never crosses more
+        // than one (head, q|k|v) block boundary (rpw <= D for every supported shape)
+        for (int r = q.r0; r < q.r1; r += rpw) {
+            if (pr.mine()) {
+                const int n = min(rpw, q.r1 - r);
+                uint8_t* dst = pr.acquire((uint32_t)n * h * 2);
+                const int m = min(n, D - r % D);
+                pr.copy(dst, ly.wqkv + (size_t)qkv_phys(r, D, h) * h, (uint32_t)m * h * 2);
+                if (m < n)
+                    pr.copy(dst + (size_t)m * h * 2, ly.wqkv + (size_t)qkv_phys(r + m, D, h) * h,
+                            (uint32_t)(n - m) * h * 2);
             }
-            // attention section
-            if (piece >= pl.n) {
-                sec = 2;
-                r = -1;
-                continue;
-            }
-            const Piece& pc = pl.p[piece];
-            if (part == 0) {
-                const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
-                const int ng = ly.fmt == 16 ? 0 : D / ly.group;
-                const int cap = att_stage_rows(row_b, ng);
-                if (r < 0) r = pc.c0;
-                if (r < pc.c1) {
+            pr.advance();
+        }
+        // B: context rows, then the static user rows, of each piece
+        const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
+        const int ng = ly.fmt == 16 ? 0 : D / ly.group;
+        const int cap = att_stage_rows(row_b, ng);
+        for (int i = 0; i < pl.n; ++i) {
+            const Piece& pc = pl.p[i];
+            const uint8_t* ck = ly.ck + (size_t)pc.head * a.S * row_b;
+            const uint8_t* cv = ly.cv + (size_t)pc.head * a.S * row_b;
+            for (int r = pc.c0; r < pc.c1; r += cap) {
+                if (pr.mine()) {
                     const int n = min(cap, pc.c1 - r);
-                    const size_t base = (size_t)pc.head * a->S + r;
                     const uint32_t kb = n * row_b, sb = n * ng * 4;
-                    d.add(ly.ck + base * row_b, kb);
-                    d.add(ly.cv + base * row_b, kb);
+                    uint8_t* dst = pr.acquire(2 * kb + 2 * sb);
+                    pr.copy(dst, ck + (size_t)r * row_b, kb);
+                    pr.copy(dst + kb, cv + (size_t)r * row_b, kb);
                     if (ng) {
-                        d.add(ly.cks + base * ng, sb);
-                        d.add(ly.cvs + base * ng, sb);
+                        const size_t so = ((size_t)pc.head * a.S + r) * ng;
+                        pr.copy(dst + 2 * kb, ly.cks + so, sb);
+                        pr.copy(dst + 2 * kb + sb, ly.cvs + so, sb);
                     }
-                    r += n;
-                    return true;
                 }
-                part = 1;
-                r = -1;
-                continue;
+                pr.advance();
             }
             const int ue = user_static_end(pc, ulen);
-            if (r < 0) r = pc.u0;
-            if (r < ue) {
-                const int n = min(ucap, ue - r);
-                const size_t base = (size_t)pc.head * a->cap + r;
-                d.add(ly.uk + base * D, (uint32_t)n * D * 2);
-                d.add(ly.uv + base * D, (uint32_t)n * D * 2);
-                r += n;
-                return true;
+            for (int r = pc.u0; r < ue; r += ucap) {
+                if (pr.mine()) {
+                    const int n = min(ucap, ue - r);
+                    const size_t base = ((size_t)pc.head * a.cap + r) * D;
+                    uint8_t* dst = pr.acquire((uint32_t)n * D * 4);
+                    pr.copy(dst, ly.uk + base, (uint32_t)n * D * 2);
+                    pr.copy(dst + (size_t)n * D * 2, ly.uv + base, (uint32_t)n * D * 2);
+                }
+                pr.advance();
             }
-            ++piece;
-            part = 0;
-            r = -1;
         }
-        return false;
+        // C: W_o head column blocks, one 2-D box of RPS rows x D columns per stage
+        const int row0 = a.wo_row0 + l * a.wo_layer_rows;
+        for (int i = 0; i < op.n; ++i) {
+            for (int r = op.p[i].n0; r < op.p[i].n1; r += RPS) {
+                if (pr.mine()) {
+                    uint8_t* dst = pr.acquire(STAGE);
+                    pr.tile(dst, op.p[i].head * D, row0 + r);
+                }
+                pr.advance();
+            }
+        }
     }
-};
-
-template <int D>
-__device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen) {
-    int stage = 0;
-    uint32_t phase = 0;
-    // (an HBM->L2 prefetch cursor running ahead of this one was measured to
-    // slow the step down -- profiles/r01_megakernel_experiments.txt -- so the
-    // ring is fed straight from HBM)
-    StageGen<D> main(a, c, G, ulen);
-    StageDesc d;
-    while (main.next(d)) {
-        mbar_wait(&sm.empty[stage], phase ^ 1);
-        mbar_expect(&sm.full[stage], d.total);
-        uint32_t off = 0;
-        for (int i = 0; i < d.n; ++i) {
-            bulk_g2s(sm.ring[stage] + off, d.src[i], d.bytes[i], &sm.full[stage]);
-            off += d.bytes[i];
-        }
-        if (++stage == NST) {
-            stage = 0;
-            phase ^= 1;
-        }
+    if (a.trace && sel == 0 && !PF) {
+        unsigned long long* t = a.trace + ((size_t)a.L * G + c) * 16;
+        t[1] = g0;
+        t[2] = gtimer();
+        t[3] = pr.count;
+        t[4] = pr.waited;
+        t[5] = clock64() - p0;
     }
 }
 
@@ -448,10 +515,14 @@ struct Cursor {
 };
 
 template <int D>
-__device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, long long k) {
-    const long long t0 = clock64();
-    mbar_wait(&sm.full[k % NST], (uint32_t)((k / NST) & 1));
-    if (sm.trace_on && (threadIdx.x & 31) == 0) atomicAdd(&sm.wait_cycles[sm.phase_id], (unsigned long long)(clock64() - t0));
+__device__ __forceinline__ const uint8_t* ring_acquire(Smem<D>& sm, long long k, bool tr = false) {
+    if (tr) {
+        const long long t0 = clock64();
+        mbar_wait(&sm.full[k % NST], (uint32_t)((k / NST) & 1));
+        if ((threadIdx.x & 31) == 0) atomicAdd(&sm.twait[sm.tphase], (unsigned long long)(clock64() - t0));
+    } else {
+        mbar_wait(&sm.full[k % NST], (uint32_t)((k / NST) & 1));
+    }
     return sm.ring[k % NST];
 }
 template <int D>
@@ -459,34 +530,54 @@ __device__ __forceinline__ void ring_release(Smem<D>& sm, long long k) {
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&sm.empty[k % NST]);
 }
+__device__ __forceinline__ int first_owned(const Cursor& cu) {
+    return (int)(((threadIdx.x >> 5) - cu.k % NCW + NCW) % NCW);
+}
 
-// Stage a phase input vector (h floats, in global, written by other CTAs) into
-// shared memory with 16-byte coherent loads; optional layer-0 input transform.
+// Layer input into shared memory.  Layer 0: the token input with the input
+// transform (plain loads: written before the launch).  Later layers: the
+// tagged words of R of the previous layer, every load in flight at once.
 template <int D>
-__device__ __forceinline__ void stage_vector(Smem<D>& sm, const float* src, int h,
-                                             const float* gamma, const float* bias,
-                                             const uint16_t* pos_row) {
-    for (int i = threadIdx.x; i < h / 4; i += NCW * 32) {
-        float4 v = __ldcg(reinterpret_cast<const float4*>(src) + i);
-        if (pos_row) {
-            const float4 g = reinterpret_cast<const float4*>(gamma)[i];
-            const float4 b = reinterpret_cast<const float4*>(bias)[i];
+__device__ __forceinline__ void stage_x(const MegaArgs& a, Smem<D>& sm, int h, int l, uint32_t prev_tag,
+                                        int ulen) {
+    if (l == 0) {
+        const uint16_t* pos_row = a.pos + (size_t)(a.S + ulen) * h;
+        for (int i = threadIdx.x; i < h / 4; i += NCW * 32) {
+            float4 v = reinterpret_cast<const float4*>(a.x)[i];
+            const float4 g = reinterpret_cast<const float4*>(a.gamma)[i];
+            const float4 b = reinterpret_cast<const float4*>(a.bias)[i];
             const uint2 p = reinterpret_cast<const uint2*>(pos_row)[i];
             v.x = g.x * (v.x + bf16_lo(p.x)) + b.x;
             v.y = g.y * (v.y + bf16_hi(p.x)) + b.y;
             v.z = g.z * (v.z + bf16_lo(p.y)) + b.z;
             v.w = g.w * (v.w + bf16_hi(p.y)) + b.w;
+            reinterpret_cast<float4*>(sm.xs)[i] = v;
         }
-        reinterpret_cast<float4*>(sm.xs)[i] = v;
+    } else {
+        constexpr int W = 2048 / (NCW * 32);  // words per thread at the largest h
+        unsigned long long w[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int i = k * NCW * 32 + threadIdx.x;
+            if (i < h) w[k] = ll_ld(a.ll_x + i);
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int i = k * NCW * 32 + threadIdx.x;
+            if (i < h) sm.xs[i] = ll_spin(a.ll_x + i, w[k], prev_tag);
+        }
     }
     consumers_sync();
 }
 
-// y[n] = sum_k x[k] W[n][k] for the CTA's rows, weights from the ring, x from
-// shared memory into registers once (lane holds x[c*256 + lane*8 + e]).
-template <int D, int KC, class Epi>
-__device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, int h, Epi epi) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// A: y[v] = sum_k x[k] W_qkv[phys(v)][k] for the CTA's virtual rows, weights
+// from the ring, x from shared memory into registers once (lane holds
+// x[c*256 + lane*8 + e]).  q goes out as tagged words; k and v are rounded to
+// bf16, appended to the user cache, and go out as tagged words too.
+template <int D, int KC>
+__device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm, Cursor& cu,
+                                         Split rows, int h, int ulen, uint32_t tag) {
+    const int lane = threadIdx.x & 31;
     float xr[KC * 8];
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
@@ -495,87 +586,123 @@ __device__ __forceinline__ void proj_rows(Smem<D>& sm, Cursor& cu, Split rows, i
         xr[c * 8 + 0] = a0.x; xr[c * 8 + 1] = a0.y; xr[c * 8 + 2] = a0.z; xr[c * 8 + 3] = a0.w;
         xr[c * 8 + 4] = a1.x; xr[c * 8 + 5] = a1.y; xr[c * 8 + 6] = a1.z; xr[c * 8 + 7] = a1.w;
     }
+    constexpr int RG = 3;  // rows in flight per warp (independent FMA and shuffle chains)
     const int rows_per_w = STAGE / (h * 2);
     const int nst = (rows.r1 - rows.r0 + rows_per_w - 1) / rows_per_w;
-    for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
+    for (int j = first_owned(cu); j < nst; j += NCW) {
         const int r = rows.r0 + j * rows_per_w;
         const int n = min(rows_per_w, rows.r1 - r);
-        const uint8_t* st = ring_acquire(sm, cu.k + j);
-        for (int i = 0; i < n; ++i) {
-            const uint16_t* w = (const uint16_t*)(st + (size_t)i * h * 2);
-            float acc[KC];
+        const uint8_t* st = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+        for (int i0 = 0; i0 < n; i0 += RG) {
+            const uint8_t* wr[RG];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) wr[g] = st + (size_t)min(i0 + g, n - 1) * h * 2 + lane * 16;
+            float acc[RG][2];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) acc[g][0] = acc[g][1] = 0.0f;
+            // software pipeline: chunk c+1 of every row is loaded before chunk c
+            // is consumed (volatile loads keep their order)
+            uint4 cur[RG], nxt[RG];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) cur[g] = lds128(wr[g]);
 #pragma unroll
             for (int c = 0; c < KC; ++c) {
-                const uint4 v = *reinterpret_cast<const uint4*>(w + c * 256 + lane * 8);
-                const uint32_t ww[4] = {v.x, v.y, v.z, v.w};
-                float a0 = 0.0f;
+                if (c + 1 < KC) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    a0 = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], a0);
-                    a0 = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], a0);
+                    for (int g = 0; g < RG; ++g) nxt[g] = lds128(wr[g] + (c + 1) * 512);
                 }
-                acc[c] = a0;
-            }
 #pragma unroll
-            for (int c = 1; c < KC; ++c) acc[0] += acc[c];
-            const float v = warp_sum(acc[0]);
-            if (lane == 0) epi(r + i, v);
+                for (int g = 0; g < RG; ++g) {
+                    const uint32_t ww[4] = {cur[g].x, cur[g].y, cur[g].z, cur[g].w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        acc[g][0] = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], acc[g][0]);
+                        acc[g][1] = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], acc[g][1]);
+                    }
+                }
+                if (c + 1 < KC) {
+#pragma unroll
+                    for (int g = 0; g < RG; ++g) cur[g] = nxt[g];
+                }
+            }
+            float y[RG];
+#pragma unroll
+            for (int g = 0; g < RG; ++g) y[g] = acc[g][0] + acc[g][1];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int g = 0; g < RG; ++g) y[g] += __shfl_xor_sync(0xffffffffu, y[g], o);
+            // lanes 0..RG-1 finish one row each
+            const float yv = lane == 0 ? y[0] : (lane == 1 ? y[1] : y[2]);
+            if (lane < RG && i0 + lane < n) {
+                const int v = r + i0 + lane;
+                const int head = v / (3 * D), rem = v - head * 3 * D, part = rem / D;
+                if (part == 0) {
+                    ll_st(a.ll_qkv + v, yv, tag);
+                } else {
+                    const uint16_t b = f32_to_bf16_bits(yv);
+                    uint16_t* dst = part == 1 ? ly.uk : ly.uv;
+                    dst[((size_t)head * a.cap + ulen) * D + (rem - part * D)] = b;
+                    ll_st(a.ll_qkv + v, __uint_as_float((uint32_t)b << 16), tag);
+                }
+            }
         }
         ring_release(sm, cu.k + j);
     }
     cu.k += nst;
 }
 
-// Attention of q over n <= ATT_ROWS rows (a ring stage, or global memory for
-// this step's user row) owned by the calling warp, into this lane's state.
-// Two passes per stage: all logits of the lane-group's rows first (registers),
-// then one rescale of the running state and one exp per row.
+// Attention of q over n <= NPASS*RPP rows of a ring stage (or the shared-memory
+// copy of this step's user row) owned by the calling warp, into this lane's
+// state.  Branch-free: every lane group walks NPASS rows with the row index
+// clamped to n-1 and masks the clamped rows out (probability 0), so the passes
+// are straight-line code with independent load/FMA/shuffle chains.
+// Pass 1 computes all logits, pass 2 does one rescale and one exp per row.
+__host__ __device__ constexpr int att_rows_fit(int bytes_per_row) {
+    return STAGE / bytes_per_row / UNIT * UNIT < ATT_ROWS ? STAGE / bytes_per_row / UNIT * UNIT : ATT_ROWS;
+}
+// passes covering the largest stage of a format (quantised: one scale group per
+// row, the most rows att_stage_rows can give)
 template <int D, int FMT>
+__host__ __device__ constexpr int att_passes() {
+    return (att_rows_fit(FMT == 16 ? 4 * D : 2 * (Fmt<D, FMT>::ROW + 4)) + Fmt<D, FMT>::RPP - 1) /
+           Fmt<D, FMT>::RPP;
+}
+
+template <int D, int FMT, int NPASS>
 __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t* vb, const float* ks,
                                                const float* vs, int ng, int group, int n,
-                                               const float* qreg, OState<Fmt<D, FMT>::EPL>& st,
-                                               bool global_src) {
+                                               const float* qreg, OState<Fmt<D, FMT>::EPL>& st) {
     using F = Fmt<D, FMT>;
-    constexpr int MAXR = (ATT_ROWS + F::RPP - 1) / F::RPP;  // rows per lane group per stage
     const int lane = threadIdx.x & 31;
     const int sub = lane % F::LPR, rsub = lane / F::LPR;
     const int grp = FMT == 16 ? 0 : (sub * F::EPL) / group;
-    // pass 1: lane-partial dots of every row (independent LDS + FMA chains),
-    // then the LPR-lane reductions of all rows together (independent shuffles)
-    float lg[MAXR];
+    float lg[NPASS];
 #pragma unroll
-    for (int p = 0; p < MAXR; ++p) {
-        const int row = p * F::RPP + rsub;
-        lg[p] = 0.0f;
-        if (p * F::RPP < n && row < n) {
-            const uint8_t* kp = kb + (size_t)row * F::ROW + sub * 16;
-            const uint4 kv = global_src ? __ldcg(reinterpret_cast<const uint4*>(kp))
-                                        : *reinterpret_cast<const uint4*>(kp);
-            float f[F::EPL];
-            expand16<FMT>(kv, f);
-            float d0 = 0.0f, d1 = 0.0f;
+    for (int p = 0; p < NPASS; ++p) {
+        const int row = min(p * F::RPP + rsub, n - 1);
+        const uint4 kv = *reinterpret_cast<const uint4*>(kb + row * F::ROW + sub * 16);
+        float f[F::EPL];
+        expand16<FMT>(kv, f);
+        float d0 = 0.0f, d1 = 0.0f;
 #pragma unroll
-            for (int e = 0; e < F::EPL; e += 2) {
-                d0 = fmaf(qreg[e], f[e], d0);
-                d1 = fmaf(qreg[e + 1], f[e + 1], d1);
-            }
-            float dot = d0 + d1;
-            if constexpr (FMT != 16) dot *= ks[(size_t)row * ng + grp];
-            lg[p] = dot;
+        for (int e = 0; e < F::EPL; e += 2) {
+            d0 = fmaf(qreg[e], f[e], d0);
+            d1 = fmaf(qreg[e + 1], f[e + 1], d1);
         }
+        float dot = d0 + d1;
+        if constexpr (FMT != 16) dot *= ks[row * ng + grp];
+        lg[p] = dot;
     }
 #pragma unroll
     for (int o = F::LPR >> 1; o > 0; o >>= 1)
 #pragma unroll
-        for (int p = 0; p < MAXR; ++p)
-            if (p * F::RPP < n) lg[p] += __shfl_xor_sync(0xffffffffu, lg[p], o);
+        for (int p = 0; p < NPASS; ++p) lg[p] += __shfl_xor_sync(0xffffffffu, lg[p], o);
     float mx = -CUDART_INF_F;
 #pragma unroll
-    for (int p = 0; p < MAXR; ++p) {
-        const int row = p * F::RPP + rsub;
-        if (p * F::RPP < n && row < n) mx = fmaxf(mx, lg[p]);
-    }
-    if (mx == -CUDART_INF_F) return;  // no rows for this lane group
+    for (int p = 0; p < NPASS; ++p)
+        if (p * F::RPP + rsub < n) mx = fmaxf(mx, lg[p]);
+    if (mx == -CUDART_INF_F) return;  // no rows for this lane group (n < RPP)
     const float mn = fmaxf(st.m, mx);
     const float corr = exp2f((st.m - mn) * kLog2e);
     st.l *= corr;
@@ -583,22 +710,18 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
     for (int e = 0; e < F::EPL; ++e) st.o[e] *= corr;
     st.m = mn;
 #pragma unroll
-    for (int p = 0; p < MAXR; ++p) {
-        const int row = p * F::RPP + rsub;
-        if (p * F::RPP < n && row < n) {
-            const float pr = exp2f((lg[p] - mn) * kLog2e);
-            const uint8_t* vp = vb + (size_t)row * F::ROW + sub * 16;
-            const uint4 vv = global_src ? __ldcg(reinterpret_cast<const uint4*>(vp))
-                                        : *reinterpret_cast<const uint4*>(vp);
-            float vsc = 1.0f;
-            if constexpr (FMT != 16) vsc = vs[(size_t)row * ng + grp];
-            float f[F::EPL];
-            expand16<FMT>(vv, f);
-            st.l += pr;
-            const float pv = pr * vsc;
+    for (int p = 0; p < NPASS; ++p) {
+        const int row = min(p * F::RPP + rsub, n - 1);
+        const float pr = p * F::RPP + rsub < n ? exp2f((lg[p] - mn) * kLog2e) : 0.0f;
+        const uint4 vv = *reinterpret_cast<const uint4*>(vb + row * F::ROW + sub * 16);
+        float vsc = 1.0f;
+        if constexpr (FMT != 16) vsc = vs[row * ng + grp];
+        float f[F::EPL];
+        expand16<FMT>(vv, f);
+        st.l += pr;
+        const float pv = pr * vsc;
 #pragma unroll
-            for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
-        }
+        for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
     }
 }
 
@@ -610,6 +733,11 @@ __device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>:
     using F = Fmt<D, FMT>;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sub = lane % F::LPR;
+    if (__all_sync(0xffffffffu, st.m == -CUDART_INF_F)) {  // the warp saw no rows
+        if (lane == 0) sm.ws_l[piece][kind][warp] = 0.0f;
+        return;
+    }
+#pragma unroll
     for (int off = F::LPR; off < 32; off <<= 1) {
         float o2[F::EPL];
         const float m2 = __shfl_xor_sync(0xffffffffu, st.m, off);
@@ -628,12 +756,133 @@ __device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>:
     }
 }
 
-// Merge of one head's partials by one warp (Eq. 5 generalised to the CTAs
-// that attended the head): every load issued before any use, shuffle-free
-// per-lane math (each lane owns D/32 output columns), result to a.concat.
+// B: attention of the CTA's pieces.  q and this step's K/V row of each head
+// arrive as tagged words from A; the context and earlier user rows come
+// through the ring.  Ends with one tagged (m, l, o) partial per piece.
+template <int D, int FMT>
+__device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
+                                                Cursor& cu, const AttnPlan& pl, int c, int ulen,
+                                                int l, uint32_t tag) {
+    using F = Fmt<D, FMT>;
+    using FU = Fmt<D, 16>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ng = FMT == 16 ? 0 : D / ly.group;
+    const int cap = att_stage_rows(F::ROW, ng);
+    const int ucap = att_stage_rows(D * 2, 0);
+    {
+        constexpr int W = (2 * 3 * D + NCW * 32 - 1) / (NCW * 32);
+        unsigned long long w[W];
+        const int nw = pl.n * 3 * D;
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int t = k * NCW * 32 + threadIdx.x;
+            if (t < nw) w[k] = ll_ld(a.ll_qkv + (size_t)pl.p[t / (3 * D)].head * 3 * D + t % (3 * D));
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int t = k * NCW * 32 + threadIdx.x;
+            if (t < nw) {
+                const int i = t / (3 * D), j = t % (3 * D);
+                const float v =
+                    ll_spin(a.ll_qkv + (size_t)pl.p[i].head * 3 * D + j, w[k], tag);
+                if (j < D) sm.qs[i][j] = v;
+                else if (j < 2 * D) sm.nk[i][j - D] = (uint16_t)(__float_as_uint(v) >> 16);
+                else sm.nv[i][j - 2 * D] = (uint16_t)(__float_as_uint(v) >> 16);
+            }
+        }
+    }
+    consumers_sync();
+    stamp(a, l, 3);
+    for (int i = 0; i < pl.n; ++i) {
+        const Piece& pc = pl.p[i];
+        {   // context rows (ring)
+            float qreg[F::EPL];
+            const int sub = lane % F::LPR;
+#pragma unroll
+            for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
+            OState<F::EPL> st;
+            ostate_init<F::EPL>(st);
+            const int nst = (pc.c1 - pc.c0 + cap - 1) / cap;
+            for (int j = first_owned(cu); j < nst; j += NCW) {
+                const int r = pc.c0 + j * cap;
+                const int n = min(cap, pc.c1 - r);
+                const uint8_t* s = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+                const int kbytes = n * F::ROW;
+                attend_rows_mk<D, FMT, att_passes<D, FMT>()>(s, s + kbytes, (const float*)(s + 2 * kbytes),
+                                       (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n,
+                                       qreg, st);
+                ring_release(sm, cu.k + j);
+            }
+            cu.k += nst;
+            if constexpr (FMT != 16) park_warp_state<D, FMT>(sm, st, i, 0);
+            // user rows: earlier steps through the ring, this step's row from
+            // shared memory; bf16 context shares the lane layout, so one state
+            OState<FU::EPL> su;
+            if constexpr (FMT == 16) {
+                su = *reinterpret_cast<OState<FU::EPL>*>(&st);
+            } else {
+                ostate_init<FU::EPL>(su);
+            }
+            float qu[FU::EPL];
+            const int subu = lane % FU::LPR;
+#pragma unroll
+            for (int e = 0; e < FU::EPL; ++e) qu[e] = sm.qs[i][subu * FU::EPL + e];
+            const int ue = user_static_end(pc, ulen);
+            const int nsu = ue > pc.u0 ? (ue - pc.u0 + ucap - 1) / ucap : 0;
+            for (int j = first_owned(cu); j < nsu; j += NCW) {
+                const int r = pc.u0 + j * ucap;
+                const int n = min(ucap, ue - r);
+                const uint8_t* s = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+                attend_rows_mk<D, 16, att_passes<D, 16>()>(s, s + n * D * 2, nullptr, nullptr, 0, D, n,
+                                                            qu, su);
+                ring_release(sm, cu.k + j);
+            }
+            cu.k += nsu;
+            if (ulen >= pc.u0 && ulen < pc.u1 && warp == (int)((cu.k + i) % NCW))
+                attend_rows_mk<D, 16, 1>((const uint8_t*)sm.nk[i], (const uint8_t*)sm.nv[i], nullptr,
+                                         nullptr, 0, D, 1, qu, su);
+            park_warp_state<D, 16>(sm, su, i, FMT == 16 ? 0 : 1);
+            if (FMT == 16 && lane == 0) sm.ws_l[i][1][warp] = 0.0f;
+        }
+    }
+    consumers_sync();
+    // one CTA-level fold of every (piece, kind, warp) state -> this CTA's tagged partials
+    for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
+        const int i = t / D, cix = t - i * D;
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int w = 0; w < NCW; ++w)
+                if (sm.ws_l[i][k][w] > 0.0f) M = fmaxf(M, sm.ws_m[i][k][w]);
+        float Ls = 0.0f, O = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+#pragma unroll
+            for (int w = 0; w < NCW; ++w) {
+                const float lw = sm.ws_l[i][k][w];
+                if (lw > 0.0f) {
+                    const float sc = exp2f((sm.ws_m[i][k][w] - M) * kLog2e);
+                    Ls += lw * sc;
+                    O += sm.ws_o[i][k][w][cix] * sc;
+                }
+            }
+        uint64_t* outp = a.ll_part + ((size_t)c * 2 + i) * (D + 2);
+        ll_st(outp + 2 + cix, O, tag);
+        if (cix == 0) {
+            ll_st(outp, M, tag);
+            ll_st(outp + 1, Ls, tag);
+        }
+    }
+    // (the next consumers_sync is in the caller, before shared state is reused)
+}
+
+// C, part 1: merge of head hh's partials (Eq. 5 generalised to the CTAs that
+// attended the head) by one warp: every tagged load in flight before any use,
+// per-lane math (each lane owns D/32 output columns), result to sm.os[slot].
 template <int D>
-__device__ __forceinline__ void merge_one_head(const MegaArgs& a, Smem<D>& sm, int hh) {
-    constexpr int MAXC = 8;
+__device__ __forceinline__ void merge_head(const MegaArgs& a, Smem<D>& sm, int hh, int slot, uint32_t tag) {
+    constexpr int MAXC = 4;
     constexpr int VPL = (D + 31) / 32;
     const int lane = threadIdx.x & 31;
     const int first = sm.hfirst[hh], last = sm.hlast[hh];
@@ -641,19 +890,32 @@ __device__ __forceinline__ void merge_one_head(const MegaArgs& a, Smem<D>& sm, i
 #pragma unroll
     for (int t = 0; t < VPL; ++t) O[t] = 0.0f;
     for (int c0 = first; c0 <= last; c0 += MAXC) {
-        float m[MAXC], l[MAXC], v[MAXC][VPL];
+        unsigned long long wm[MAXC], wl[MAXC], wv[MAXC][VPL];
+        const uint64_t* pp[MAXC];
+        bool ok[MAXC];
 #pragma unroll
         for (int j = 0; j < MAXC; ++j) {
             const int cc = c0 + j;
-            const bool ok = cc <= last && sm.ch0[cc] >= 0;
-            const int sl = ok && sm.ch0[cc] == hh ? 0 : 1;
-            const float* pp = a.ws + ((size_t)(ok ? cc : first) * 2 + sl) * (D + 2);
-            m[j] = ok ? __ldcg(pp) : -CUDART_INF_F;
-            l[j] = ok ? __ldcg(pp + 1) : 0.0f;
+            ok[j] = cc <= last && sm.ch0[cc] >= 0;
+            const int sl = ok[j] && sm.ch0[cc] == hh ? 0 : 1;
+            pp[j] = a.ll_part + ((size_t)(ok[j] ? cc : first) * 2 + sl) * (D + 2);
+            if (ok[j]) {
+                wm[j] = ll_ld(pp[j]);
+                wl[j] = ll_ld(pp[j] + 1);
+#pragma unroll
+                for (int t = 0; t < VPL; ++t)
+                    if (lane + 32 * t < D) wv[j][t] = ll_ld(pp[j] + 2 + lane + 32 * t);
+            }
+        }
+        float m[MAXC], l[MAXC], v[MAXC][VPL];
+#pragma unroll
+        for (int j = 0; j < MAXC; ++j) {
+            m[j] = ok[j] ? ll_spin(pp[j], wm[j], tag) : -CUDART_INF_F;
+            l[j] = ok[j] ? ll_spin(pp[j] + 1, wl[j], tag) : 0.0f;
 #pragma unroll
             for (int t = 0; t < VPL; ++t) {
                 const int cix = lane + 32 * t;
-                v[j][t] = (ok && cix < D) ? __ldcg(pp + 2 + cix) : 0.0f;
+                v[j][t] = (ok[j] && cix < D) ? ll_spin(pp[j] + 2 + cix, wv[j][t], tag) : 0.0f;
             }
         }
         float Mn = M;
@@ -677,137 +939,95 @@ __device__ __forceinline__ void merge_one_head(const MegaArgs& a, Smem<D>& sm, i
 #pragma unroll
     for (int t = 0; t < VPL; ++t) {
         const int cix = lane + 32 * t;
-        if (cix < D) a.concat[hh * D + cix] = O[t] * inv;
+        if (cix < D) sm.os[slot][cix] = O[t] * inv;
     }
 }
 
-template <int D, int FMT>
-__device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
-                                                Cursor& cu, const AttnPlan& pl, int c, int G,
-                                                int ulen) {
-    stamp(a, sm, 10);
-    using F = Fmt<D, FMT>;
-    using FU = Fmt<D, 16>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int ng = FMT == 16 ? 0 : D / ly.group;
-    const int cap = att_stage_rows(F::ROW, ng);
-    const int ucap = att_stage_rows(D * 2, 0);
-    // q and this step's user K/V row of the heads this CTA attends (written by
-    // P1 on other CTAs): one round of coherent loads into shared memory
-    for (int i = 0; i < pl.n; ++i) {
-        for (int t = threadIdx.x; t < D / 4; t += NCW * 32)
-            reinterpret_cast<float4*>(sm.qs[i])[t] =
-                __ldcg(reinterpret_cast<const float4*>(a.q + pl.p[i].head * D) + t);
-        if (ulen >= pl.p[i].u0 && ulen < pl.p[i].u1) {
-            const size_t row = ((size_t)pl.p[i].head * a.cap + ulen) * D;
-            for (int t = threadIdx.x; t < D / 8; t += NCW * 32) {
-                reinterpret_cast<uint4*>(sm.nk[i])[t] = __ldcg(reinterpret_cast<const uint4*>(ly.uk + row) + t);
-                reinterpret_cast<uint4*>(sm.nv[i])[t] = __ldcg(reinterpret_cast<const uint4*>(ly.uv + row) + t);
+// C, part 2: rows [n0, n1) of W_o[:, head] (2-D boxes from the ring, RPS rows of
+// D bf16 each) dotted with the merged head output -> tagged per-head partials.
+template <int D>
+__device__ __forceinline__ void proj_wo(const MegaArgs& a, Smem<D>& sm, Cursor& cu, const OPiece& op,
+                                        int slot, int h, uint32_t tag) {
+    constexpr int LPR = D / 8;  // lanes per row, 8 bf16 each
+    constexpr int RPP = 32 / LPR;
+    constexpr int RPS = STAGE / (2 * D);
+    const int lane = threadIdx.x & 31, sub = lane % LPR, rsub = lane / LPR;
+    float o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = sm.os[slot][sub * 8 + e];
+    uint64_t* out = a.ll_xpart + (size_t)op.head * h;
+    const int nst = (op.n1 - op.n0 + RPS - 1) / RPS;
+    for (int j = first_owned(cu); j < nst; j += NCW) {
+        const int r = op.n0 + j * RPS;
+        const int n = min(RPS, op.n1 - r);
+        const uint8_t* st = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+        constexpr int PB = 4;  // passes in flight
+        static_assert((RPS / RPP) % PB == 0, "pass batching");
+#pragma unroll 1
+        for (int p0 = 0; p0 < RPS / RPP; p0 += PB) {
+            float dot[PB];
+#pragma unroll
+            for (int b = 0; b < PB; ++b) {
+                const int row = (p0 + b) * RPP + rsub;
+                const uint4 w = *reinterpret_cast<const uint4*>(st + row * D * 2 + sub * 16);
+                float d0 = bf16_lo(w.x) * o[0], d1 = bf16_hi(w.x) * o[1];
+                d0 = fmaf(bf16_lo(w.y), o[2], d0);
+                d1 = fmaf(bf16_hi(w.y), o[3], d1);
+                d0 = fmaf(bf16_lo(w.z), o[4], d0);
+                d1 = fmaf(bf16_hi(w.z), o[5], d1);
+                d0 = fmaf(bf16_lo(w.w), o[6], d0);
+                d1 = fmaf(bf16_hi(w.w), o[7], d1);
+                dot[b] = d0 + d1;
             }
-        }
-    }
-    consumers_sync();
-    stamp(a, sm, 11);
-    for (int i = 0; i < pl.n; ++i) {
-        const Piece& pc = pl.p[i];
-        {   // context rows (ring)
-            float qreg[F::EPL];
-            const int sub = lane % F::LPR;
 #pragma unroll
-            for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
-            OState<F::EPL> st;
-            ostate_init<F::EPL>(st);
-            const int nst = (pc.c1 - pc.c0 + cap - 1) / cap;
-            for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
-                const int r = pc.c0 + j * cap;
-                const int n = min(cap, pc.c1 - r);
-                const uint8_t* s = ring_acquire(sm, cu.k + j);
-                const int kbytes = n * F::ROW;
-                attend_rows_mk<D, FMT>(s, s + kbytes, (const float*)(s + 2 * kbytes),
-                                       (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n,
-                                       qreg, st, false);
-                ring_release(sm, cu.k + j);
-            }
-            cu.k += nst;
-            park_warp_state<D, FMT>(sm, st, i, 0);
-        }
-        {   // user rows: earlier steps through the ring, this step's row directly
-            float qreg[FU::EPL];
-            const int sub = lane % FU::LPR;
+            for (int off = LPR >> 1; off > 0; off >>= 1)
 #pragma unroll
-            for (int e = 0; e < FU::EPL; ++e) qreg[e] = sm.qs[i][sub * FU::EPL + e];
-            OState<FU::EPL> su;
-            ostate_init<FU::EPL>(su);
-            const int ue = user_static_end(pc, ulen);
-            const int nst = ue > pc.u0 ? (ue - pc.u0 + ucap - 1) / ucap : 0;
-            for (int j = (int)((warp - cu.k % NCW + NCW) % NCW); j < nst; j += NCW) {
-                const int r = pc.u0 + j * ucap;
-                const int n = min(ucap, ue - r);
-                const uint8_t* s = ring_acquire(sm, cu.k + j);
-                attend_rows_mk<D, 16>(s, s + n * D * 2, nullptr, nullptr, 0, D, n, qreg, su, false);
-                ring_release(sm, cu.k + j);
-            }
-            cu.k += nst;
-            if (ulen >= pc.u0 && ulen < pc.u1 && warp == (int)((cu.k + i) % NCW))
-                attend_rows_mk<D, 16>((const uint8_t*)sm.nk[i], (const uint8_t*)sm.nv[i], nullptr,
-                                      nullptr, 0, D, 1, qreg, su, false);
-            park_warp_state<D, 16>(sm, su, i, 1);
-        }
-    }
-    consumers_sync();
-    stamp(a, sm, 12);
-    // one CTA-level fold of every (piece, kind, warp) state -> this CTA's partials
-    for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
-        const int i = t / D, cix = t - i * D;
-        float M = -CUDART_INF_F;
+                for (int b = 0; b < PB; ++b) dot[b] += __shfl_xor_sync(0xffffffffu, dot[b], off);
+            if (sub == 0) {
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int w = 0; w < NCW; ++w)
-                if (sm.ws_l[i][k][w] > 0.0f) M = fmaxf(M, sm.ws_m[i][k][w]);
-        float Ls = 0.0f, O = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int w = 0; w < NCW; ++w) {
-                const float l = sm.ws_l[i][k][w];
-                if (l > 0.0f) {
-                    const float sc = exp2f((sm.ws_m[i][k][w] - M) * kLog2e);
-                    Ls += l * sc;
-                    O += sm.ws_o[i][k][w][cix] * sc;
+                for (int b = 0; b < PB; ++b) {
+                    const int row = (p0 + b) * RPP + rsub;
+                    if (row < n) ll_st(out + r + row, dot[b], tag);
                 }
             }
-        float* outp = a.ws + ((size_t)c * 2 + i) * (D + 2);
-        outp[2 + cix] = O;
-        if (cix == 0) {
-            outp[0] = M;
-            outp[1] = Ls;
+            if (p0 * RPP + PB * RPP >= n) break;
+        }
+        ring_release(sm, cu.k + j);
+    }
+    cu.k += nst;
+}
+
+// R: this CTA's output elements [e0, e1): the H per-head partials summed in
+// head order.  Tagged for the next layer, or (last layer) the step output.
+template <int D>
+__device__ __forceinline__ void reduce_heads(const MegaArgs& a, Smem<D>& sm, Split el, int h, bool last,
+                                             int step, uint32_t tag) {
+    const int ne = el.r1 - el.r0, nw = a.H * ne;
+    constexpr int W = 4;  // H * ne <= 64 * 14 < 4 * 256 for every supported shape
+    unsigned long long w[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int t = k * NCW * 32 + threadIdx.x;
+        if (t < nw) w[k] = ll_ld(a.ll_xpart + (size_t)(t / ne) * h + el.r0 + t % ne);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int t = k * NCW * 32 + threadIdx.x;
+        if (t < nw) sm.xs[t] = ll_spin(a.ll_xpart + (size_t)(t / ne) * h + el.r0 + t % ne, w[k], tag);
+    }
+    consumers_sync();
+    if (threadIdx.x < ne) {
+        float s = 0.0f;
+        for (int hh = 0; hh < a.H; ++hh) s += sm.xs[hh * ne + threadIdx.x];
+        const int e = el.r0 + threadIdx.x;
+        if (last) {
+            a.x[e] = s;
+            a.hist[(size_t)step * h + e] = s;
+        } else {
+            ll_st(a.ll_x + e, s, tag);
         }
     }
     consumers_sync();
-    // publish; the last CTA to finish a head merges it (one warp per head, every
-    // load of the merge in flight at once) into the attention output
-    if (threadIdx.x == 0) {
-        int nm = 0;
-        for (int i = 0; i < pl.n; ++i) {
-            const int hh = pl.p[i].head;
-            unsigned prev;
-            // release: this CTA's partials (ordered by the bar.sync above);
-            // acquire: every other contributor's partials for the merger
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                         : "=r"(prev) : "l"(&a.head_ctr[hh]) : "memory");
-            if (prev == (unsigned)sm.hcount[hh] - 1) {
-                a.head_ctr[hh] = 0u;  // re-arm (next use is after a grid barrier)
-                sm.merge_head[nm++] = hh;
-            }
-        }
-        sm.merge_heads_n = nm;
-    }
-    consumers_sync();
-    stamp(a, sm, 13);
-    if (warp < sm.merge_heads_n) merge_one_head<D>(a, sm, sm.merge_head[warp]);
-    consumers_sync();
-    stamp(a, sm, 14);
 }
 
 // Per-step merge topology (depends only on the step's user length): the first
@@ -820,99 +1040,83 @@ __device__ __forceinline__ void plan_merge(const MegaArgs& a, Smem<D>& sm, int G
         const int u0 = cc * TU / G, u1 = (cc + 1) * TU / G;
         sm.ch0[cc] = u0 < u1 ? u0 / per : -1;
     }
-    consumers_sync();
     for (int hh = threadIdx.x; hh < a.H; hh += NCW * 32) {
-        const int f = owner32(hh * per, G, TU), l = owner32((hh + 1) * per - 1, G, TU);
-        int n = 0;
-        for (int cc = f; cc <= l; ++cc) n += sm.ch0[cc] >= 0;
-        sm.hfirst[hh] = f;
-        sm.hlast[hh] = l;
-        sm.hcount[hh] = n;
+        sm.hfirst[hh] = owner32(hh * per, G, TU);
+        sm.hlast[hh] = owner32((hh + 1) * per - 1, G, TU);
     }
     consumers_sync();
 }
 
 template <int D, int KC>
 __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_constant__ MegaArgs a) {
-    extern __shared__ uint8_t smem_raw[];
-    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    // (declared aligned and cast directly, so every access compiles to LDS/STS:
+    // an integer round trip would lose the address space and give generic loads)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
     const int c = blockIdx.x, G = gridDim.x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = a.H * D;
     const int ulen = a.state->user_len;  // user rows before this token
     const int step = a.state->step;
-    const unsigned long long base = a.sync[1];  // barrier counter value at launch
-    if (a.trace && threadIdx.x == 0) a.trace[(size_t)a.L * 6 * G + c] = gtimer();  // start
+    const uint32_t epoch = *(volatile unsigned*)a.sync;
+    if (a.trace && threadIdx.x == 0) a.trace[((size_t)a.L * G + c) * 16] = gtimer();  // start
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
+        sm.prod_k[0] = sm.prod_k[1] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == NCW) {  // producer
-        if (lane == 0) produce<D>(a, sm, c, G, ulen);
+    if (warp >= NCW) {  // producers, then the L2 prefetcher
+        if (lane == 0) {
+            if (warp < NCW + NPW) produce<D, false>(a, sm, c, G, ulen, warp - NCW);
+            else if (a.prefetch_stages > 0) produce<D, true>(a, sm, c, G, ulen, 0);
+        }
         return;
     }
     Cursor cu;
-    const Split qrows = rows_of(c, G, 3 * h), orows = rows_of(c, G, h);
+    const Split qrows = rows_of(c, G, 3 * h), elems = rows_of(c, G, h);
     const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
+    const OPlan op = plan_outproj(c, G, a.H, h);
     plan_merge<D>(a, sm, G, ulen + 1);
-    unsigned long long nb = 0;  // barriers passed in this launch
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
-        unsigned long long* tr = a.trace ? a.trace + (size_t)(3 * l) * 2 * G : nullptr;
-        // ---- P1: QKV (input transform fused at layer 0) ----
-        if (threadIdx.x == 0) {
-            sm.trace_on = (l == a.L - 1);
-            sm.phase_id = 0;
-            for (int i = 0; i < 4; ++i) sm.wait_cycles[i] = 0;
-        }
+        const uint32_t tag = epoch * 128u + (uint32_t)l + 1u;
+        stamp(a, l, 0);
+        if (a.trace && threadIdx.x == 0) sm.twait[0] = sm.twait[1] = sm.twait[2] = 0;
+        set_tphase(a, sm, 0);
+        // ---- A: QKV (input transform fused at layer 0) ----
+        stage_x<D>(a, sm, h, l, tag - 1u, ulen);
+        stamp(a, l, 1);
+        proj_qkv<D, KC>(a, ly, sm, cu, qrows, h, ulen, tag);
+        stamp(a, l, 2);
+        set_tphase(a, sm, 1);
+        // ---- B: attention ----
+        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        stamp(a, l, 4);
+        // ---- C: merge + output-projection column blocks of this CTA's heads ----
+        if (warp < op.n) merge_head<D>(a, sm, op.p[warp].head, warp, tag);
         consumers_sync();
-        stamp(a, sm, 0);
-        stage_vector<D>(sm, a.x, h, a.gamma, a.bias,
-                        l == 0 ? a.pos + (size_t)(a.S + ulen) * h : nullptr);
-        stamp(a, sm, 1);
-        proj_rows<D, KC>(sm, cu, qrows, h, [&](int n, float v) {
-            const int part = n / h, rem = n - part * h;
-            if (part == 0) {
-                a.q[rem] = v;
-            } else {
-                const int head = rem / D, cix = rem - head * D;
-                uint16_t* dst = part == 1 ? ly.uk : ly.uv;
-                dst[((size_t)head * a.cap + ulen) * D + cix] = f32_to_bf16_bits(v);
-            }
-        });
-        stamp(a, sm, 3);
-        grid_sync(a.sync, base + (++nb) * G, tr);
-        if (threadIdx.x == 0) sm.phase_id = 1;
-        // ---- P2: attention ----
-        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, G, ulen);
-        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, G, ulen);
-        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, G, ulen);
-        grid_sync(a.sync, base + (++nb) * G, tr ? tr + 2 * G : nullptr);
-        // ---- P3: output projection ----
-        if (threadIdx.x == 0) sm.phase_id = 2;
-        stamp(a, sm, 20);
-        stage_vector<D>(sm, a.concat, h, nullptr, nullptr, nullptr);
-        stamp(a, sm, 21);
-        const bool last = l == a.L - 1;
-        proj_rows<D, KC>(sm, cu, orows, h, [&](int n, float v) {
-            a.x[n] = v;
-            if (last) a.hist[(size_t)step * h + n] = v;
-        });
-        stamp(a, sm, 22);
-        if (sm.trace_on && threadIdx.x == 0 && a.trace)
-            for (int i = 0; i < 3; ++i)
-                a.trace[(size_t)(6 * a.L + 1) * G + (size_t)c * 32 + 28 + i] = sm.wait_cycles[i];
-
-        grid_sync(a.sync, base + (++nb) * G, tr ? tr + 4 * G : nullptr);
+        stamp(a, l, 5);
+        set_tphase(a, sm, 2);
+        for (int i = 0; i < op.n; ++i) proj_wo<D>(a, sm, cu, op.p[i], i, h, tag);
+        stamp(a, l, 6);
+        // ---- R: sum over heads ----
+        reduce_heads<D>(a, sm, elems, h, l == a.L - 1, step, tag);
+        stamp(a, l, 7);
+        if (a.trace && threadIdx.x == 0)
+            for (int i = 0; i < 3; ++i) a.trace[((size_t)l * G + c) * 16 + 8 + i] = sm.twait[i];
     }
     if (c == 0 && threadIdx.x == 0) {
+        // every CTA read state/epoch before its first A, and this CTA's last R
+        // needed every CTA's last A
         a.state->user_len = ulen + 1;
         a.state->step = step + 1;
-        a.sync[1] = base + nb * G;  // every CTA read `base` before the first barrier
+        *(volatile unsigned*)a.sync = epoch + 1u;
     }
 }
 
@@ -920,14 +1124,16 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
 
 size_t mega_smem_bytes(int D) {
     switch (D) {
-        case 32: return sizeof(mk::Smem<32>) + 128;
-        case 64: return sizeof(mk::Smem<64>) + 128;
-        default: return sizeof(mk::Smem<128>) + 128;
+        case 32: return sizeof(mk::Smem<32>);
+        case 64: return sizeof(mk::Smem<64>);
+        default: return sizeof(mk::Smem<128>);
     }
 }
 
+int mega_wo_box_rows(int D) { return mk::STAGE / (2 * D); }
+
 bool mega_supported(int L, int H, int D, int S, int h) {
-    if (L > kMegaMaxLayers || H > 148 || S % mk::UNIT != 0) return false;
+    if (L > kMegaMaxLayers || H > 64 || S % mk::UNIT != 0) return false;
     if (!(D == 32 || D == 64 || D == 128)) return false;
     if (h % 256 != 0 || h > 2048) return false;  // x held in registers (KC <= 8)
     if (mk::STAGE / (h * 2) < 1) return false;
@@ -949,7 +1155,7 @@ static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].id = cudaLaunchAttributeCooperative;  // co-residency of every CTA (the dataflow waits)
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
@@ -970,6 +1176,7 @@ static void launch_d(const MegaArgs& a, int grid, int kc, cudaStream_t st) {
 
 void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st) {
     require(num_sms <= 160, "decode megakernel: at most 160 SMs", EKV_EUNSUPPORTED);
+    require(a.H * a.D >= num_sms, "decode megakernel: hidden size below the SM count", EKV_EUNSUPPORTED);
     const int kc = a.H * a.D / 256;
     switch (a.D) {
         case 32: launch_d<32>(a, num_sms, kc, st); break;

@@ -367,8 +367,9 @@ class Session:
         return "mega" if act.value == 0 else "graph"
 
     def trace_step(self, num_sms: int) -> np.ndarray:
-        """Persistent path: %globaltimer stamps of one step, [(6L+1)*G] (see ekv_capi.h)."""
-        n = (6 * self.model.L + 1) * num_sms + 32 * num_sms
+        """Persistent path: phase stamps and ring counters of one step, [16*(L+1)*G]
+        (see ekv_capi.h)."""
+        n = 16 * (self.model.L + 1) * num_sms
         out = np.zeros(n, dtype=np.uint64)
         got = C.c_int()
         call("ekv_session_trace_step", self.hnd, out.ctypes.data_as(C.POINTER(C.c_uint64)), n,

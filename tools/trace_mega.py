@@ -1,4 +1,5 @@
-"""Per-barrier timeline of one persistent decode step (diagnostics)."""
+"""Phase timeline of one persistent decode step (diagnostics): per layer, the
+mean/max over CTAs of each phase's duration and of the waits for its inputs."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -11,35 +12,30 @@ kvc = ek.AssembledContext(m, S, [16] * (L - DEEP) + [8] * DEEP, group=d); kvc.sy
 sess = ek.Session(m, kvc, 128)
 sess.forward(torch.zeros((16, H * d), device="cuda"))
 sess.decode(3)
-t = sess.trace_step(G).astype(np.int64).reshape(-1)
-start = t[6 * L * G:6 * L * G + G]
-bars = t[:6 * L * G].reshape(3 * L, 2, G)
+t = sess.trace_step(G).astype(np.int64).reshape(L + 1, G, 16)
+st = t[:L, :, :8]
+start = t[L, :, 0]
 t0 = start.min()
-print("start spread us", (start.max() - start.min()) / 1e3)
-prev_rel = start
-names = ["P1 qkv", "P2 attn", "P3 out"]
-tot = {n: 0.0 for n in names}
-for b in range(3 * L):
-    arr, rel = bars[b, 0], bars[b, 1]
-    work = (arr - prev_rel) / 1e3          # per-CTA phase work time
-    sync = (rel - arr) / 1e3
-    if b < 9 or b >= 3 * L - 3:
-        print(f"L{b//3:2d} {names[b%3]:7s} work mean {work.mean():7.2f} max {work.max():7.2f} (cta {work.argmax():3d}) | "
-              f"barrier wait mean {sync.mean():6.2f} | last arrival->release {(rel.min()-arr.max())/1e3:6.2f}")
-    tot[names[b % 3]] += (rel.max() - prev_rel.min()) / 1e3
-    prev_rel = rel
-print("phase totals us", {k: round(v, 1) for k, v in tot.items()}, "step us", (bars[-1, 1].max() - t0) / 1e3)
-
-sub = t[(6 * L + 1) * G:].reshape(G, 32).astype(np.int64)
-names = {0: "P1 start", 1: "x staged", 3: "qkv done", 10: "P2 start", 11: "q staged", 12: "rows done",
-         13: "partials+atomics", 14: "merge", 20: "P3 start", 21: "concat staged", 22: "out proj done"}
-for cta in [0, 18, 70, 120]:
-    row = sub[cta]
-    out = []
-    prev = None
-    for k in sorted(names):
-        if row[k] > 0:
-            if prev is not None:
-                out.append(f"{names[k]} +{(row[k] - prev) / 1e3:.2f}")
-            prev = row[k]
-    print("cta", cta, "| ".join(out), "| ring-wait cycles (sum over warps) P1/P2/P3:", row[28:31])
+print(f"CTA start spread {(start.max() - start.min()) / 1e3:.2f} us; step {(st[-1, :, 7].max() - t0) / 1e3:.1f} us")
+pr = t[L]
+print(f"producer: stages/CTA {pr[:, 3].mean():.0f}, busy {(pr[:, 2] - pr[:, 1]).mean() / 1e3:.1f} us, "
+      f"waiting for free slots {pr[:, 4].mean() / pr[:, 5].mean() * 100:.1f}% of its cycles")
+names = ["x wait", "A qkv", "qkv wait", "B attn", "merge", "C outproj", "R reduce"]
+tot = np.zeros(7)
+rw = np.zeros(3)
+for l in range(L):
+    seg = np.diff(st[l], axis=1) / 1e3  # [G][7]
+    tot += seg.mean(0)
+    rw += t[l, :, 8:11].mean(0) / 8 / 1.9e3  # per-warp us at ~1.9 GHz
+    if l < 3 or l >= L - 2:
+        print(f"L{l:2d} " + " | ".join(f"{n} {seg[:, i].mean():5.2f}/{seg[:, i].max():5.2f}" for i, n in enumerate(names))
+              + f" | layer {(st[l, :, 7].max() - st[l, :, 0].min()) / 1e3:6.2f}"
+              + " | ring wait/warp A,B,C " + " ".join(f"{v / 8 / 1.9e3:.2f}" for v in t[l, :, 8:11].mean(0)))
+print("sum over layers of per-CTA mean (us):", {n: round(v, 1) for n, v in zip(names, tot)})
+print("sum over layers of per-warp ring wait (us) A,B,C:", np.round(rw, 1))
+if os.environ.get("DBG"):
+    for l in [1, 5, 15]:
+        for cta in [0, 40, 100]:
+            row = t[l, cta]
+            base = row[1]
+            print("dbg L", l, "cta", cta, [round((row[k] - base) / 1e3, 2) if row[k] else None for k in [2, 11, 12, 13, 14, 15]])
