@@ -329,6 +329,9 @@ struct Smem {
     float os[2][D];               // merged attention output of this CTA's W_o heads
     float ws_o[2][2][NCW][D];     // per (piece, context/user, warp) partial output
     float ws_m[2][2][NCW], ws_l[2][2][NCW];
+    float fsc[2][2 * NCW];        // fold: rescale factor of each (kind, warp) state
+    AttnPlan pl;                  // this CTA's attention pieces (shared: indexed at run time,
+    OPlan op;                     // a per-thread copy would live in local memory)
     int hfirst[160], hlast[160];  // contributing CTA range of each head's attention
     int ch0[160];                 // first attention head of each CTA (-1: idle CTA)
     volatile long long prod_k[2]; // stages issued so far by each producer (for the prefetcher)
@@ -425,8 +428,8 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
     pr.sel = sel;
     const int h = a.H * D;
     const Split q = rows_of(c, G, 3 * h);
-    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
-    const OPlan op = plan_outproj(c, G, a.H, h);
+    const AttnPlan& pl = sm.pl;
+    const OPlan& op = sm.op;
     const int rpw = STAGE / (h * 2);
     const int ucap = att_stage_rows(D * 2, 0);
     constexpr int RPS = STAGE / (2 * D);
@@ -846,101 +849,109 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
         }
     }
     consumers_sync();
-    // one CTA-level fold of every (piece, kind, warp) state -> this CTA's tagged partials
+    // CTA-level fold of every (piece, kind, warp) state -> this CTA's tagged
+    // partials: warp 0 computes the 2*2*NCW rescale factors and the totals
+    // (one lane per state), then every column is an independent 2*NCW-term sum.
+    static_assert(2 * NCW <= 32, "one lane per (kind, warp) state");
+    if (warp == 0) {
+        for (int i = 0; i < pl.n; ++i) {
+            const int k = lane / NCW, w = lane % NCW;
+            const bool on = lane < 2 * NCW && sm.ws_l[i][k][w] > 0.0f;
+            const float m = on ? sm.ws_m[i][k][w] : -CUDART_INF_F;
+            const float M = warp_max(m);
+            const float sc = on ? exp2f((m - M) * kLog2e) : 0.0f;
+            const float Ls = warp_sum(on ? sm.ws_l[i][k][w] * sc : 0.0f);
+            if (lane < 2 * NCW) sm.fsc[i][lane] = sc;
+            if (lane == 0) {
+                uint64_t* outp = a.ll_part + ((size_t)c * 2 + i) * (D + 2);
+                ll_st(outp, M, tag);
+                ll_st(outp + 1, Ls, tag);
+            }
+        }
+    }
+    consumers_sync();
     for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
         const int i = t / D, cix = t - i * D;
-        float M = -CUDART_INF_F;
+        float o0 = 0.0f, o1 = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int w = 0; w < NCW; ++w)
-                if (sm.ws_l[i][k][w] > 0.0f) M = fmaxf(M, sm.ws_m[i][k][w]);
-        float Ls = 0.0f, O = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-#pragma unroll
-            for (int w = 0; w < NCW; ++w) {
-                const float lw = sm.ws_l[i][k][w];
-                if (lw > 0.0f) {
-                    const float sc = exp2f((sm.ws_m[i][k][w] - M) * kLog2e);
-                    Ls += lw * sc;
-                    O += sm.ws_o[i][k][w][cix] * sc;
-                }
-            }
-        uint64_t* outp = a.ll_part + ((size_t)c * 2 + i) * (D + 2);
-        ll_st(outp + 2 + cix, O, tag);
-        if (cix == 0) {
-            ll_st(outp, M, tag);
-            ll_st(outp + 1, Ls, tag);
+        for (int w = 0; w < NCW; ++w) {
+            o0 = fmaf(sm.ws_o[i][0][w][cix], sm.fsc[i][w], o0);
+            o1 = fmaf(sm.ws_o[i][1][w][cix], sm.fsc[i][NCW + w], o1);
         }
+        ll_st(a.ll_part + ((size_t)c * 2 + i) * (D + 2) + 2 + cix, o0 + o1, tag);
     }
     // (the next consumers_sync is in the caller, before shared state is reused)
 }
 
-// C, part 1: merge of head hh's partials (Eq. 5 generalised to the CTAs that
-// attended the head) by one warp: every tagged load in flight before any use,
-// per-lane math (each lane owns D/32 output columns), result to sm.os[slot].
+// C, part 1: merge of the partials of this CTA's W_o heads (Eq. 5 generalised
+// to the CTAs that attended each head).  All consumer threads stage up to 8
+// contributors per head at a time into shared memory (every tagged load in
+// flight before any use), then one thread per (head, column) folds them
+// online; the result is the normalised head output in sm.os[slot].
+// Missing contributors are staged as (m = 0, l = 0): every staged value stays
+// finite (the staging area is the fold's ws_o, which must stay finite).
 template <int D>
-__device__ __forceinline__ void merge_head(const MegaArgs& a, Smem<D>& sm, int hh, int slot, uint32_t tag) {
-    constexpr int MAXC = 4;
-    constexpr int VPL = (D + 31) / 32;
-    const int lane = threadIdx.x & 31;
-    const int first = sm.hfirst[hh], last = sm.hlast[hh];
-    float M = -CUDART_INF_F, Ls = 0.0f, O[VPL];
+__device__ __forceinline__ void merge_heads(const MegaArgs& a, Smem<D>& sm, const OPlan& op, uint32_t tag) {
+    constexpr int MAXC = 8, W = D + 2;
+    static_assert(2 * MAXC * W <= 2 * 2 * NCW * D, "staging fits the fold buffer");
+    float* stage = &sm.ws_o[0][0][0][0];  // [2 slots][MAXC][D + 2]
+    const int t = threadIdx.x;
+    const int col = t % D, slot = t / D;
+    const bool mine = t < op.n * D;
+    float M = -CUDART_INF_F, Ls = 0.0f, O = 0.0f;
+    int most = 0;
+    for (int s2 = 0; s2 < op.n; ++s2) {
+        const int hh = op.p[s2].head;
+        most = max(most, sm.hlast[hh] - sm.hfirst[hh] + 1);
+    }
+    consumers_sync();  // the fold has finished reading ws_o
+    for (int base = 0; base < most; base += MAXC) {
+        constexpr int PER = (2 * MAXC * W + NCW * 32 - 1) / (NCW * 32);
+        unsigned long long w[PER];
+        const uint64_t* src[PER];
 #pragma unroll
-    for (int t = 0; t < VPL; ++t) O[t] = 0.0f;
-    for (int c0 = first; c0 <= last; c0 += MAXC) {
-        unsigned long long wm[MAXC], wl[MAXC], wv[MAXC][VPL];
-        const uint64_t* pp[MAXC];
-        bool ok[MAXC];
-#pragma unroll
-        for (int j = 0; j < MAXC; ++j) {
-            const int cc = c0 + j;
-            ok[j] = cc <= last && sm.ch0[cc] >= 0;
-            const int sl = ok[j] && sm.ch0[cc] == hh ? 0 : 1;
-            pp[j] = a.ll_part + ((size_t)(ok[j] ? cc : first) * 2 + sl) * (D + 2);
-            if (ok[j]) {
-                wm[j] = ll_ld(pp[j]);
-                wl[j] = ll_ld(pp[j] + 1);
-#pragma unroll
-                for (int t = 0; t < VPL; ++t)
-                    if (lane + 32 * t < D) wv[j][t] = ll_ld(pp[j] + 2 + lane + 32 * t);
+        for (int k = 0; k < PER; ++k) {
+            const int idx = k * NCW * 32 + t;
+            src[k] = nullptr;
+            if (idx < op.n * MAXC * W) {
+                const int s2 = idx / (MAXC * W), rem = idx - s2 * MAXC * W;
+                const int j = rem / W, e = rem - j * W;
+                const int hh = op.p[s2].head;
+                const int cc = sm.hfirst[hh] + base + j;
+                if (cc <= sm.hlast[hh] && sm.ch0[cc] >= 0) {
+                    const int sl = sm.ch0[cc] == hh ? 0 : 1;
+                    src[k] = a.ll_part + ((size_t)cc * 2 + sl) * W + e;
+                    w[k] = ll_ld(src[k]);
+                } else {
+                    stage[idx] = 0.0f;  // (m, l, o) = 0: ignored (l == 0)
+                }
             }
         }
-        float m[MAXC], l[MAXC], v[MAXC][VPL];
 #pragma unroll
-        for (int j = 0; j < MAXC; ++j) {
-            m[j] = ok[j] ? ll_spin(pp[j], wm[j], tag) : -CUDART_INF_F;
-            l[j] = ok[j] ? ll_spin(pp[j] + 1, wl[j], tag) : 0.0f;
+        for (int k = 0; k < PER; ++k)
+            if (src[k]) stage[k * NCW * 32 + t] = ll_spin(src[k], w[k], tag);
+        consumers_sync();
+        if (mine) {
+            const float* st = stage + slot * MAXC * W;
+            float Mn = M;
 #pragma unroll
-            for (int t = 0; t < VPL; ++t) {
-                const int cix = lane + 32 * t;
-                v[j][t] = (ok[j] && cix < D) ? ll_spin(pp[j] + 2 + cix, wv[j][t], tag) : 0.0f;
+            for (int j = 0; j < MAXC; ++j)
+                if (st[j * W + 1] > 0.0f) Mn = fmaxf(Mn, st[j * W]);
+            const float corr = M == -CUDART_INF_F ? 0.0f : exp2f((M - Mn) * kLog2e);
+            Ls *= corr;
+            O *= corr;
+#pragma unroll
+            for (int j = 0; j < MAXC; ++j) {
+                const float l = st[j * W + 1];
+                const float sc = l > 0.0f ? exp2f((st[j * W] - Mn) * kLog2e) : 0.0f;
+                Ls += l * sc;
+                O += st[j * W + 2 + col] * sc;
             }
+            M = Mn;
         }
-        float Mn = M;
-#pragma unroll
-        for (int j = 0; j < MAXC; ++j)
-            if (l[j] > 0.0f) Mn = fmaxf(Mn, m[j]);
-        const float corr = M == -CUDART_INF_F ? 0.0f : exp2f((M - Mn) * kLog2e);
-        Ls *= corr;
-#pragma unroll
-        for (int t = 0; t < VPL; ++t) O[t] *= corr;
-#pragma unroll
-        for (int j = 0; j < MAXC; ++j) {
-            const float w = l[j] > 0.0f ? exp2f((m[j] - Mn) * kLog2e) : 0.0f;
-            Ls += l[j] * w;
-#pragma unroll
-            for (int t = 0; t < VPL; ++t) O[t] += w * v[j][t];
-        }
-        M = Mn;
+        consumers_sync();
     }
-    const float inv = 1.0f / Ls;
-#pragma unroll
-    for (int t = 0; t < VPL; ++t) {
-        const int cix = lane + 32 * t;
-        if (cix < D) sm.os[slot][cix] = O[t] * inv;
-    }
+    if (mine) sm.os[slot][col] = O / Ls;
 }
 
 // C, part 2: rows [n0, n1) of W_o[:, head] (2-D boxes from the ring, RPS rows of
@@ -1066,6 +1077,8 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
             mbar_init(&sm.empty[i], 1);
         }
         sm.prod_k[0] = sm.prod_k[1] = 0;
+        sm.pl = plan_attention(c, G, a.H, a.S, ulen + 1);
+        sm.op = plan_outproj(c, G, a.H, a.H * D);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1078,8 +1091,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     }
     Cursor cu;
     const Split qrows = rows_of(c, G, 3 * h), elems = rows_of(c, G, h);
-    const AttnPlan pl = plan_attention(c, G, a.H, a.S, ulen + 1);
-    const OPlan op = plan_outproj(c, G, a.H, h);
+    const AttnPlan& pl = sm.pl;
+    const OPlan& op = sm.op;
+    // the fold multiplies every parked state by its factor (0 for empty ones):
+    // start from finite values
+    for (int i = threadIdx.x; i < 2 * 2 * NCW * D; i += NCW * 32) (&sm.ws_o[0][0][0][0])[i] = 0.0f;
     plan_merge<D>(a, sm, G, ulen + 1);
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
@@ -1099,7 +1115,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
         else attention_phase<D, 4>(a, ly, sm, cu, pl, c, ulen, l, tag);
         stamp(a, l, 4);
         // ---- C: merge + output-projection column blocks of this CTA's heads ----
-        if (warp < op.n) merge_head<D>(a, sm, op.p[warp].head, warp, tag);
+        merge_heads<D>(a, sm, op, tag);
         consumers_sync();
         stamp(a, l, 5);
         set_tphase(a, sm, 2);
