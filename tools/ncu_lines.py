@@ -69,7 +69,7 @@ def regions_from_source(path):
     """Region = from a phase function's definition line to the next one."""
     marks = [("producer", "__device__ void produce("), ("stage_x", "void stage_x("),
              ("A qkv", "void proj_qkv("), ("B attn", "void attend_rows_mk("),
-             ("C merge", "void merge_head("), ("C outproj", "void proj_wo("),
+             ("C merge", "void merge_heads("), ("C outproj", "void proj_wo("),
              ("R reduce", "void reduce_heads("), ("plan", "void plan_merge("),
              ("kernel", "decode_step_kernel(const")]
     src = open(path).read().split("\n")
