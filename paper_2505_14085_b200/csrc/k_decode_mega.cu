@@ -442,10 +442,12 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
     const int rpw = STAGE / (h * 2);
     const int ucap = att_stage_rows(D * 2, 0);
     constexpr int RPS = STAGE / (2 * D);
+    #pragma unroll 1
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
         // A: QKV rows in virtual head-major order; a stage never crosses more
         // than one (head, q|k|v) block boundary (rpw <= D for every supported shape)
+        #pragma unroll 1
         for (int r = q.r0; r < q.r1; r += rpw) {
             if (pr.mine()) {
                 const int n = min(rpw, q.r1 - r);
@@ -462,10 +464,12 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
         const int row_b = ly.fmt == 16 ? D * 2 : (ly.fmt == 8 ? D : D / 2);
         const int ng = ly.fmt == 16 ? 0 : D / ly.group;
         const int cap = att_stage_rows(row_b, ng);
+        #pragma unroll 1
         for (int i = 0; i < pl.n; ++i) {
             const Piece& pc = pl.p[i];
             const uint8_t* ck = ly.ck + (size_t)pc.head * a.S * row_b;
             const uint8_t* cv = ly.cv + (size_t)pc.head * a.S * row_b;
+            #pragma unroll 1
             for (int r = pc.c0; r < pc.c1; r += cap) {
                 if (pr.mine()) {
                     const int n = min(cap, pc.c1 - r);
@@ -482,6 +486,7 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
                 pr.advance();
             }
             const int ue = user_static_end(pc, ulen);
+            #pragma unroll 1
             for (int r = pc.u0; r < ue; r += ucap) {
                 if (pr.mine()) {
                     const int n = min(ucap, ue - r);
@@ -495,7 +500,9 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
         }
         // C: W_o head column blocks, one 2-D box of RPS rows x D columns per stage
         const int row0 = a.wo_row0 + l * a.wo_layer_rows;
+        #pragma unroll 1
         for (int i = 0; i < op.n; ++i) {
+            #pragma unroll 1
             for (int r = op.p[i].n0; r < op.p[i].n1; r += RPS) {
                 if (pr.mine()) {
                     uint8_t* dst = pr.acquire(STAGE);
