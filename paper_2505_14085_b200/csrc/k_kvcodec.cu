@@ -51,8 +51,10 @@ __device__ __forceinline__ uint32_t quant_bits(float x, float inv) {
 }
 
 // Tile kernel: TILE contiguous rows of one job are moved global -> shared by a
-// single bulk-async copy (TMA 1D, mbarrier completion), double-buffered, so the
-// HBM stream runs ahead of the quantisation.  8 kept channels per lane, LPR =
+// single bulk-async copy (TMA 1D, mbarrier completion) into an NS-stage ring,
+// so NS-1 tiles per CTA stay in flight while one is quantised.  Persistent:
+// the grid is exactly the resident CTAs, each walking the flattened (job, tile)
+// space with a grid stride (no second wave).  8 kept channels per lane, LPR =
 // DE/8 lanes per row, 32/LPR rows per warp pass; per-group absmax by xor
 // shuffles inside the row's lanes; 8 (int8) or 4 (int4) code bytes stored per
 // lane (coalesced rows).
@@ -61,24 +63,25 @@ struct TileCfg {
     static constexpr int TILE = 8192 / DC;              // rows per stage (16 KB)
     static constexpr int BYTES = TILE * DC * 2;         // 16 KB
 };
+constexpr int kCompressStages = 2;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
 template <int DC, int DE, int BITS>
-__global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs, int64_t rows,
+__global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs, int n_jobs, int64_t rows,
                                                                const int* __restrict__ kept,
                                                                int group) {
     using TC = TileCfg<DC>;
+    constexpr int NS = kCompressStages;
     constexpr int LPR = DE / 8, RPW = 32 / LPR, NWARP = 4;
     constexpr int PASSES = TC::TILE / (RPW * NWARP);
     constexpr float Q = BITS == 8 ? 127.0f : 7.0f;
     static_assert(PASSES >= 1 && TC::TILE % (RPW * NWARP) == 0, "tile shape");
-    __shared__ __align__(128) uint8_t buf[2][TC::BYTES];
-    __shared__ __align__(8) uint64_t bar[2];
-    const CompressJob job = jobs.job[blockIdx.y];
-    const uint8_t* src = (const uint8_t*)job.src;
+    extern __shared__ __align__(1024) uint8_t dyn[];
+    uint8_t (*buf)[TC::BYTES] = reinterpret_cast<uint8_t (*)[TC::BYTES]>(dyn);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(dyn + NS * TC::BYTES);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane % LPR, rsub = lane / LPR;
     const int glanes = group / 8;  // lanes per group (power of two, <= LPR)
@@ -87,14 +90,16 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
 #pragma unroll
     for (int e = 0; e < 8; ++e) ch2[e] = 2 * kept[sub * 8 + e];
     const int64_t ntiles = (rows + TC::TILE - 1) / TC::TILE;
+    const int64_t total = ntiles * n_jobs;
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[1])));
+        for (int i = 0; i < NS; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[i])));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    auto issue = [&](int64_t t, int stage) {
-        const int64_t r0 = t * TC::TILE;
+    auto issue = [&](int64_t T, int stage) {
+        const int jb = (int)(T / ntiles);
+        const int64_t r0 = (T - (int64_t)jb * ntiles) * TC::TILE;
         const int n = (int)min((int64_t)TC::TILE, rows - r0);
         const uint32_t bytes = (uint32_t)n * DC * 2;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
@@ -104,18 +109,19 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 smem_addr(buf[stage])),
-            "l"(src + r0 * DC * 2), "r"(bytes), "r"(smem_addr(&bar[stage]))
+            "l"((const uint8_t*)jobs.job[jb].src + r0 * DC * 2), "r"(bytes), "r"(smem_addr(&bar[stage]))
             : "memory");
     };
-    int64_t t = blockIdx.x;
-    if (threadIdx.x == 0 && t < ntiles) issue(t, 0);
-    uint32_t phase[2] = {0, 0};
-    for (int it = 0; t < ntiles; t += gridDim.x, ++it) {
-        const int stage = it & 1;
-        const int64_t tn = t + gridDim.x;
-        if (threadIdx.x == 0 && tn < ntiles) issue(tn, stage ^ 1);  // next tile in flight
-        // wait for this tile
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NS; ++i) {
+            const int64_t T = blockIdx.x + (int64_t)i * gridDim.x;
+            if (T < total) issue(T, i);
+        }
+    int it = 0;
+    for (int64_t T = blockIdx.x; T < total; T += gridDim.x, ++it) {
+        const int stage = it % NS;
         {
+            const uint32_t parity = (uint32_t)((it / NS) & 1);
             uint32_t done = 0;
             while (!done) {
                 asm volatile(
@@ -123,12 +129,13 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                     "selp.u32 %0, 1, 0, p;\n\t}"
                     : "=r"(done)
-                    : "r"(smem_addr(&bar[stage])), "r"(phase[stage])
+                    : "r"(smem_addr(&bar[stage])), "r"(parity)
                     : "memory");
             }
-            phase[stage] ^= 1;
         }
-        const int64_t r0 = t * TC::TILE;
+        const int jb = (int)(T / ntiles);
+        const CompressJob job = jobs.job[jb];
+        const int64_t r0 = (T - (int64_t)jb * ntiles) * TC::TILE;
         const uint8_t* tile = buf[stage];
 #pragma unroll
         for (int p = 0; p < PASSES; ++p) {
@@ -167,6 +174,10 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
             }
         }
         __syncthreads();  // every warp is done with this stage before it is refilled
+        if (threadIdx.x == 0) {
+            const int64_t Tn = T + (int64_t)NS * gridDim.x;
+            if (Tn < total) issue(Tn, stage);
+        }
     }
 }
 
@@ -224,12 +235,21 @@ static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c
     for (int i = 0; i < n_jobs; ++i)  // bulk copies need 16-byte aligned sources
         if (((uintptr_t)jobs.job[i].src & 15) || ((uintptr_t)jobs.job[i].codes & 7))
             return false;
-    const int64_t tiles = (rows + TileCfg<DC>::TILE - 1) / TileCfg<DC>::TILE;
-    int64_t bx = (148 * 12 + n_jobs - 1) / n_jobs;  // ~12 CTAs (2 tiles each in flight) per SM
-    if (bx > tiles) bx = tiles;
-    if (bx < 1) bx = 1;
-    kv_compress_tile_kernel<DC, DE, BITS><<<dim3((unsigned)bx, n_jobs), 128, 0, st>>>(jobs, rows, kept,
-                                                                                 group);
+    const int64_t total = (rows + TileCfg<DC>::TILE - 1) / TileCfg<DC>::TILE * n_jobs;
+    auto fn = kv_compress_tile_kernel<DC, DE, BITS>;
+    const int smem = kCompressStages * TileCfg<DC>::BYTES + 64;
+    static int occ = 0, sms = 0;
+    if (!occ) {
+        EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        EKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
+        int dev = 0;
+        EKV_CUDA(cudaGetDevice(&dev));
+        EKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (occ < 1) occ = 1;
+    }
+    int64_t grid = (int64_t)sms * occ;  // persistent: exactly the resident CTAs
+    if (grid > total) grid = total;
+    fn<<<(unsigned)grid, 128, smem, st>>>(jobs, n_jobs, rows, kept, group);
     return true;
 }
 
