@@ -348,17 +348,17 @@ struct Smem {
     unsigned long long twait[3];  // diagnostics: ring-wait cycles of A, B, C (sum over warps)
 };
 
-// Diagnostics (a.trace != nullptr): trace[(l*G + c)*16 + k], k = 0 layer start,
+// Diagnostics (TR): trace[(l*G + c)*16 + k], k = 0 layer start,
 // 1 x ready, 2 A done, 3 q/k/v ready, 4 B done, 5 partials merged, 6 C done,
 // 7 R done (%globaltimer ns); 8..10 = consumer ring-wait cycles in A, B, C.
 // trace[(L*G + c)*16 + k]: 0 CTA start, 1/2 producer start/end (ns), 3 stages
 // issued, 4 producer cycles waiting for free slots, 5 producer cycles total.
-__device__ __forceinline__ void stamp(const MegaArgs& a, int l, int k) {
-    if (a.trace && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + k] = gtimer();
+__device__ __forceinline__ void stamp(const MegaArgs& a, bool tr, int l, int k) {
+    if (tr && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + k] = gtimer();
 }
 template <class SM>
-__device__ __forceinline__ void set_tphase(const MegaArgs& a, SM& sm, int ph) {
-    if (a.trace && threadIdx.x == 0) sm.tphase = ph;
+__device__ __forceinline__ void set_tphase(bool tr, SM& sm, int ph) {
+    if (tr && threadIdx.x == 0) sm.tphase = ph;
 }
 
 // Per-piece schedule pieces that go through the ring: context rows [c0, c1) and
@@ -422,7 +422,7 @@ struct Prod {
     }
 };
 
-template <int D, bool PF>
+template <int D, bool PF, bool TR>
 __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, int sel) {
     const long long p0 = clock64();
     const unsigned long long g0 = gtimer();
@@ -433,7 +433,7 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
     pr.full = sm.full;
     pr.empty = sm.empty;
     pr.ring = &sm.ring[0][0];
-    pr.trace = a.trace != nullptr;
+    pr.trace = TR;
     pr.sel = sel;
     const int h = a.H * D;
     const Split q = rows_of(c, G, 3 * h);
@@ -512,7 +512,7 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
             }
         }
     }
-    if (a.trace && sel == 0 && !PF) {
+    if (TR && sel == 0 && !PF) {
         unsigned long long* t = a.trace + ((size_t)a.L * G + c) * 16;
         t[1] = g0;
         t[2] = gtimer();
@@ -593,7 +593,7 @@ __device__ __forceinline__ void stage_x(const MegaArgs& a, Smem<D>& sm, int h, i
 // from the ring, x from shared memory into registers once (lane holds
 // x[c*256 + lane*8 + e]).  q goes out as tagged words; k and v are rounded to
 // bf16, appended to the user cache, and go out as tagged words too.
-template <int D, int KC>
+template <int D, int KC, bool TR>
 __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm, Cursor& cu,
                                          Split rows, int h, int ulen, uint32_t tag) {
     const int lane = threadIdx.x & 31;
@@ -611,7 +611,7 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
     for (int j = first_owned(cu); j < nst; j += NCW) {
         const int r = rows.r0 + j * rows_per_w;
         const int n = min(rows_per_w, rows.r1 - r);
-        const uint8_t* st = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+        const uint8_t* st = ring_acquire(sm, cu.k + j, TR);
         for (int i0 = 0; i0 < n; i0 += RG) {
             const uint8_t* wr[RG];
 #pragma unroll
@@ -778,7 +778,7 @@ __device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>:
 // B: attention of the CTA's pieces.  q and this step's K/V row of each head
 // arrive as tagged words from A; the context and earlier user rows come
 // through the ring.  Ends with one tagged (m, l, o) partial per piece.
-template <int D, int FMT>
+template <int D, int FMT, bool TR>
 __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
                                                 Cursor& cu, const AttnPlan& pl, int c, int ulen,
                                                 int l, uint32_t tag) {
@@ -811,7 +811,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
         }
     }
     consumers_sync();
-    stamp(a, l, 3);
+    stamp(a, TR, l, 3);
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
         {   // context rows (ring)
@@ -825,7 +825,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             for (int j = first_owned(cu); j < nst; j += NCW) {
                 const int r = pc.c0 + j * cap;
                 const int n = min(cap, pc.c1 - r);
-                const uint8_t* s = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+                const uint8_t* s = ring_acquire(sm, cu.k + j, TR);
                 const int kbytes = n * F::ROW;
                 attend_rows_mk<D, FMT, att_passes<D, FMT>()>(s, s + kbytes, (const float*)(s + 2 * kbytes),
                                        (const float*)(s + 2 * kbytes + n * ng * 4), ng, ly.group, n,
@@ -851,7 +851,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             for (int j = first_owned(cu); j < nsu; j += NCW) {
                 const int r = pc.u0 + j * ucap;
                 const int n = min(ucap, ue - r);
-                const uint8_t* s = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+                const uint8_t* s = ring_acquire(sm, cu.k + j, TR);
                 attend_rows_mk<D, 16, att_passes<D, 16>()>(s, s + n * D * 2, nullptr, nullptr, 0, D, n,
                                                             qu, su);
                 ring_release(sm, cu.k + j);
@@ -972,7 +972,7 @@ __device__ __forceinline__ void merge_heads(const MegaArgs& a, Smem<D>& sm, cons
 
 // C, part 2: rows [n0, n1) of W_o[:, head] (2-D boxes from the ring, RPS rows of
 // D bf16 each) dotted with the merged head output -> tagged per-head partials.
-template <int D>
+template <int D, bool TR>
 __device__ __forceinline__ void proj_wo(const MegaArgs& a, Smem<D>& sm, Cursor& cu, const OPiece& op,
                                         int slot, int h, uint32_t tag) {
     constexpr int LPR = D / 8;  // lanes per row, 8 bf16 each
@@ -987,7 +987,7 @@ __device__ __forceinline__ void proj_wo(const MegaArgs& a, Smem<D>& sm, Cursor& 
     for (int j = first_owned(cu); j < nst; j += NCW) {
         const int r = op.n0 + j * RPS;
         const int n = min(RPS, op.n1 - r);
-        const uint8_t* st = ring_acquire(sm, cu.k + j, a.trace != nullptr);
+        const uint8_t* st = ring_acquire(sm, cu.k + j, TR);
         constexpr int PB = 4;  // passes in flight
         static_assert((RPS / RPP) % PB == 0, "pass batching");
 #pragma unroll 1
@@ -1074,7 +1074,7 @@ __device__ __forceinline__ void plan_merge(const MegaArgs& a, Smem<D>& sm, int G
     consumers_sync();
 }
 
-template <int D, int KC>
+template <int D, int KC, bool TR>
 __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_constant__ MegaArgs a) {
     // (declared aligned and cast directly, so every access compiles to LDS/STS:
     // an integer round trip would lose the address space and give generic loads)
@@ -1086,7 +1086,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     const int ulen = a.state->user_len;  // user rows before this token
     const int step = a.state->step;
     const uint32_t epoch = *(volatile unsigned*)a.sync;
-    if (a.trace && threadIdx.x == 0) a.trace[((size_t)a.L * G + c) * 16] = gtimer();  // start
+    if (TR && threadIdx.x == 0) a.trace[((size_t)a.L * G + c) * 16] = gtimer();  // start
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
@@ -1099,7 +1099,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     }
     __syncthreads();
     if (warp >= NCW) {  // producers
-        if (lane == 0) produce<D, false>(a, sm, c, G, ulen, warp - NCW);
+        if (lane == 0) produce<D, false, TR>(a, sm, c, G, ulen, warp - NCW);
         return;
     }
     Cursor cu;
@@ -1113,31 +1113,31 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     for (int l = 0; l < a.L; ++l) {
         const MegaLayer& ly = a.layer[l];
         const uint32_t tag = epoch * 128u + (uint32_t)l + 1u;
-        stamp(a, l, 0);
-        if (a.trace && threadIdx.x == 0) sm.twait[0] = sm.twait[1] = sm.twait[2] = 0;
-        set_tphase(a, sm, 0);
+        stamp(a, TR, l, 0);
+        if (TR && threadIdx.x == 0) sm.twait[0] = sm.twait[1] = sm.twait[2] = 0;
+        set_tphase(TR, sm, 0);
         // ---- A: QKV (input transform fused at layer 0) ----
         stage_x<D>(a, sm, h, l, tag - 1u, ulen);
-        stamp(a, l, 1);
-        proj_qkv<D, KC>(a, ly, sm, cu, qrows, h, ulen, tag);
-        stamp(a, l, 2);
-        set_tphase(a, sm, 1);
+        stamp(a, TR, l, 1);
+        proj_qkv<D, KC, TR>(a, ly, sm, cu, qrows, h, ulen, tag);
+        stamp(a, TR, l, 2);
+        set_tphase(TR, sm, 1);
         // ---- B: attention ----
-        if (ly.fmt == 16) attention_phase<D, 16>(a, ly, sm, cu, pl, c, ulen, l, tag);
-        else if (ly.fmt == 8) attention_phase<D, 8>(a, ly, sm, cu, pl, c, ulen, l, tag);
-        else attention_phase<D, 4>(a, ly, sm, cu, pl, c, ulen, l, tag);
-        stamp(a, l, 4);
+        if (ly.fmt == 16) attention_phase<D, 16, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        else if (ly.fmt == 8) attention_phase<D, 8, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        else attention_phase<D, 4, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        stamp(a, TR, l, 4);
         // ---- C: merge + output-projection column blocks of this CTA's heads ----
         merge_heads<D>(a, sm, op, tag);
         consumers_sync();
-        stamp(a, l, 5);
-        set_tphase(a, sm, 2);
-        for (int i = 0; i < op.n; ++i) proj_wo<D>(a, sm, cu, op.p[i], i, h, tag);
-        stamp(a, l, 6);
+        stamp(a, TR, l, 5);
+        set_tphase(TR, sm, 2);
+        for (int i = 0; i < op.n; ++i) proj_wo<D, TR>(a, sm, cu, op.p[i], i, h, tag);
+        stamp(a, TR, l, 6);
         // ---- R: sum over heads ----
         reduce_heads<D>(a, sm, elems, h, l == a.L - 1, step, tag);
-        stamp(a, l, 7);
-        if (a.trace && threadIdx.x == 0)
+        stamp(a, TR, l, 7);
+        if (TR && threadIdx.x == 0)
             for (int i = 0; i < 3; ++i) a.trace[((size_t)l * G + c) * 16 + 8 + i] = sm.twait[i];
     }
     if (c == 0 && threadIdx.x == 0) {
@@ -1169,9 +1169,9 @@ bool mega_supported(int L, int H, int D, int S, int h) {
     return true;
 }
 
-template <int D, int KC>
-static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
-    auto fn = mk::decode_step_kernel<D, KC>;
+template <int D, int KC, bool TR>
+static void launch_dkt(const MegaArgs& a, int grid, cudaStream_t st) {
+    auto fn = mk::decode_step_kernel<D, KC, TR>;
     const size_t smem = mega_smem_bytes(D);
     static bool set = false;
     if (!set) {
@@ -1189,6 +1189,14 @@ static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     EKV_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
+}
+
+// the diagnostics (phase stamps, ring counters) are compiled into a separate
+// instantiation, so the production kernel carries none of their code
+template <int D, int KC>
+static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
+    if (a.trace) launch_dkt<D, KC, true>(a, grid, st);
+    else launch_dkt<D, KC, false>(a, grid, st);
 }
 
 template <int D>

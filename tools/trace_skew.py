@@ -1,24 +1,20 @@
-"""Per-CTA skew of the attention phase vs its plan (pieces, user rows)."""
+"""Per-CTA skew of each phase: which CTAs are slow, and how often."""
 import numpy as np, os, sys
 exec(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), 'trace_mega.py')).read().split("t = sess.trace_step(G)")[0])
-t = sess.trace_step(G).astype(np.int64).reshape(L + 1, G, 16)
-ulen = 16 + 3
-UNIT = 16
-cu = S // UNIT; uu = (ulen + 1 + UNIT - 1) // UNIT; per = cu + uu; TU = H * per
-npieces = []; users = []
-for c in range(G):
-    a0, b0 = c * TU // G, (c + 1) * TU // G
-    hs = set(u // per for u in range(a0, b0))
-    npieces.append(len(hs))
-    users.append(sum(1 for u in range(a0, b0) if u % per >= cu))
-npieces = np.array(npieces); users = np.array(users)
-Bt = np.stack([(t[l, :, 4] - t[l, :, 3]) / 1e3 for l in range(L)])  # [L][G]
-At = np.stack([(t[l, :, 2] - t[l, :, 1]) / 1e3 for l in range(L)])
-print("B time by (pieces, user units): mean over layers")
-for np_ in (1, 2):
-    for uu_ in sorted(set(users)):
-        m = (npieces == np_) & (users == uu_)
-        if m.any():
-            print(f"  pieces={np_} user_units={uu_}: n={m.sum():3d}  B mean {Bt[:, m].mean():.2f}  max {Bt[:, m].max():.2f}   A mean {At[:, m].mean():.2f}")
-print("B per-CTA mean (first 40 CTAs):", np.round(Bt.mean(0)[:40], 1))
-print("A per-CTA mean (first 40 CTAs):", np.round(At.mean(0)[:40], 1))
+res = []
+for rep in range(3):
+    t = sess.trace_step(G).astype(np.int64).reshape(L + 1, G, 16)
+    res.append(t)
+names = ["x wait", "A", "qkv wait", "B", "merge", "C", "R"]
+for t in res[-1:]:
+    seg = np.stack([np.diff(t[l, :, :8], axis=1) / 1e3 for l in range(L)])  # [L][G][7]
+    base, extra = G // H, G % H
+    heads_n = np.array([base + 1 if (c < extra * (base + 1)) else base for c in range(G)])
+    for i, n in enumerate(names):
+        v = seg[:, :, i]
+        m4 = v[:, heads_n == base].mean(); m5 = v[:, heads_n == base + 1].mean()
+        p90 = np.percentile(v, 90); mx = v.max()
+        slow = np.argsort(v.mean(0))[-5:][::-1]
+        print(f"{n:9s} mean {v.mean():5.2f}  p90 {p90:5.2f}  max {mx:6.2f}  |  {base}-CTA heads {m4:5.2f}  {base+1}-CTA heads {m5:5.2f} | slowest CTAs {slow.tolist()}")
+    lay = (t[:L, :, 7].max(1) - t[:L, :, 0].min(1)) / 1e3
+    print("layer times:", np.round(lay, 1))
