@@ -693,54 +693,59 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
                                                const float* vs, int ng, int group, int n,
                                                const float* qreg, OState<Fmt<D, FMT>::EPL>& st) {
     using F = Fmt<D, FMT>;
+    constexpr int CP = NPASS < 4 ? NPASS : 4;  // passes per chunk (code size: one chunk body)
     const int lane = threadIdx.x & 31;
     const int sub = lane % F::LPR, rsub = lane / F::LPR;
     const int grp = FMT == 16 ? 0 : (sub * F::EPL) / group;
-    float lg[NPASS];
+#pragma unroll 1
+    for (int p0 = 0; p0 < NPASS && p0 * F::RPP < n; p0 += CP) {
+        float lg[CP];
 #pragma unroll
-    for (int p = 0; p < NPASS; ++p) {
-        const int row = min(p * F::RPP + rsub, n - 1);
-        const uint4 kv = *reinterpret_cast<const uint4*>(kb + row * F::ROW + sub * 16);
-        float f[F::EPL];
-        expand16<FMT>(kv, f);
-        float d0 = 0.0f, d1 = 0.0f;
+        for (int q = 0; q < CP; ++q) {
+            const int row = min((p0 + q) * F::RPP + rsub, n - 1);
+            const uint4 kv = *reinterpret_cast<const uint4*>(kb + row * F::ROW + sub * 16);
+            float f[F::EPL];
+            expand16<FMT>(kv, f);
+            float d0 = 0.0f, d1 = 0.0f;
 #pragma unroll
-        for (int e = 0; e < F::EPL; e += 2) {
-            d0 = fmaf(qreg[e], f[e], d0);
-            d1 = fmaf(qreg[e + 1], f[e + 1], d1);
+            for (int e = 0; e < F::EPL; e += 2) {
+                d0 = fmaf(qreg[e], f[e], d0);
+                d1 = fmaf(qreg[e + 1], f[e + 1], d1);
+            }
+            float dot = d0 + d1;
+            if constexpr (FMT != 16) dot *= ks[row * ng + grp];
+            lg[q] = dot;
         }
-        float dot = d0 + d1;
-        if constexpr (FMT != 16) dot *= ks[row * ng + grp];
-        lg[p] = dot;
-    }
 #pragma unroll
-    for (int o = F::LPR >> 1; o > 0; o >>= 1)
+        for (int o = F::LPR >> 1; o > 0; o >>= 1)
 #pragma unroll
-        for (int p = 0; p < NPASS; ++p) lg[p] += __shfl_xor_sync(0xffffffffu, lg[p], o);
-    float mx = -CUDART_INF_F;
+            for (int q = 0; q < CP; ++q) lg[q] += __shfl_xor_sync(0xffffffffu, lg[q], o);
+        float mx = -CUDART_INF_F;
 #pragma unroll
-    for (int p = 0; p < NPASS; ++p)
-        if (p * F::RPP + rsub < n) mx = fmaxf(mx, lg[p]);
-    if (mx == -CUDART_INF_F) return;  // no rows for this lane group (n < RPP)
-    const float mn = fmaxf(st.m, mx);
-    const float corr = exp2f((st.m - mn) * kLog2e);
-    st.l *= corr;
+        for (int q = 0; q < CP; ++q)
+            if ((p0 + q) * F::RPP + rsub < n) mx = fmaxf(mx, lg[q]);
+        if (mx != -CUDART_INF_F) {  // (no shuffles below: divergence is harmless)
+            const float mn = fmaxf(st.m, mx);
+            const float corr = exp2f((st.m - mn) * kLog2e);
+            st.l *= corr;
 #pragma unroll
-    for (int e = 0; e < F::EPL; ++e) st.o[e] *= corr;
-    st.m = mn;
+            for (int e = 0; e < F::EPL; ++e) st.o[e] *= corr;
+            st.m = mn;
 #pragma unroll
-    for (int p = 0; p < NPASS; ++p) {
-        const int row = min(p * F::RPP + rsub, n - 1);
-        const float pr = p * F::RPP + rsub < n ? exp2f((lg[p] - mn) * kLog2e) : 0.0f;
-        const uint4 vv = *reinterpret_cast<const uint4*>(vb + row * F::ROW + sub * 16);
-        float vsc = 1.0f;
-        if constexpr (FMT != 16) vsc = vs[row * ng + grp];
-        float f[F::EPL];
-        expand16<FMT>(vv, f);
-        st.l += pr;
-        const float pv = pr * vsc;
+            for (int q = 0; q < CP; ++q) {
+                const int row = min((p0 + q) * F::RPP + rsub, n - 1);
+                const float pr = (p0 + q) * F::RPP + rsub < n ? exp2f((lg[q] - mn) * kLog2e) : 0.0f;
+                const uint4 vv = *reinterpret_cast<const uint4*>(vb + row * F::ROW + sub * 16);
+                float vsc = 1.0f;
+                if constexpr (FMT != 16) vsc = vs[row * ng + grp];
+                float f[F::EPL];
+                expand16<FMT>(vv, f);
+                st.l += pr;
+                const float pv = pr * vsc;
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
+                for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
+            }
+        }
     }
 }
 
