@@ -553,6 +553,13 @@ __device__ __forceinline__ int first_owned(const Cursor& cu) {
     return (int)(((threadIdx.x >> 5) - cu.k % NCW + NCW) % NCW);
 }
 
+// x lives in shared memory swizzled for proj_qkv's register load: lane l takes
+// x[c*256 + l*8 .. +8] of every 256-chunk c as two 16-byte loads at lane stride
+// 16 B (conflict-free), i.e. float4 index (c, half, l) -> c*64 + half*32 + l.
+__device__ __forceinline__ int xs_idx4(int i4) {
+    return ((i4 >> 6) << 6) | ((i4 & 1) << 5) | ((i4 & 63) >> 1);
+}
+
 // Layer input into shared memory.  Layer 0: the token input with the input
 // transform (plain loads: written before the launch).  Later layers: the
 // tagged words of R of the previous layer, every load in flight at once.
@@ -570,7 +577,7 @@ __device__ __forceinline__ void stage_x(const MegaArgs& a, Smem<D>& sm, int h, i
             v.y = g.y * (v.y + bf16_hi(p.x)) + b.y;
             v.z = g.z * (v.z + bf16_lo(p.y)) + b.z;
             v.w = g.w * (v.w + bf16_hi(p.y)) + b.w;
-            reinterpret_cast<float4*>(sm.xs)[i] = v;
+            reinterpret_cast<float4*>(sm.xs)[xs_idx4(i)] = v;
         }
     } else {
         constexpr int W = 2048 / (NCW * 32);  // words per thread at the largest h
@@ -583,7 +590,7 @@ __device__ __forceinline__ void stage_x(const MegaArgs& a, Smem<D>& sm, int h, i
 #pragma unroll
         for (int k = 0; k < W; ++k) {
             const int i = k * NCW * 32 + threadIdx.x;
-            if (i < h) sm.xs[i] = ll_spin(a.ll_x + i, w[k], prev_tag);
+            if (i < h) sm.xs[xs_idx4(i >> 2) * 4 + (i & 3)] = ll_spin(a.ll_x + i, w[k], prev_tag);
         }
     }
     consumers_sync();
@@ -600,8 +607,8 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
     float xr[KC * 8];
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
-        const float4 a0 = *reinterpret_cast<const float4*>(sm.xs + c * 256 + lane * 8);
-        const float4 a1 = *reinterpret_cast<const float4*>(sm.xs + c * 256 + lane * 8 + 4);
+        const float4 a0 = reinterpret_cast<const float4*>(sm.xs)[c * 64 + lane];
+        const float4 a1 = reinterpret_cast<const float4*>(sm.xs)[c * 64 + 32 + lane];
         xr[c * 8 + 0] = a0.x; xr[c * 8 + 1] = a0.y; xr[c * 8 + 2] = a0.z; xr[c * 8 + 3] = a0.w;
         xr[c * 8 + 4] = a1.x; xr[c * 8 + 5] = a1.y; xr[c * 8 + 6] = a1.z; xr[c * 8 + 7] = a1.w;
     }
