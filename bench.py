@@ -353,13 +353,22 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     b_user = L * 2 * H * n_user_avg * d * 2
     step_bytes = L * (b_qkv + b_out) + (L - DEEP) * b_att_local + DEEP * b_att_deep + b_user
     step_s = ms / K * 1e-3
+    # DRAM traffic per launch from the committed ncu --set full capture (tools/ncu_traffic.py)
+    ncu_bytes = {}
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                               "ncu_dram_bytes.json")) as f:
+            ncu_bytes = {k: v["dram_bytes_per_launch"] for k, v in json.load(f).items()}
+    except (OSError, ValueError, KeyError):
+        pass
     if path == "mega":
         per_launch = float(np.mean([p[0] for p in prof]))  # ms, one kernel = one step
         achieved = step_bytes / (per_launch * 1e-3) / 1e9
         roofline = {
             "bound": "hbm", "kernel": "decode_step_kernel (persistent, 1 launch per token)",
             "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": step_bytes,
+            "traffic": ncu_bytes.get("decode_step_kernel"), "peak_kind": peak_kind,
+            "bytes_per_launch": step_bytes,
             "avg_launch_us": per_launch * 1e3, "share_of_step": 1.0,
             "how": f"CUDA events around {prof_steps} single launches on the launching stream; "
                    "bytes = weights + context KV + attended user rows of one token",
