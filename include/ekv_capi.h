@@ -126,6 +126,14 @@ int ekv_rank_channels(const double* q_colsq, const double* k_colsq, int d_c, int
 int ekv_match_layers(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc,
                      int cc, int n, double theta_cka, double theta_rsa, double* cka, double* rsa,
                      int* best);
+/* K7: the same layer map on the device.  edge_outs / cloud_outs are DEVICE
+ * buffers (the probe-prefill outputs, fp64); cka / rsa / best are host arrays.
+ * Bit-identical to match_layers (layer_match.cpp:166-228): fp64 in the
+ * reference's operation order.  Same errors and messages.  n <= 256.
+ * Synchronises the context's stream. */
+int ekv_match_layers_dev(ekv_ctx_t c, const double* edge_outs, int me, int ce,
+                         const double* cloud_outs, int nc, int cc, int n, double theta_cka,
+                         double theta_rsa, double* cka, double* rsa, int* best);
 
 /* ------------------------------------------------------------------ */
 /* Stage 2: representation compression (gather + quantise + pack)     */

@@ -57,6 +57,7 @@ PROTOS = {
     "ekv_kv_colnorm": [_vp, _vp, _i64, _i, _vp],
     "ekv_rank_channels": [_dp, _dp, _i, _i, _ip, _dp],
     "ekv_match_layers": [_dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
+    "ekv_match_layers_dev": [_vp, _vp, _i, _i, _vp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
     "ekv_kv_gather": [_vp, _vp, _i64, _i, _vp, _i, _vp],
     "ekv_gather_columns": [_vp, _vp, _i64, _i, _vp, _i, _i, _vp],
     "ekv_kv_compress": [_vp, _vp, _i64, _i, _vp, _i, _i, _i, _vp, _vp],

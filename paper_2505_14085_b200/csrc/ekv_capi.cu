@@ -654,6 +654,69 @@ std::vector<double> normalized(const double* o, int n, int c) {
 }
 }  // namespace
 
+int ekv_match_layers_dev(ekv_ctx_t c, const double* edge_outs, int me, int ce, const double* cloud_outs,
+                         int nc, int cc, int n, double theta_cka, double theta_rsa, double* cka_out,
+                         double* rsa_out, int* best) {
+    return guard([&] {
+        require(c && edge_outs && cloud_outs && cka_out && rsa_out && best, "null argument");
+        require(me >= 1 && nc >= 1, "match_layers: empty layer output list");
+        require(theta_cka >= 0.0, "SimilarityConfig: theta_cka must be >= 0");
+        require(theta_rsa >= -1.0, "SimilarityConfig: theta_rsa must be >= -1");
+        require(n >= 3, "rsa: need N >= 3 samples");
+        require(n <= 256, "match_layers_dev: at most 256 probe rows", EKV_EUNSUPPORTED);
+        require(ce >= 1 && cc >= 1, "match_layers: bad layer width");
+        set_dev(c);
+        const int L = me + nc;
+        const size_t m = (size_t)n * (n - 1) / 2, P = (size_t)me * nc;
+        // one work allocation: doubles then ints
+        const size_t nd = L + 2 * (size_t)L * n * n + L + (size_t)L * m + 2 * P;
+        const size_t ni = L + P;
+        char* w = nullptr;
+        EKV_CUDA(cudaMallocAsync((void**)&w, nd * sizeof(double) + ni * sizeof(int), c->stream));
+        double* d = (double*)w;
+        double* scale = d;
+        double* gram = scale + L;
+        double* centred = gram + (size_t)L * n * n;
+        double* self_h = centred + (size_t)L * n * n;
+        double* cosflat = self_h + L;
+        double* hsic = cosflat + (size_t)L * m;
+        double* corr = hsic + P;
+        int* zero_row = (int*)(corr + P);
+        int* zero_var = zero_row + L;
+        launch_layer_match(edge_outs, me, ce, cloud_outs, nc, cc, n, scale, gram, centred, self_h, cosflat,
+                           zero_row, hsic, corr, zero_var, c->stream);
+        std::vector<double> hself(L), hh(P), hc(P);
+        std::vector<int> hz(L), hv(P);
+        EKV_CUDA(cudaMemcpyAsync(hself.data(), self_h, sizeof(double) * L, cudaMemcpyDeviceToHost, c->stream));
+        EKV_CUDA(cudaMemcpyAsync(hh.data(), hsic, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
+        EKV_CUDA(cudaMemcpyAsync(hc.data(), corr, sizeof(double) * P, cudaMemcpyDeviceToHost, c->stream));
+        EKV_CUDA(cudaMemcpyAsync(hz.data(), zero_row, sizeof(int) * L, cudaMemcpyDeviceToHost, c->stream));
+        EKV_CUDA(cudaMemcpyAsync(hv.data(), zero_var, sizeof(int) * P, cudaMemcpyDeviceToHost, c->stream));
+        EKV_CUDA(cudaFreeAsync(w, c->stream));
+        EKV_CUDA(cudaStreamSynchronize(c->stream));
+        // the reference's argmax and its error order (cka, then rsa, per (le, lc))
+        for (int le = 0; le < me; ++le) {
+            int bl = -1;
+            double bc = 0.0;
+            for (int lc = 0; lc < nc; ++lc) {
+                const size_t p = (size_t)le * nc + lc;
+                require(hself[le] >= 1e-15 && hself[me + lc] >= 1e-15, "cka: degenerate representation");
+                require(hz[le] < 0, "rsa: zero-norm row " + std::to_string(hz[le]));
+                require(hz[me + lc] < 0, "rsa: zero-norm row " + std::to_string(hz[me + lc]));
+                require(!hv[p], "pearson_corr: zero variance");
+                const double ck = hh[p] / std::sqrt(hself[le] * hself[me + lc]);
+                cka_out[p] = ck;
+                rsa_out[p] = hc[p];
+                if (ck >= theta_cka && hc[p] >= theta_rsa && (bl < 0 || ck > bc)) {
+                    bl = lc;
+                    bc = ck;
+                }
+            }
+            best[le] = bl;
+        }
+    });
+}
+
 int ekv_match_layers(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc,
                      int cc, int n, double theta_cka, double theta_rsa, double* cka_out,
                      double* rsa_out, int* best) {

@@ -36,6 +36,10 @@ void launch_gather_columns(const void* src, int64_t rows, int d_c, const int* ke
 void launch_kv_dequant(const void* codes, const float* scales, int64_t rows, int d_e, int bits,
                        int group, void* dst, cudaStream_t st);
 void launch_kv_colnorm(const void* K, int64_t rows, int d_c, double* colsq, cudaStream_t st);
+void launch_layer_match(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc, int cc,
+                        int n, double* scale, double* gram, double* centred, double* self_hsic,
+                        double* cosflat, int* zero_row, double* hsic, double* corr, int* zero_var,
+                        cudaStream_t st);
 
 // ---- K4 decode attention -------------------------------------------------
 struct AttnArgs {

@@ -881,7 +881,10 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
     // partials: warp 0 computes the 2*2*NCW rescale factors and the totals
     // (one lane per state), then every column is an independent 2*NCW-term sum.
     static_assert(2 * NCW <= 32, "one lane per (kind, warp) state");
+#pragma unroll 1
+    for (int rep = TR ? 0 : 1; rep < 2; ++rep)  // EXPERIMENT: trace build runs it twice
     if (warp == 0) {
+        if (TR && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + 12 + rep] = clock64();
         for (int i = 0; i < pl.n; ++i) {
             const int k = lane / NCW, w = lane % NCW;
             const bool on = lane < 2 * NCW && sm.ws_l[i][k][w] > 0.0f;
@@ -897,6 +900,7 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             }
         }
     }
+    if (TR && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + 14] = clock64();
     consumers_sync();
     for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
         const int i = t / D, cix = t - i * D;

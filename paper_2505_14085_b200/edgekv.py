@@ -24,7 +24,7 @@ from .capi import EKV_KV_BF16, EKV_KV_INT4, EKV_KV_INT8, EkvError, call, ekv_mod
 __all__ = [
     "Context", "EkvError", "prune_retained", "align_qnorm", "kv_colnorm", "rank_channels",
     "select_channels", "prune_cache", "kv_compress", "kv_dequant", "decode_attention",
-    "match_layers", "cache_source", "pipeline_schedule", "EdgeModel", "AssembledContext",
+    "match_layers", "match_layers_dev", "cache_source", "pipeline_schedule", "EdgeModel", "AssembledContext",
     "Session", "collaborative_decode", "build_deep_kv", "EKV_KV_BF16", "EKV_KV_INT8",
     "EKV_KV_INT4",
 ]
@@ -223,6 +223,21 @@ def match_layers(edge_outs: np.ndarray, cloud_outs: np.ndarray, theta_cka: float
     cka = np.zeros((me, nc)); rsa = np.zeros((me, nc)); best = np.zeros(me, dtype=np.int32)
     call("ekv_match_layers", _dp(e), me, ce, _dp(c), nc, cc, n, theta_cka, theta_rsa, _dp(cka),
          _dp(rsa), _ip(best))
+    return cka, rsa, best
+
+
+def match_layers_dev(ctx: "Context", edge_outs: torch.Tensor, cloud_outs: torch.Tensor,
+                     theta_cka: float, theta_rsa: float):
+    """K7: match_layers on the device over fp64 probe outputs already in HBM
+    ([me][n][ce], [nc][n][cc]); bit-identical to the reference.  Returns numpy
+    (cka, rsa, best)."""
+    assert edge_outs.dtype == torch.float64 and cloud_outs.dtype == torch.float64
+    e, c = edge_outs.contiguous(), cloud_outs.contiguous()
+    me, n, ce = e.shape
+    nc, _, cc = c.shape
+    cka = np.zeros((me, nc)); rsa = np.zeros((me, nc)); best = np.zeros(me, dtype=np.int32)
+    call("ekv_match_layers_dev", ctx.h, _ptr(e), me, ce, _ptr(c), nc, cc, n, theta_cka, theta_rsa,
+         _dp(cka), _dp(rsa), _ip(best))
     return cka, rsa, best
 
 
