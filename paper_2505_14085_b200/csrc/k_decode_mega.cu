@@ -338,7 +338,6 @@ struct Smem {
     float os[2][D];               // merged attention output of this CTA's W_o heads
     float ws_o[2][2][NCW][D];     // per (piece, context/user, warp) partial output
     float ws_m[2][2][NCW], ws_l[2][2][NCW];
-    float fsc[2][2 * NCW];        // fold: rescale factor of each (kind, warp) state
     AttnPlan pl;                  // this CTA's attention pieces (shared: indexed at run time,
     OPlan op;                     // a per-thread copy would live in local memory)
     int hfirst[160], hlast[160];  // contributing CTA range of each head's attention
@@ -878,39 +877,32 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
     }
     consumers_sync();
     // CTA-level fold of every (piece, kind, warp) state -> this CTA's tagged
-    // partials: warp 0 computes the 2*2*NCW rescale factors and the totals
-    // (one lane per state), then every column is an independent 2*NCW-term sum.
+    // partials.  Each warp that owns 32 output columns (of one piece: 32 | D)
+    // computes the 2*NCW rescale factors itself (one lane per state, shuffled to
+    // every lane) -- no second block barrier, no serial warp-0 step.
     static_assert(2 * NCW <= 32, "one lane per (kind, warp) state");
-#pragma unroll 1
-    for (int rep = TR ? 0 : 1; rep < 2; ++rep)  // EXPERIMENT: trace build runs it twice
-    if (warp == 0) {
-        if (TR && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + 12 + rep] = clock64();
-        for (int i = 0; i < pl.n; ++i) {
-            const int k = lane / NCW, w = lane % NCW;
-            const bool on = lane < 2 * NCW && sm.ws_l[i][k][w] > 0.0f;
-            const float m = on ? sm.ws_m[i][k][w] : -CUDART_INF_F;
-            const float M = warp_max(m);
-            const float sc = on ? exp2f((m - M) * kLog2e) : 0.0f;
+    for (int t0 = warp * 32; t0 < pl.n * D; t0 += NCW * 32) {
+        const int i = t0 / D, cix = t0 - i * D + lane;
+        const int k = lane / NCW, w = lane % NCW;
+        const bool on = lane < 2 * NCW && sm.ws_l[i][k][w] > 0.0f;
+        const float m = on ? sm.ws_m[i][k][w] : -CUDART_INF_F;
+        const float M = warp_max(m);
+        const float sc = on ? exp2f((m - M) * kLog2e) : 0.0f;
+        uint64_t* outp = a.ll_part + ((size_t)c * 2 + i) * (D + 2);
+        if (t0 == i * D) {  // the first warp of the piece publishes (m, l)
             const float Ls = warp_sum(on ? sm.ws_l[i][k][w] * sc : 0.0f);
-            if (lane < 2 * NCW) sm.fsc[i][lane] = sc;
             if (lane == 0) {
-                uint64_t* outp = a.ll_part + ((size_t)c * 2 + i) * (D + 2);
                 ll_st(outp, M, tag);
                 ll_st(outp + 1, Ls, tag);
             }
         }
-    }
-    if (TR && threadIdx.x == 0) a.trace[((size_t)l * gridDim.x + blockIdx.x) * 16 + 14] = clock64();
-    consumers_sync();
-    for (int t = threadIdx.x; t < pl.n * D; t += NCW * 32) {
-        const int i = t / D, cix = t - i * D;
         float o0 = 0.0f, o1 = 0.0f;
 #pragma unroll
-        for (int w = 0; w < NCW; ++w) {
-            o0 = fmaf(sm.ws_o[i][0][w][cix], sm.fsc[i][w], o0);
-            o1 = fmaf(sm.ws_o[i][1][w][cix], sm.fsc[i][NCW + w], o1);
+        for (int ww = 0; ww < NCW; ++ww) {
+            o0 = fmaf(sm.ws_o[i][0][ww][cix], __shfl_sync(0xffffffffu, sc, ww), o0);
+            o1 = fmaf(sm.ws_o[i][1][ww][cix], __shfl_sync(0xffffffffu, sc, NCW + ww), o1);
         }
-        ll_st(a.ll_part + ((size_t)c * 2 + i) * (D + 2) + 2 + cix, o0 + o1, tag);
+        ll_st(outp + 2 + cix, o0 + o1, tag);
     }
     // (the next consumers_sync is in the caller, before shared state is reused)
 }
