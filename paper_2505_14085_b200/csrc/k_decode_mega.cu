@@ -115,6 +115,44 @@ __device__ __forceinline__ void prefetch_tile_l2(const CUtensorMap* map, int c0,
                  "r"(c1)
                  : "memory");
 }
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2): two lanes of fp32
+// math per instruction, exactly the IEEE result of each lane.
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x f2pack(float lo, float hi) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float f2lo(f2x v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ float f2hi(f2x v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// a bf16 pair word -> {low element, high element} as fp32
+__device__ __forceinline__ f2x bf16x2_to_f2(uint32_t w) {
+    return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
 __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NCW * 32) : "memory");
 }
@@ -603,13 +641,13 @@ template <int D, int KC, bool TR>
 __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm, Cursor& cu,
                                          Split rows, int h, int ulen, uint32_t tag) {
     const int lane = threadIdx.x & 31;
-    float xr[KC * 8];
+    f2x xr[KC * 4];  // x pairs {x[2k], x[2k+1]} of this lane's 8 elements per chunk
 #pragma unroll
     for (int c = 0; c < KC; ++c) {
         const float4 a0 = reinterpret_cast<const float4*>(sm.xs)[c * 64 + lane];
         const float4 a1 = reinterpret_cast<const float4*>(sm.xs)[c * 64 + 32 + lane];
-        xr[c * 8 + 0] = a0.x; xr[c * 8 + 1] = a0.y; xr[c * 8 + 2] = a0.z; xr[c * 8 + 3] = a0.w;
-        xr[c * 8 + 4] = a1.x; xr[c * 8 + 5] = a1.y; xr[c * 8 + 6] = a1.z; xr[c * 8 + 7] = a1.w;
+        xr[c * 4 + 0] = f2pack(a0.x, a0.y); xr[c * 4 + 1] = f2pack(a0.z, a0.w);
+        xr[c * 4 + 2] = f2pack(a1.x, a1.y); xr[c * 4 + 3] = f2pack(a1.z, a1.w);
     }
     constexpr int RG = 3;  // rows in flight per warp (independent FMA and shuffle chains)
     const int rows_per_w = STAGE / (h * 2);
@@ -622,9 +660,9 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
             const uint8_t* wr[RG];
 #pragma unroll
             for (int g = 0; g < RG; ++g) wr[g] = st + (size_t)min(i0 + g, n - 1) * h * 2 + lane * 16;
-            float acc[RG][2];
+            f2x acc[RG];  // {even, odd} partial sums
 #pragma unroll
-            for (int g = 0; g < RG; ++g) acc[g][0] = acc[g][1] = 0.0f;
+            for (int g = 0; g < RG; ++g) acc[g] = 0ull;
             // software pipeline: chunk c+1 of every row is loaded before chunk c
             // is consumed (volatile loads keep their order)
             uint4 cur[RG], nxt[RG];
@@ -640,10 +678,7 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
                 for (int g = 0; g < RG; ++g) {
                     const uint32_t ww[4] = {cur[g].x, cur[g].y, cur[g].z, cur[g].w};
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        acc[g][0] = fmaf(bf16_lo(ww[k]), xr[c * 8 + 2 * k], acc[g][0]);
-                        acc[g][1] = fmaf(bf16_hi(ww[k]), xr[c * 8 + 2 * k + 1], acc[g][1]);
-                    }
+                    for (int k = 0; k < 4; ++k) acc[g] = ffma2(bf16x2_to_f2(ww[k]), xr[c * 4 + k], acc[g]);
                 }
                 if (c + 1 < KC) {
 #pragma unroll
@@ -652,7 +687,7 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
             }
             float y[RG];
 #pragma unroll
-            for (int g = 0; g < RG; ++g) y[g] = acc[g][0] + acc[g][1];
+            for (int g = 0; g < RG; ++g) y[g] = f2lo(acc[g]) + f2hi(acc[g]);
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
