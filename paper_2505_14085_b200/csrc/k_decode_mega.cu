@@ -337,10 +337,42 @@ __device__ __forceinline__ void expand16(const uint4& v, float* f) {
     }
 }
 
+// the same 16 bytes as EPL/2 packed fp32 pairs (consecutive elements)
+template <int FMT>
+__device__ __forceinline__ void expand16_2(const uint4& v, f2x* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if constexpr (FMT == 16) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) f[k] = bf16x2_to_f2(w[k]);
+    } else if constexpr (FMT == 8) {
+        const f2x bias = f2pack(-8388736.0f, -8388736.0f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t u = w[k] ^ 0x80808080u;
+            f[2 * k] = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7440)),
+                                    __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7441))), bias);
+            f[2 * k + 1] = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7442)),
+                                        __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7443))), bias);
+        }
+    } else {
+        const f2x bias = f2pack(-8388616.0f, -8388616.0f);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t lo = (w[k] & 0x0F0F0F0Fu) ^ 0x08080808u;
+            const uint32_t hi = ((w[k] >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                f[4 * k + b] = fadd2(f2pack(__uint_as_float(__byte_perm(lo, 0x4B000000u, 0x7440 + b)),
+                                            __uint_as_float(__byte_perm(hi, 0x4B000000u, 0x7440 + b))), bias);
+        }
+    }
+}
+
 // Online-softmax state of one lane group (the LPR lanes of one row subgroup).
 template <int EPL>
 struct OState {
-    float m, l, o[EPL];
+    float m, l;
+    f2x o[EPL / 2];  // output columns as packed pairs
 };
 
 template <int EPL>
@@ -348,17 +380,18 @@ __device__ __forceinline__ void ostate_init(OState<EPL>& s) {
     s.m = -CUDART_INF_F;
     s.l = 0.0f;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) s.o[e] = 0.0f;
+    for (int e = 0; e < EPL / 2; ++e) s.o[e] = 0ull;
 }
 
 template <int EPL>
-__device__ __forceinline__ void ostate_merge_from(OState<EPL>& s, float m2, float l2, const float* o2) {
+__device__ __forceinline__ void ostate_merge_from(OState<EPL>& s, float m2, float l2, const f2x* o2) {
     const float mn = fmaxf(s.m, m2);
     if (mn == -CUDART_INF_F) return;
     const float a = exp2f((s.m - mn) * kLog2e), b = exp2f((m2 - mn) * kLog2e);
     s.l = s.l * a + l2 * b;
+    const f2x a2 = f2pack(a, a), b2 = f2pack(b, b);
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) s.o[e] = s.o[e] * a + o2[e] * b;
+    for (int e = 0; e < EPL / 2; ++e) s.o[e] = ffma2(s.o[e], a2, fmul2(o2[e], b2));
     s.m = mn;
 }
 
@@ -732,7 +765,7 @@ __host__ __device__ constexpr int att_passes() {
 template <int D, int FMT, int NPASS>
 __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t* vb, const float* ks,
                                                const float* vs, int ng, int group, int n,
-                                               const float* qreg, OState<Fmt<D, FMT>::EPL>& st) {
+                                               const f2x* qreg, OState<Fmt<D, FMT>::EPL>& st) {
     using F = Fmt<D, FMT>;
     constexpr int CP = NPASS < 4 ? NPASS : 4;  // passes per chunk (code size: one chunk body)
     const int lane = threadIdx.x & 31;
@@ -745,15 +778,12 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
         for (int q = 0; q < CP; ++q) {
             const int row = min((p0 + q) * F::RPP + rsub, n - 1);
             const uint4 kv = *reinterpret_cast<const uint4*>(kb + row * F::ROW + sub * 16);
-            float f[F::EPL];
-            expand16<FMT>(kv, f);
-            float d0 = 0.0f, d1 = 0.0f;
+            f2x f[F::EPL / 2];
+            expand16_2<FMT>(kv, f);
+            f2x d2 = 0ull;
 #pragma unroll
-            for (int e = 0; e < F::EPL; e += 2) {
-                d0 = fmaf(qreg[e], f[e], d0);
-                d1 = fmaf(qreg[e + 1], f[e + 1], d1);
-            }
-            float dot = d0 + d1;
+            for (int e = 0; e < F::EPL / 2; ++e) d2 = ffma2(qreg[e], f[e], d2);
+            float dot = f2lo(d2) + f2hi(d2);
             if constexpr (FMT != 16) dot *= ks[row * ng + grp];
             lg[q] = dot;
         }
@@ -769,8 +799,9 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
             const float mn = fmaxf(st.m, mx);
             const float corr = exp2f((st.m - mn) * kLog2e);
             st.l *= corr;
+            const f2x corr2 = f2pack(corr, corr);
 #pragma unroll
-            for (int e = 0; e < F::EPL; ++e) st.o[e] *= corr;
+            for (int e = 0; e < F::EPL / 2; ++e) st.o[e] = fmul2(st.o[e], corr2);
             st.m = mn;
 #pragma unroll
             for (int q = 0; q < CP; ++q) {
@@ -779,12 +810,13 @@ __device__ __forceinline__ void attend_rows_mk(const uint8_t* kb, const uint8_t*
                 const uint4 vv = *reinterpret_cast<const uint4*>(vb + row * F::ROW + sub * 16);
                 float vsc = 1.0f;
                 if constexpr (FMT != 16) vsc = vs[row * ng + grp];
-                float f[F::EPL];
-                expand16<FMT>(vv, f);
+                f2x f[F::EPL / 2];
+                expand16_2<FMT>(vv, f);
                 st.l += pr;
                 const float pv = pr * vsc;
+                const f2x pv2 = f2pack(pv, pv);
 #pragma unroll
-                for (int e = 0; e < F::EPL; ++e) st.o[e] = fmaf(pv, f[e], st.o[e]);
+                for (int e = 0; e < F::EPL / 2; ++e) st.o[e] = ffma2(pv2, f[e], st.o[e]);
             }
         }
     }
@@ -804,16 +836,21 @@ __device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>:
     }
 #pragma unroll
     for (int off = F::LPR; off < 32; off <<= 1) {
-        float o2[F::EPL];
+        f2x o2[F::EPL / 2];
         const float m2 = __shfl_xor_sync(0xffffffffu, st.m, off);
         const float l2 = __shfl_xor_sync(0xffffffffu, st.l, off);
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) o2[e] = __shfl_xor_sync(0xffffffffu, st.o[e], off);
+        for (int e = 0; e < F::EPL / 2; ++e)
+            o2[e] = f2pack(__shfl_xor_sync(0xffffffffu, f2lo(st.o[e]), off),
+                           __shfl_xor_sync(0xffffffffu, f2hi(st.o[e]), off));
         ostate_merge_from<F::EPL>(st, m2, l2, o2);
     }
     if (lane < F::LPR) {
 #pragma unroll
-        for (int e = 0; e < F::EPL; ++e) sm.ws_o[piece][kind][warp][sub * F::EPL + e] = st.o[e];
+        for (int e = 0; e < F::EPL / 2; ++e) {
+            sm.ws_o[piece][kind][warp][sub * F::EPL + 2 * e] = f2lo(st.o[e]);
+            sm.ws_o[piece][kind][warp][sub * F::EPL + 2 * e + 1] = f2hi(st.o[e]);
+        }
     }
     if (lane == 0) {
         sm.ws_m[piece][kind][warp] = st.m;
@@ -861,10 +898,11 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
         {   // context rows (ring)
-            float qreg[F::EPL];
+            f2x qreg[F::EPL / 2];
             const int sub = lane % F::LPR;
 #pragma unroll
-            for (int e = 0; e < F::EPL; ++e) qreg[e] = sm.qs[i][sub * F::EPL + e];
+            for (int e = 0; e < F::EPL / 2; ++e)
+                qreg[e] = f2pack(sm.qs[i][sub * F::EPL + 2 * e], sm.qs[i][sub * F::EPL + 2 * e + 1]);
             OState<F::EPL> st;
             ostate_init<F::EPL>(st);
             const int nst = (pc.c1 - pc.c0 + cap - 1) / cap;
@@ -888,10 +926,11 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
             } else {
                 ostate_init<FU::EPL>(su);
             }
-            float qu[FU::EPL];
+            f2x qu[FU::EPL / 2];
             const int subu = lane % FU::LPR;
 #pragma unroll
-            for (int e = 0; e < FU::EPL; ++e) qu[e] = sm.qs[i][subu * FU::EPL + e];
+            for (int e = 0; e < FU::EPL / 2; ++e)
+                qu[e] = f2pack(sm.qs[i][subu * FU::EPL + 2 * e], sm.qs[i][subu * FU::EPL + 2 * e + 1]);
             const int ue = user_static_end(pc, ulen);
             const int nsu = ue > pc.u0 ? (ue - pc.u0 + ucap - 1) / ucap : 0;
             for (int j = first_owned(cu); j < nsu; j += NCW) {
