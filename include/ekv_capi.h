@@ -57,6 +57,7 @@ typedef struct ekv_ctx_s* ekv_ctx_t;         /* device, stream, workspace       
 typedef struct ekv_model_s* ekv_model_t;     /* edge model weights (Model)          */
 typedef struct ekv_kvctx_s* ekv_kvctx_t;     /* assembled context (AssembledContext)*/
 typedef struct ekv_session_s* ekv_session_t; /* user cache + decode state          */
+typedef struct ekv_batch_s* ekv_batch_t;     /* B sessions over one shared context */
 
 /* ------------------------------------------------------------------ */
 /* Context, errors, utilities                                          */
@@ -299,6 +300,35 @@ int ekv_session_user_kv(ekv_session_t s, int layer, void** k_dev, void** v_dev, 
  * "align with head pruning" (context dims differ from the model). */
 int ekv_collaborative_decode(ekv_session_t s, const float* user_emb_host, int U, int steps,
                              float* prefill_out_host, float* step_out_host);
+
+/* ------------------------------------------------------------------ */
+/* Batched sessions (BASELINE configs[2], concurrent edge sessions)     */
+/* ------------------------------------------------------------------ */
+/* B independent sessions that share one assembled context (the paper's
+ * shared system prompt; one read-only context cache, many
+ * user caches: cache_merge.cpp:252) and advance in lock-step
+ * (all sessions have the same number of user rows).  Per session the
+ * result is collaborative_decode (cache_merge.cpp:230-273); the weights and
+ * the context are streamed once per step for all B sessions (tensor-core
+ * projections and a cascade context attention, k_batch.cu).
+ * max_rows bounds user + generated rows per session.  Supported: hidden
+ * size a multiple of 128; context layers bf16 with head_dim 64. */
+int ekv_batch_create(ekv_model_t m, ekv_kvctx_t c, int sessions, int max_rows, ekv_batch_t* out);
+int ekv_batch_destroy(ekv_batch_t b);
+int ekv_batch_reset(ekv_batch_t b);
+/* sessions, rows forwarded so far, and the work splits {QKV split-K,
+ * out-proj split-K, context splits per head} (any pointer may be NULL) */
+int ekv_batch_info(ekv_batch_t b, int* sessions, int* rows, int* splits);
+/* merged_forward of n user rows of every session: emb_dev fp32 [B][n][h];
+ * out_dev (may be NULL) receives fp32 [n][B][h]. */
+int ekv_batch_forward(ekv_batch_t b, const float* emb_dev, int n, float* out_dev);
+/* `steps` decode steps of every session; out_dev (may be NULL) fp32 [steps][B][h]. */
+int ekv_batch_decode(ekv_batch_t b, int steps, float* out_dev);
+/* collaborative_decode of all B sessions with HOST buffers, synchronous:
+ * user_emb fp32 [B][U][h]; prefill_out [U][B][h] (may be NULL);
+ * step_out [steps][B][h].  Same errors as ekv_collaborative_decode. */
+int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb_host, int U, int steps,
+                                   float* prefill_out_host, float* step_out_host);
 
 /* ------------------------------------------------------------------ */
 /* Scheduler interface (cost_model.hpp:53-84)                          */

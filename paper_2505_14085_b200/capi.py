@@ -88,6 +88,13 @@ PROTOS = {
     "ekv_session_trace_step": [_vp, C.POINTER(C.c_uint64), _i, _ip],
     "ekv_session_profile_step": [_vp, _fp, _i, _ip],
     "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
+    "ekv_batch_create": [_vp, _vp, _i, _i, _pp],
+    "ekv_batch_destroy": [_vp],
+    "ekv_batch_reset": [_vp],
+    "ekv_batch_info": [_vp, _ip, _ip, _ip],
+    "ekv_batch_forward": [_vp, _vp, _i, _vp],
+    "ekv_batch_decode": [_vp, _i, _vp],
+    "ekv_collaborative_decode_batch": [_vp, _vp, _i, _i, _vp, _vp],
     "ekv_collaborative_decode": [_vp, _vp, _i, _i, _vp, _vp],
     "ekv_cache_source": [_i, _d, _d, _i, _i, _ip],
     "ekv_pipeline_schedule": [_dp, _dp, _i, _dp, _dp, _dp],

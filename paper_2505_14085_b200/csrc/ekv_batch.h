@@ -1,0 +1,58 @@
+// Launch interface of the batched-session decode kernels (k_batch.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ekv_kernels.h"
+
+namespace ekv {
+
+struct BatchXprep {
+    int mode;              // 0: layer-0 input transform of xin; 1: sum partials; 2: final output
+    int B, h, KS;
+    const float* part;     // [KS][B][h] split-K partials of the output projection
+    float* xin;            // [B][h] step input (mode 0 reads, mode 2 writes)
+    float* hist;           // [rows][B][h] output rows (mode 2), row = state->step
+    const float* gamma;
+    const float* bias;
+    const uint16_t* pos;   // [max_pos][h]
+    int pos_offset;        // S: position of user row u is S + u
+    const DevState* state;
+    uint16_t* xhl;         // [2][B][h] bf16 hi, lo (projection operand)
+};
+
+struct BatchCtxAttn {
+    int B, H, D, S, nsplit, KS, n_qkv;
+    const float* qkv;      // [KS][B][n_qkv] partials of the QKV projection (q at column 0)
+    float* part;           // [B][H][nsplit][D + 2]  (m, l, o[D]) unnormalised
+};
+
+struct BatchUserMerge {
+    int B, H, D, L, layer, cap, KS, n_qkv, nsplit;
+    const float* qkv;      // [KS][B][3h]
+    const float* part;     // context partials (nsplit may be 0)
+    uint16_t* uk;          // [B][L][H][cap][D]
+    uint16_t* uv;
+    const DevState* state;
+    uint16_t* xhl;         // [2][B][h] attention output hi, lo
+};
+
+CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t inner,
+                        uint64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
+CUtensorMap make_map_3d_bf16(const void* base, uint64_t inner, uint64_t rows, uint64_t depth,
+                             uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
+
+int batch_proj_bn(int B);
+int batch_proj_splits(int N_out, int K, int B, int num_sms);
+void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, const CUtensorMap& map_x,
+                       int B, int KS, float* out, cudaStream_t st);
+void launch_batch_xprep(const BatchXprep& a, cudaStream_t st);
+int batch_ctx_splits(int S, int H, int B, int num_sms);
+bool batch_ctx_supported(int D, int fmt);
+void launch_batch_ctx_attn(const CUtensorMap& map_k, const CUtensorMap& map_v, const BatchCtxAttn& a,
+                           cudaStream_t st);
+void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st);
+
+}  // namespace ekv

@@ -13,6 +13,7 @@
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
 #include "ekv_mega.h"
+#include "ekv_batch.h"
 
 namespace ekv {
 
@@ -412,6 +413,206 @@ void ctx_storage(ekv_kvctx_s* c) {
             s.v_scales = vs;
         }
     }
+}
+
+}  // namespace
+
+// ===========================================================================
+// Batched sessions (k_batch.cu): B sessions over one shared context, one
+// forward row of every session per replay of one captured CUDA graph.
+// ===========================================================================
+struct ekv_batch_s {
+    ekv_model_s* model = nullptr;
+    ekv_kvctx_s* kv = nullptr;
+    int B = 0, cap = 0;
+    int KSq = 1, KSo = 1, nsplit = 0;
+    uint16_t* uk = nullptr;   // [B][L][H][cap][D]
+    uint16_t* uv = nullptr;
+    float* xin = nullptr;     // [B][h] step input / last output
+    float* hist = nullptr;    // [cap][B][h] output rows
+    float* emb = nullptr;     // [B][cap][h] staged user embeddings
+    uint16_t* xhl = nullptr;  // [2][B][h]
+    float* qkv = nullptr;     // [KSq][B][3h]
+    float* xpart = nullptr;   // [KSo][B][h]
+    float* part = nullptr;    // [B][H][nsplit][D+2]
+    DevState* state = nullptr;
+    CUtensorMap map_w{}, map_x{};
+    std::vector<CUtensorMap> map_k, map_v;
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_kernels = 0;
+    int user_len = 0, rows = 0;
+};
+
+namespace {
+
+void batch_row(ekv_batch_s* b, cudaStream_t st) {
+    ekv_model_s* m = b->model;
+    const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = d_of(m), h = m->h, B = b->B;
+    BatchXprep x0{};
+    x0.mode = 0;
+    x0.B = B;
+    x0.h = h;
+    x0.xin = b->xin;
+    x0.gamma = m->gamma;
+    x0.bias = m->bias;
+    x0.pos = m->pos;
+    x0.pos_offset = b->kv->S;
+    x0.state = b->state;
+    x0.xhl = b->xhl;
+    launch_batch_xprep(x0, st);
+    for (int l = 0; l < L; ++l) {
+        launch_batch_proj(b->map_w, l * 4 * h, 3 * h, h, b->map_x, B, b->KSq, b->qkv, st);
+        const ekv_segment& sg = b->kv->seg[l];
+        const int ns = sg.S > 0 ? b->nsplit : 0;
+        if (ns > 0) {
+            BatchCtxAttn a{};
+            a.B = B;
+            a.H = H;
+            a.D = D;
+            a.S = sg.S;
+            a.nsplit = ns;
+            a.KS = b->KSq;
+            a.n_qkv = 3 * h;
+            a.qkv = b->qkv;
+            a.part = b->part;
+            launch_batch_ctx_attn(b->map_k[l], b->map_v[l], a, st);
+        }
+        BatchUserMerge u{};
+        u.B = B;
+        u.H = H;
+        u.D = D;
+        u.L = L;
+        u.layer = l;
+        u.cap = b->cap;
+        u.KS = b->KSq;
+        u.n_qkv = 3 * h;
+        u.nsplit = ns;
+        u.qkv = b->qkv;
+        u.part = b->part;
+        u.uk = b->uk;
+        u.uv = b->uv;
+        u.state = b->state;
+        u.xhl = b->xhl;
+        launch_batch_user_merge(u, st);
+        launch_batch_proj(b->map_w, l * 4 * h + 3 * h, h, h, b->map_x, B, b->KSo, b->xpart, st);
+        BatchXprep xp{};
+        xp.mode = (l == L - 1) ? 2 : 1;
+        xp.B = B;
+        xp.h = h;
+        xp.KS = b->KSo;
+        xp.part = b->xpart;
+        xp.xin = b->xin;
+        xp.hist = b->hist;
+        xp.state = b->state;
+        xp.xhl = b->xhl;
+        launch_batch_xprep(xp, st);
+    }
+    launch_advance(b->state, 1, st);
+}
+
+void batch_free(ekv_batch_s* b) {
+    for (void* p : {(void*)b->uk, (void*)b->uv, (void*)b->xin, (void*)b->hist, (void*)b->emb,
+                    (void*)b->xhl, (void*)b->qkv, (void*)b->xpart, (void*)b->part, (void*)b->state})
+        if (p) cudaFree(p);
+}
+
+void batch_alloc(ekv_batch_s* b) {
+    ekv_model_s* m = b->model;
+    const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = d_of(m), h = m->h, B = b->B;
+    const int G = m->ctx->num_sms;
+    b->KSq = batch_proj_splits(3 * h, h, B, G);
+    b->KSo = batch_proj_splits(h, h, B, G);
+    b->nsplit = batch_ctx_splits(b->kv->S, H, B, G);
+    const size_t ukv = (size_t)B * L * H * b->cap * D;
+    b->uk = dalloc<uint16_t>(ukv);
+    b->uv = dalloc<uint16_t>(ukv);
+    b->xin = dalloc<float>((size_t)B * h);
+    b->hist = dalloc<float>((size_t)b->cap * B * h);
+    b->emb = dalloc<float>((size_t)B * b->cap * h);
+    b->xhl = dalloc<uint16_t>((size_t)2 * B * h);
+    b->qkv = dalloc<float>((size_t)b->KSq * B * 3 * h);
+    b->xpart = dalloc<float>((size_t)b->KSo * B * h);
+    b->part = dalloc<float>((size_t)B * H * std::max(b->nsplit, 1) * (D + 2));
+    b->state = dalloc<DevState>(1);
+    EKV_CUDA(cudaMemset(b->uk, 0, sizeof(uint16_t) * ukv));
+    EKV_CUDA(cudaMemset(b->uv, 0, sizeof(uint16_t) * ukv));
+    EKV_CUDA(cudaMemset(b->xin, 0, sizeof(float) * B * h));
+    EKV_CUDA(cudaMemset(b->state, 0, sizeof(DevState)));
+    b->map_w = make_map_2d(m->weights, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)h,
+                           (uint64_t)L * 4 * h, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    b->map_x = make_map_3d_bf16(b->xhl, (uint64_t)h, (uint64_t)B, 2, 64, (uint32_t)batch_proj_bn(B),
+                                CU_TENSOR_MAP_SWIZZLE_128B);
+    b->map_k.resize(L);
+    b->map_v.resize(L);
+    for (int l = 0; l < L; ++l) {
+        const ekv_segment& sg = b->kv->seg[l];
+        if (sg.S == 0) continue;
+        b->map_k[l] = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D,
+                                  (uint64_t)H * sg.S, (uint32_t)D, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        b->map_v[l] = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D,
+                                  (uint64_t)H * sg.S, (uint32_t)D, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+}
+
+void batch_check(ekv_batch_s* b, int n) {
+    const int total = b->kv->S + b->user_len + n;
+    require(total <= b->model->cfg.max_positions,
+            "position overflow: " + std::to_string(total) + " > max_positions " +
+                std::to_string(b->model->cfg.max_positions));
+    require(b->rows + n <= b->cap, "session full: " + std::to_string(b->rows + n) +
+                                       " rows > capacity " + std::to_string(b->cap));
+}
+
+void batch_replay(ekv_batch_s* b, cudaStream_t st) {
+    if (!b->graph) {
+        ekv_ctx_s* c = b->model->ctx;
+        const int64_t before = g_launches.load();
+        EKV_CUDA(cudaStreamBeginCapture(c->capture, cudaStreamCaptureModeThreadLocal));
+        try {
+            batch_row(b, c->capture);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(c->capture, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        EKV_CUDA(cudaStreamEndCapture(c->capture, &g));
+        EKV_CUDA(cudaGraphInstantiate(&b->graph, g, 0));
+        EKV_CUDA(cudaGraphDestroy(g));
+        b->graph_kernels = g_launches.load() - before;
+        g_launches -= b->graph_kernels;
+    }
+    EKV_CUDA(cudaGraphLaunch(b->graph, st));
+    count_launches(b->graph_kernels);
+}
+
+// rows [0, n) of emb (device, fp32 [B][n][h], row stride `ld` rows) as user rows
+void batch_forward(ekv_batch_s* b, const float* emb, int n, int ld, cudaStream_t st) {
+    batch_check(b, n);
+    const size_t h = b->model->h;
+    for (int r = 0; r < n; ++r) {
+        EKV_CUDA(cudaMemcpy2DAsync(b->xin, sizeof(float) * h, emb + (size_t)r * h, sizeof(float) * h * ld,
+                                   sizeof(float) * h, b->B, cudaMemcpyDeviceToDevice, st));
+        batch_replay(b, st);
+    }
+    b->user_len += n;
+    b->rows += n;
+}
+
+void batch_decode(ekv_batch_s* b, int steps, cudaStream_t st) {
+    require(steps >= 1, "collaborative_decode: steps must be >= 1");
+    batch_check(b, steps);
+    for (int t = 0; t < steps; ++t) batch_replay(b, st);
+    b->user_len += steps;
+    b->rows += steps;
+}
+
+void batch_reset(ekv_batch_s* b, cudaStream_t st) {
+    EKV_CUDA(cudaMemsetAsync(b->state, 0, sizeof(DevState), st));
+    EKV_CUDA(cudaMemsetAsync(b->xin, 0, sizeof(float) * b->B * b->model->h, st));
+    b->user_len = 0;
+    b->rows = 0;
 }
 
 }  // namespace
@@ -1355,6 +1556,137 @@ int ekv_collaborative_decode(ekv_session_t s, const float* user_emb, int U, int 
         }
         session_decode(s, steps, st);
         EKV_CUDA(cudaMemcpyAsync(step_out, s->hist, sizeof(float) * steps * h,
+                                 cudaMemcpyDeviceToHost, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+
+// ---------------------------------------------------------------- batched sessions
+int ekv_batch_create(ekv_model_t m, ekv_kvctx_t c, int sessions, int max_rows, ekv_batch_t* out) {
+    return guard([&] {
+        require(m && c && out, "ekv_batch_create: null argument");
+        require(c->model == m || (c->model->cfg.num_heads == m->cfg.num_heads &&
+                                  c->model->cfg.head_dim == m->cfg.head_dim),
+                "collaborative_decode: context dims do not match model; align with head pruning "
+                "first");
+        require((int)c->seg.size() == m->cfg.num_layers,
+                "collaborative_decode: context has " + std::to_string(c->seg.size()) +
+                    " layers, model has " + std::to_string(m->cfg.num_layers));
+        require(sessions >= 1, "ekv_batch_create: sessions must be >= 1");
+        require(max_rows >= 1, "ekv_batch_create: max_rows must be >= 1");
+        require(m->h % 128 == 0, "batched decode: hidden size must be a multiple of 128",
+                EKV_EUNSUPPORTED);
+        for (int l = 0; l < m->cfg.num_layers; ++l)
+            require(c->seg[l].S == 0 || batch_ctx_supported(d_of(m), c->seg[l].format),
+                    "batched decode: context layer " + std::to_string(l) + " format " +
+                        std::to_string(c->seg[l].format) + " with head_dim " +
+                        std::to_string(d_of(m)) + " not supported",
+                    EKV_EUNSUPPORTED);
+        set_dev(m->ctx);
+        auto* b = new ekv_batch_s();
+        b->model = m;
+        b->kv = c;
+        b->B = sessions;
+        b->cap = max_rows;
+        try {
+            batch_alloc(b);
+        } catch (...) {
+            batch_free(b);
+            delete b;
+            throw;
+        }
+        *out = b;
+    });
+}
+
+int ekv_batch_destroy(ekv_batch_t b) {
+    return guard([&] {
+        if (!b) return;
+        cudaSetDevice(b->model->ctx->device);
+        cudaStreamSynchronize(b->model->ctx->stream);
+        if (b->graph) cudaGraphExecDestroy(b->graph);
+        batch_free(b);
+        delete b;
+    });
+}
+
+int ekv_batch_reset(ekv_batch_t b) {
+    return guard([&] {
+        require(b != nullptr, "null batch");
+        set_dev(b->model->ctx);
+        batch_reset(b, b->model->ctx->stream);
+    });
+}
+
+int ekv_batch_info(ekv_batch_t b, int* sessions, int* rows, int* splits) {
+    return guard([&] {
+        require(b != nullptr, "null batch");
+        if (sessions) *sessions = b->B;
+        if (rows) *rows = b->rows;
+        if (splits) {
+            splits[0] = b->KSq;
+            splits[1] = b->KSo;
+            splits[2] = b->nsplit;
+        }
+    });
+}
+
+int ekv_batch_forward(ekv_batch_t b, const float* emb_dev, int n, float* out_dev) {
+    return guard([&] {
+        require(b && (emb_dev || n == 0), "ekv_batch_forward: null argument");
+        require(n >= 0, "ekv_batch_forward: negative row count");
+        if (n == 0) return;
+        set_dev(b->model->ctx);
+        cudaStream_t st = b->model->ctx->stream;
+        const int r0 = b->rows;
+        batch_forward(b, emb_dev, n, n, st);
+        if (out_dev)
+            EKV_CUDA(cudaMemcpyAsync(out_dev, b->hist + (size_t)r0 * b->B * b->model->h,
+                                     sizeof(float) * n * b->B * b->model->h, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+int ekv_batch_decode(ekv_batch_t b, int steps, float* out_dev) {
+    return guard([&] {
+        require(b != nullptr, "null batch");
+        set_dev(b->model->ctx);
+        cudaStream_t st = b->model->ctx->stream;
+        const int r0 = b->rows;
+        batch_decode(b, steps, st);
+        if (out_dev)
+            EKV_CUDA(cudaMemcpyAsync(out_dev, b->hist + (size_t)r0 * b->B * b->model->h,
+                                     sizeof(float) * steps * b->B * b->model->h, cudaMemcpyDeviceToDevice,
+                                     st));
+    });
+}
+
+int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb, int U, int steps,
+                                   float* prefill_out, float* step_out) {
+    return guard([&] {
+        require(b && step_out && (U == 0 || user_emb), "collaborative_decode: null argument");
+        require(steps >= 1, "collaborative_decode: steps must be >= 1");
+        require(U >= 0, "collaborative_decode: negative user rows");
+        ekv_model_s* m = b->model;
+        set_dev(m->ctx);
+        cudaStream_t st = m->ctx->stream;
+        const int total = b->kv->S + U + steps;
+        require(total <= m->cfg.max_positions,
+                "position overflow: " + std::to_string(total) + " > max_positions " +
+                    std::to_string(m->cfg.max_positions));
+        require(U + steps <= b->cap, "session full: " + std::to_string(U + steps) +
+                                         " rows > capacity " + std::to_string(b->cap));
+        batch_reset(b, st);
+        const size_t h = m->h, B = b->B;
+        if (U > 0) {
+            EKV_CUDA(cudaMemcpyAsync(b->emb, user_emb, sizeof(float) * B * U * h, cudaMemcpyHostToDevice, st));
+            batch_forward(b, b->emb, U, U, st);
+            if (prefill_out)
+                EKV_CUDA(cudaMemcpyAsync(prefill_out, b->hist, sizeof(float) * U * B * h,
+                                         cudaMemcpyDeviceToHost, st));
+        }
+        batch_decode(b, steps, st);
+        EKV_CUDA(cudaMemcpyAsync(step_out, b->hist + (size_t)U * B * h, sizeof(float) * steps * B * h,
                                  cudaMemcpyDeviceToHost, st));
         EKV_CUDA(cudaStreamSynchronize(st));
     });

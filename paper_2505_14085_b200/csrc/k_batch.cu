@@ -1,0 +1,634 @@
+// Batched collaborative decode: B concurrent edge sessions that share one
+// assembled context (the paper's shared system prompt; the
+// reference serves every request with its own user cache over one read-only
+// context cache, cache_merge.cpp:252) advance one row per step
+// in lock-step.  Per session the arithmetic is merged_forward
+// (cache_merge.cpp:156-226); the kernels below change only how the work of
+// the B sessions is laid out on the B200:
+//
+//   K9  batch_proj_kernel   y^T[n][b] = W[n][:] . x[b][:] on tcgen05 (swap-AB:
+//                           the weight rows are the M=128 side, the sessions the
+//                           N side), x split into bf16 hi + lo halves (two MMAs
+//                           into one fp32 TMEM accumulator: ~2^-17 input
+//                           precision), split-K partials written, not atomically
+//                           added (deterministic).  Every weight byte is read
+//                           once per step for all B sessions.
+//   K10 batch_ctx_attn_kernel  the context segment (segment_attention over the S
+//                           shared rows, cache_merge.cpp:12-38) of all sessions
+//                           of a head as a cascade: S = Q K^T and O = P V on
+//                           tcgen05 (Q and P also split hi + lo), online
+//                           softmax on the CUDA cores, K/V chunks moved by TMA;
+//                           every context byte is read once per step.
+//   K11 batch_user_merge_kernel  per (session, head): this step's K/V appended
+//                           to the session's bf16 user cache, the user segment
+//                           (causal over the session's own rows), the Eq. 5
+//                           merge with the context partials
+//                           (merge_attention, cache_merge.cpp:59-80), output
+//                           split hi + lo as the next projection's operand.
+//   K12 batch_xprep_kernel  sums split-K partials; layer-0 input transform
+//                           (cache_merge.cpp:167-177); final-layer output row.
+#include "ekv_common.cuh"
+#include "ekv_batch.h"
+#include "ekv_tc.cuh"
+
+namespace ekv {
+
+using namespace tc;
+
+// ============================================================================
+// K9: projection GEMM  out[ks][b][n] = sum_{k in split ks} W[w_row0 + n][k] * x[b][k]
+// ============================================================================
+namespace k9 {
+constexpr int BM = 128, BK = 64, THREADS = 256;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB weight tile
+
+__global__ void __launch_bounds__(THREADS, 1)
+    batch_proj_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                      int w_row0, int N_out, int K, int B, int BN, int KS, int stages, uint32_t idesc,
+                      float* __restrict__ out) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int x_bytes = BN * BK * 2;              // one of hi / lo
+    const int stage_bytes = A_BYTES + 2 * x_bytes;
+    uint64_t* bars = (uint64_t*)(smem + stages * stage_bytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + stages;
+    uint64_t* tfull = bars + 2 * stages;
+    uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mt = blockIdx.x, nt = blockIdx.y, ks = blockIdx.z;
+    const int kblocks = K / BK;
+    const int kb0 = (int)((long long)ks * kblocks / KS), kb1 = (int)((long long)(ks + 1) * kblocks / KS);
+    const uint32_t tcols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));  // power of 2
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+        for (int i = 0; i < stages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tfull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, tcols);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_expect_tx(&full[stage], stage_bytes);
+                uint8_t* s = smem + stage * stage_bytes;
+                tma_load_2d(&map_w, &full[stage], s, kb * BK, w_row0 + mt * BM);
+                tma_load_3d(&map_x, &full[stage], s + A_BYTES, kb * BK, nt * BN, 0);
+                tma_load_3d(&map_x, &full[stage], s + A_BYTES + x_bytes, kb * BK, nt * BN, 1);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = kb0; kb < kb1; ++kb) {
+                mbar_wait(&full[stage], phase);
+                fence_after();
+                const uint32_t a0 = smem_u32(smem + stage * stage_bytes);
+                const uint32_t bh = a0 + A_BYTES, bl = bh + x_bytes;
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+                    const uint64_t ad = desc_sw128(a0 + k * 32);
+                    mma_bf16(tmem, ad, desc_sw128(bh + k * 32), idesc, (kb > kb0) || (k > 0));
+                    mma_bf16(tmem, ad, desc_sw128(bl + k * 32), idesc, 1);
+                }
+                mma_commit(&empty[stage]);
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            mma_commit(tfull);
+        }
+    } else if (warp >= 4) {
+        const int quad = warp - 4;
+        mbar_wait(tfull, 0);
+        fence_after();
+        const int n = mt * BM + quad * 32 + lane;
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16);
+        float* o = out + (size_t)ks * B * N_out + n;
+        for (int c = 0; c < BN / 32; ++c) {
+            float v[32];
+            tmem_ld32(taddr + c * 32, v);
+            const int b0 = nt * BN + c * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (b0 + i < B && n < N_out) o[(size_t)(b0 + i) * N_out] = v[i];
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 2) tmem_dealloc(tmem, tcols);
+}
+}  // namespace k9
+
+// ============================================================================
+// K12: x preparation.  x[b] = in (mode 0: xin[b]; else sum_ks part[ks][b]);
+// layer-0 transform x0 = gamma*(x + pos[S + user_len]) + bias (mode 0);
+// final layer (mode 2): x -> hist[step][b] and xin[b].  Writes hi/lo bf16.
+// ============================================================================
+__global__ void batch_xprep_kernel(BatchXprep a) {
+    const int b = blockIdx.y;
+    const int h = a.h;
+    const DevState st = *a.state;
+    const int p = a.pos_offset + st.user_len;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < h; k += gridDim.x * blockDim.x) {
+        float x;
+        if (a.mode == 0) {
+            x = a.xin[(size_t)b * h + k];
+            const float pe = __uint_as_float((uint32_t)a.pos[(size_t)p * h + k] << 16);
+            x = a.gamma[k] * (x + pe) + a.bias[k];
+        } else {
+            x = 0.0f;
+            for (int s = 0; s < a.KS; ++s) x += a.part[((size_t)s * a.B + b) * h + k];
+        }
+        if (a.mode == 2) {
+            a.hist[((size_t)st.step * a.B + b) * h + k] = x;
+            a.xin[(size_t)b * h + k] = x;
+        } else {
+            uint16_t hi, lo;
+            split_bf16(x, hi, lo);
+            a.xhl[(size_t)b * h + k] = hi;
+            a.xhl[((size_t)a.B + b) * h + k] = lo;
+        }
+    }
+}
+
+// ============================================================================
+// K10: context attention of B sessions over the shared context, one head and
+// one contiguous range of 128-row chunks per CTA.
+// ============================================================================
+namespace k10 {
+constexpr int BT = 128;        // sessions per CTA (MMA M)
+constexpr int CH = 128;        // context rows per chunk (MMA N of S = Q K^T; K of O = P V)
+constexpr int THREADS = 256;   // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 int8 expand helper, 4-7 softmax
+constexpr int STAGES = 3;
+
+template <int D>
+struct Cfg {
+    static constexpr int ROWB = D * 2;                  // bf16 row bytes (== swizzle width)
+    static constexpr int Q_BYTES = BT * ROWB;           // one of Q hi / lo
+    static constexpr int KV_BYTES = CH * ROWB;          // one K or V chunk (bf16)
+    static constexpr int P_BYTES = BT * CH * 2;         // one of P hi / lo (2 panels of 64 rows)
+    static constexpr int STAGE_BYTES = 2 * KV_BYTES;    // K + V
+    static constexpr int CODE_BYTES = CH * D;           // int8 staging of one K or V chunk
+    static constexpr int SMEM = 2 * Q_BYTES + STAGES * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
+};
+
+// swizzle helpers for the 128-byte-row K-major panels (D = 64 rows are exactly one atom)
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); }
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 1)
+    batch_ctx_attn_kernel(const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
+                          BatchCtxAttn a) {
+    static_assert(D == 64, "batched context attention: head_dim 64");
+    using C = Cfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sQ = smem;                                   // hi, lo
+    uint8_t* sKV = sQ + 2 * C::Q_BYTES;                   // STAGES x (K, V)
+    uint8_t* sP = sKV + STAGES * C::STAGE_BYTES;          // hi (2 panels), lo (2 panels)
+    uint64_t* bars = (uint64_t*)(sP + 2 * C::P_BYTES);
+    uint64_t* full = bars;                 // [STAGES] TMA -> MMA
+    uint64_t* empty = bars + STAGES;       // [STAGES] MMA -> TMA
+    uint64_t* qready = bars + 2 * STAGES;  // softmax warps -> MMA (Q staged), count 4
+    uint64_t* sfull = qready + 1;          // MMA -> softmax (S in TMEM)
+    uint64_t* sfree = sfull + 1;           // softmax -> MMA (S read), count 4
+    uint64_t* pready = sfree + 1;          // softmax -> MMA (P staged), count 4
+    uint64_t* ofull = pready + 1;          // MMA -> softmax (O chunk in TMEM)
+    uint32_t* tmem_slot = (uint32_t*)(ofull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int hd = blockIdx.x, split = blockIdx.y, bt = blockIdx.z;
+    const int nchunks = (a.S + CH - 1) / CH;
+    const int c0 = (int)((long long)split * nchunks / a.nsplit);
+    const int c1 = (int)((long long)(split + 1) * nchunks / a.nsplit);
+    const int nloc = c1 - c0;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_k) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_v) : "memory");
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(qready, 4);
+        mbar_init(sfull, 1);
+        mbar_init(sfree, 4);
+        mbar_init(pready, 4);
+        mbar_init(ofull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, 256);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tS = tmem, tO = tmem + CH;  // S: 128 columns, O: D columns
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int c = c0; c < c1; ++c) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+                uint8_t* s = sKV + stage * C::STAGE_BYTES;
+                const int row = hd * a.S + c * CH;
+                tma_load_2d(&map_k, &full[stage], s, 0, row);
+                tma_load_2d(&map_v, &full[stage], s + C::KV_BYTES, 0, row);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t idS = idesc_bf16(BT, CH);
+            const uint32_t idO = idesc_bf16(BT, D, false, true);  // V is MN-major (d contiguous)
+            const uint32_t q0 = smem_u32(sQ), q1 = q0 + C::Q_BYTES;
+            const uint32_t p0 = smem_u32(sP), p1 = p0 + C::P_BYTES;
+            mbar_wait(qready, 0);
+            fence_after();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < nloc; ++i) {
+                mbar_wait(&full[stage], phase);
+                mbar_wait(sfree, (i & 1) ^ 1);  // S of the previous chunk consumed
+                fence_after();
+                const uint32_t kb = smem_u32(sKV + stage * C::STAGE_BYTES);
+                const uint32_t vb = kb + C::KV_BYTES;
+#pragma unroll
+                for (int k = 0; k < D / 16; ++k) {
+                    const uint64_t bd = desc_sw128(kb + k * 32);
+                    mma_bf16(tS, desc_sw128(q0 + k * 32), bd, idS, k > 0);
+                    mma_bf16(tS, desc_sw128(q1 + k * 32), bd, idS, 1);
+                }
+                mma_commit(sfull);
+                mbar_wait(pready, i & 1);
+                fence_after();
+                // O = P V: K dimension = the 128 chunk rows (2 panels of 64), 16 per MMA;
+                // V rows are 128-byte MN-major rows, 8-row atoms 1024 B apart.
+#pragma unroll
+                for (int k = 0; k < CH / 16; ++k) {
+                    const uint32_t poff = (k >> 2) * (BT * 128) + (k & 3) * 32;
+                    const uint64_t vd = desc_sw128(vb + k * 16 * C::ROWB, 16, 1024);
+                    mma_bf16(tO, desc_sw128(p0 + poff), vd, idO, k > 0);
+                    mma_bf16(tO, desc_sw128(p1 + poff), vd, idO, 1);
+                }
+                mma_commit(ofull);
+                mma_commit(&empty[stage]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int quad = warp - 4;
+        const int r = quad * 32 + lane;             // session row of this CTA's tile
+        const int b = bt * BT + r;
+        const bool live = b < a.B;
+        const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+        // ---- stage q (sum of the split-K partials of the QKV projection) as hi / lo ----
+        {
+            const uint32_t qh = smem_u32(sQ), ql = qh + C::Q_BYTES;
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+                uint16_t hi[8], lo[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    float x = 0.0f;
+                    if (live) {
+                        const float* qp = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8 + e;
+                        for (int s = 0; s < a.KS; ++s) x += qp[(size_t)s * a.B * a.n_qkv];
+                    }
+                    split_bf16(x, hi[e], lo[e]);
+                }
+                const uint32_t off = sw128_off(r, c);
+                st_shared_v4(qh + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
+                             pack2(hi[6], hi[7]));
+                st_shared_v4(ql + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
+                             pack2(lo[6], lo[7]));
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(qready);
+        }
+        float m = -INFINITY, l = 0.0f;
+        float o[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) o[i] = 0.0f;
+        const uint32_t ph = smem_u32(sP), pl = ph + C::P_BYTES;
+        for (int i = 0; i < nloc; ++i) {
+            const int cbase = (c0 + i) * CH;
+            const int valid = min(CH, a.S - cbase);
+            mbar_wait(sfull, i & 1);
+            fence_after();
+            float s[CH];
+#pragma unroll
+            for (int c = 0; c < CH / 32; ++c) tmem_ld32(tS + lane_off + c * 32, s + c * 32);
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sfree);
+            float mx = m;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                if (j >= valid) s[j] = -INFINITY;
+                mx = fmaxf(mx, s[j]);
+            }
+            const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
+            float rs = 0.0f;
+#pragma unroll
+            for (int c = 0; c < CH / 8; ++c) {
+                uint16_t hi[8], lo[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float p = (c * 8 + e < valid) ? __expf(s[c * 8 + e] - mx) : 0.0f;
+                    rs += p;
+                    split_bf16(p, hi[e], lo[e]);
+                }
+                const uint32_t off = (c >> 3) * (BT * 128) + sw128_off(r, c & 7);
+                st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
+                             pack2(hi[6], hi[7]));
+                st_shared_v4(pl + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
+                             pack2(lo[6], lo[7]));
+            }
+            m = mx;
+            l = l * alpha + rs;
+            fence_async_smem();
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(pready);
+            mbar_wait(ofull, i & 1);
+            fence_after();
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                float v[32];
+                tmem_ld32(tO + lane_off + c * 32, v);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha + v[e];
+            }
+            fence_before();
+        }
+        if (live) {
+            float* w = a.part + (((size_t)b * a.H + hd) * a.nsplit + split) * (D + 2);
+            w[0] = m;
+            w[1] = l;
+#pragma unroll
+            for (int e = 0; e < D; ++e) w[2 + e] = o[e];
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 2) tmem_dealloc(tmem, 256);
+}
+}  // namespace k10
+
+// ============================================================================
+// K11: user segment + append + Eq. 5 merge, one warp per (session, head).
+// ============================================================================
+template <int D>
+__global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a) {
+    constexpr int E = D / 32;  // dims per lane
+    const int lane = threadIdx.x & 31;
+    const int item = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (item >= a.B * a.H) return;
+    const int b = item / a.H, hd = item - b * a.H;
+    const int h = a.H * D;
+    const int ulen = a.state->user_len;
+    // this step's q, k, v: sum of the split-K partials
+    float q[E], kc[E], vc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int n = hd * D + lane * E + e;
+        float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
+        for (int s = 0; s < a.KS; ++s) {
+            const float* p = a.qkv + ((size_t)s * a.B + b) * a.n_qkv;
+            x0 += p[n];
+            x1 += p[h + n];
+            x2 += p[2 * h + n];
+        }
+        q[e] = x0;
+        kc[e] = __bfloat162float(__float2bfloat16_rn(x1));
+        vc[e] = __bfloat162float(__float2bfloat16_rn(x2));
+    }
+    // append (cache_merge.cpp:189-199): row ulen of this session's user cache
+    const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
+    uint16_t* uk = a.uk + head_off;
+    uint16_t* uv = a.uv + head_off;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        uk[(size_t)ulen * D + lane * E + e] = f32_to_bf16_bits(kc[e]);
+        uv[(size_t)ulen * D + lane * E + e] = f32_to_bf16_bits(vc[e]);
+    }
+    // user segment over rows [0, ulen) from the cache, then the current row
+    float m = -INFINITY, l = 0.0f, o[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    for (int j0 = 0; j0 < ulen; j0 += 32) {
+        const int nj = min(32, ulen - j0);
+        float pp[32];
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) {
+            float acc = 0.0f;
+            if (jj < nj) {
+                const uint16_t* kr = uk + (size_t)(j0 + jj) * D + lane * E;
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc += q[e] * __uint_as_float((uint32_t)kr[e] << 16);
+            }
+            pp[jj] = acc;
+        }
+        // butterfly reduce-scatter: lane jj ends with the full dot of row j0 + jj
+#pragma unroll
+        for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+            const bool upper = lane & off;
+#pragma unroll
+            for (int i = 0; i < n / 2; ++i) {
+                const float send = upper ? pp[i] : pp[i + n / 2];
+                const float keep = upper ? pp[i + n / 2] : pp[i];
+                pp[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+            }
+        }
+        // lane -> row mapping of the butterfly: lane L holds row bitrev-free index L
+        const float s = lane < nj ? pp[0] : -INFINITY;
+        const float mx = fmaxf(m, warp_max(s));
+        const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
+        const float p = lane < nj ? __expf(s - mx) : 0.0f;
+        l = l * alpha + warp_sum(p);
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] *= alpha;
+        for (int jj = 0; jj < nj; ++jj) {
+            const float pj = __shfl_sync(0xffffffffu, p, jj);
+            const uint16_t* vr = uv + (size_t)(j0 + jj) * D + lane * E;
+#pragma unroll
+            for (int e = 0; e < E; ++e) o[e] += pj * __uint_as_float((uint32_t)vr[e] << 16);
+        }
+        m = mx;
+    }
+    {
+        float acc = 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc += q[e] * kc[e];
+        const float s = warp_sum(acc);
+        const float mx = fmaxf(m, s);
+        const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
+        const float p = __expf(s - mx);
+        l = l * alpha + p;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = o[e] * alpha + p * vc[e];
+        m = mx;
+    }
+    // Eq. 5 generalised: log-sum-exp merge of the user partial with the context partials
+    if (a.nsplit > 0) {
+        const float* w = a.part + ((size_t)b * a.H + hd) * a.nsplit * (D + 2);
+        float M = m;
+        for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, w[s * (D + 2)]);
+        const float fu = __expf(m - M);
+        float Lt = l * fu, ot[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) ot[e] = o[e] * fu;
+        for (int s = 0; s < a.nsplit; ++s) {
+            const float* ws = w + s * (D + 2);
+            const float f = ws[0] == -INFINITY ? 0.0f : __expf(ws[0] - M);
+            Lt += ws[1] * f;
+#pragma unroll
+            for (int e = 0; e < E; ++e) ot[e] += ws[2 + lane * E + e] * f;
+        }
+        l = Lt;
+#pragma unroll
+        for (int e = 0; e < E; ++e) o[e] = ot[e];
+    }
+    const float inv = 1.0f / l;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        uint16_t hi, lo;
+        split_bf16(o[e] * inv, hi, lo);
+        const size_t k = (size_t)b * h + hd * D + lane * E + e;
+        a.xhl[k] = hi;
+        a.xhl[(size_t)a.B * h + k] = lo;
+    }
+}
+
+// ============================================================================
+// host launchers
+// ============================================================================
+CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t inner,
+                        uint64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
+CUtensorMap make_map_3d_bf16(const void* base, uint64_t inner, uint64_t rows, uint64_t depth,
+                             uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
+
+int batch_proj_bn(int B) {
+    int bn = ((B + 31) / 32) * 32;
+    return bn > 256 ? 256 : bn;
+}
+
+int batch_proj_splits(int N_out, int K, int B, int num_sms) {
+    const int tiles = (N_out / k9::BM) * ((B + batch_proj_bn(B) - 1) / batch_proj_bn(B));
+    int ks = (num_sms + tiles / 2) / tiles;
+    const int kblocks = K / k9::BK;
+    if (ks < 1) ks = 1;
+    if (ks > kblocks) ks = kblocks;
+    if (ks > 16) ks = 16;
+    return ks;
+}
+
+void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, const CUtensorMap& map_x,
+                       int B, int KS, float* out, cudaStream_t st) {
+    using namespace k9;
+    require(N_out % BM == 0 && K % BK == 0, "batch projection: h must be a multiple of 128",
+            EKV_EUNSUPPORTED);
+    const int BN = batch_proj_bn(B);
+    const int stage_bytes = A_BYTES + 2 * BN * BK * 2;
+    int stages = (200 * 1024) / stage_bytes;
+    if (stages > 6) stages = 6;
+    const int smem = stages * stage_bytes + 1024 + 256;
+    static int attr = 0;
+    if (attr < smem) {
+        EKV_CUDA(cudaFuncSetAttribute(batch_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = 227 * 1024;
+    }
+    dim3 grid(N_out / BM, (B + BN - 1) / BN, KS);
+    batch_proj_kernel<<<grid, THREADS, smem, st>>>(map_w, map_x, w_row0, N_out, K, B, BN, KS, stages,
+                                                    idesc_bf16(BM, BN), out);
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+void launch_batch_xprep(const BatchXprep& a, cudaStream_t st) {
+    dim3 grid((a.h + 255) / 256, a.B);
+    batch_xprep_kernel<<<grid, 256, 0, st>>>(a);
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+int batch_ctx_splits(int S, int H, int B, int num_sms) {
+    if (S <= 0) return 0;
+    const int nchunks = (S + k10::CH - 1) / k10::CH;
+    const int nbt = (B + k10::BT - 1) / k10::BT;
+    int ns = (num_sms + H * nbt - 1) / (H * nbt);
+    if (ns > nchunks) ns = nchunks;
+    if (ns < 1) ns = 1;
+    return ns;
+}
+
+bool batch_ctx_supported(int D, int fmt) { return D == 64 && fmt == EKV_KV_BF16; }
+
+void launch_batch_ctx_attn(const CUtensorMap& map_k, const CUtensorMap& map_v, const BatchCtxAttn& a,
+                           cudaStream_t st) {
+    using namespace k10;
+    require(a.D == 64, "batched context attention supports head_dim 64", EKV_EUNSUPPORTED);
+    using Cf = Cfg<64>;
+    static bool attr = false;
+    if (!attr) {
+        EKV_CUDA(cudaFuncSetAttribute(batch_ctx_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cf::SMEM));
+        attr = true;
+    }
+    dim3 grid(a.H, a.nsplit, (a.B + BT - 1) / BT);
+    batch_ctx_attn_kernel<64><<<grid, THREADS, Cf::SMEM, st>>>(map_k, map_v, a);
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st) {
+    const int items = a.B * a.H;
+    const int grid = (items + 3) / 4;
+    switch (a.D) {
+        case 32: batch_user_merge_kernel<32><<<grid, 128, 0, st>>>(a); break;
+        case 64: batch_user_merge_kernel<64><<<grid, 128, 0, st>>>(a); break;
+        case 128: batch_user_merge_kernel<128><<<grid, 128, 0, st>>>(a); break;
+        default: require(false, "batched decode: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
+    }
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+}  // namespace ekv

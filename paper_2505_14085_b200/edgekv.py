@@ -413,6 +413,66 @@ class Session:
             pass
 
 
+class SessionBatch:
+    """ekv_batch: B concurrent sessions over one shared AssembledContext, advanced in
+    lock-step (BASELINE configs[2]).  Per session the result is collaborative_decode
+    (cache_merge.cpp:230-273); weights and context are streamed once per step for all
+    sessions (k_batch.cu)."""
+
+    def __init__(self, model: EdgeModel, context: AssembledContext, sessions: int, max_rows: int):
+        self.model, self.context, self.B, self.cap = model, context, sessions, max_rows
+        hnd = C.c_void_p()
+        call("ekv_batch_create", model.hnd, context.hnd, sessions, max_rows, C.byref(hnd))
+        self.hnd = hnd
+
+    def reset(self):
+        call("ekv_batch_reset", self.hnd)
+
+    def info(self):
+        b = C.c_int(); r = C.c_int(); sp = (C.c_int * 3)()
+        call("ekv_batch_info", self.hnd, C.byref(b), C.byref(r), sp)
+        return {"sessions": b.value, "rows": r.value, "qkv_splitk": sp[0], "out_splitk": sp[1],
+                "ctx_splits": sp[2]}
+
+    def forward(self, emb: torch.Tensor) -> torch.Tensor:
+        """n user rows of every session: device fp32 [B][n][h] -> outputs [n][B][h]."""
+        emb = emb.contiguous().float()
+        n = emb.shape[1]
+        out = torch.empty((n, self.B, self.model.h), dtype=torch.float32, device=emb.device)
+        _sync_in()
+        call("ekv_batch_forward", self.hnd, _ptr(emb), n, _ptr(out))
+        self.model.ctx.synchronize()
+        return out
+
+    def decode(self, steps: int, out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((steps, self.B, self.model.h), dtype=torch.float32,
+                              device=f"cuda:{self.model.ctx.device}")
+        call("ekv_batch_decode", self.hnd, steps, _ptr(out))
+        if sync:
+            self.model.ctx.synchronize()
+        return out
+
+    def __del__(self):
+        try:
+            capi.load().ekv_batch_destroy(self.hnd)
+        except Exception:
+            pass
+
+
+def collaborative_decode_batch(batch: SessionBatch, user_embeddings: np.ndarray, steps: int):
+    """collaborative_decode of every session of the batch through the host-buffer C-ABI
+    entry point: user_embeddings [B][U][h] -> (prefill [U][B][h], steps [steps][B][h])."""
+    h, B = batch.model.h, batch.B
+    ue = np.ascontiguousarray(np.asarray(user_embeddings, dtype=np.float32).reshape(B, -1, h))
+    U = ue.shape[1]
+    pre = np.zeros((max(U, 1), B, h), dtype=np.float32)
+    st = np.zeros((max(steps, 1), B, h), dtype=np.float32)
+    call("ekv_collaborative_decode_batch", batch.hnd, ue.ctypes.data_as(C.c_void_p), U, steps,
+         pre.ctypes.data_as(C.c_void_p), st.ctypes.data_as(C.c_void_p))
+    return pre[:U], st[:steps]
+
+
 def collaborative_decode(session: Session, user_embeddings: np.ndarray, steps: int):
     """collaborative_decode (cache_merge.cpp:230-273) through the host-buffer C-ABI entry
     point.  Returns (prefill_outputs [U][h], step_outputs [steps][h]) as fp32 numpy."""
