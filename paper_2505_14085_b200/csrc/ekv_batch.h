@@ -41,6 +41,7 @@ struct BatchUserMerge {
 
 CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t inner,
                         uint64_t rows, uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
+CUtensorMap make_map_1d(const void* base, CUtensorMapDataType dt, uint64_t n, uint32_t box);
 CUtensorMap make_map_3d_bf16(const void* base, uint64_t inner, uint64_t rows, uint64_t depth,
                              uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw);
 
@@ -50,9 +51,14 @@ void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, c
                        int B, int KS, float* out, cudaStream_t st);
 void launch_batch_xprep(const BatchXprep& a, cudaStream_t st);
 int batch_ctx_splits(int S, int H, int B, int num_sms);
-bool batch_ctx_supported(int D, int fmt);
-void launch_batch_ctx_attn(const CUtensorMap& map_k, const CUtensorMap& map_v, const BatchCtxAttn& a,
-                           cudaStream_t st);
+// tensor maps of one context layer: bf16 -> k, v tiles [H*S][D] (SW128);
+// int8 -> k, v codes [H*S][D] bytes and ks, vs row scales [H*S] fp32 (1-D)
+struct BatchCtxMaps {
+    int fmt;
+    CUtensorMap k, v, ks, vs;
+};
+bool batch_ctx_supported(int D, int fmt, int group);
+void launch_batch_ctx_attn(const BatchCtxMaps& maps, const BatchCtxAttn& a, cudaStream_t st);
 void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st);
 
 }  // namespace ekv

@@ -437,7 +437,7 @@ struct ekv_batch_s {
     float* part = nullptr;    // [B][H][nsplit][D+2]
     DevState* state = nullptr;
     CUtensorMap map_w{}, map_x{};
-    std::vector<CUtensorMap> map_k, map_v;
+    std::vector<BatchCtxMaps> maps;   // per context layer
     cudaGraphExec_t graph = nullptr;
     int64_t graph_kernels = 0;
     int user_len = 0, rows = 0;
@@ -475,7 +475,7 @@ void batch_row(ekv_batch_s* b, cudaStream_t st) {
             a.n_qkv = 3 * h;
             a.qkv = b->qkv;
             a.part = b->part;
-            launch_batch_ctx_attn(b->map_k[l], b->map_v[l], a, st);
+            launch_batch_ctx_attn(b->maps[l], a, st);
         }
         BatchUserMerge u{};
         u.B = B;
@@ -542,15 +542,26 @@ void batch_alloc(ekv_batch_s* b) {
                            (uint64_t)L * 4 * h, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
     b->map_x = make_map_3d_bf16(b->xhl, (uint64_t)h, (uint64_t)B, 2, 64, (uint32_t)batch_proj_bn(B),
                                 CU_TENSOR_MAP_SWIZZLE_128B);
-    b->map_k.resize(L);
-    b->map_v.resize(L);
+    b->maps.resize(L);
     for (int l = 0; l < L; ++l) {
         const ekv_segment& sg = b->kv->seg[l];
+        BatchCtxMaps& mp = b->maps[l];
+        mp.fmt = sg.format;
         if (sg.S == 0) continue;
-        b->map_k[l] = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D,
-                                  (uint64_t)H * sg.S, (uint32_t)D, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-        b->map_v[l] = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D,
-                                  (uint64_t)H * sg.S, (uint32_t)D, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        const uint64_t rows = (uint64_t)H * sg.S;
+        if (sg.format == EKV_KV_BF16) {
+            mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
+                               CU_TENSOR_MAP_SWIZZLE_128B);
+            mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
+                               CU_TENSOR_MAP_SWIZZLE_128B);
+        } else {
+            mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+            mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+            mp.ks = make_map_1d(sg.k_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
+            mp.vs = make_map_1d(sg.v_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
+        }
     }
 }
 
@@ -1578,7 +1589,7 @@ int ekv_batch_create(ekv_model_t m, ekv_kvctx_t c, int sessions, int max_rows, e
         require(m->h % 128 == 0, "batched decode: hidden size must be a multiple of 128",
                 EKV_EUNSUPPORTED);
         for (int l = 0; l < m->cfg.num_layers; ++l)
-            require(c->seg[l].S == 0 || batch_ctx_supported(d_of(m), c->seg[l].format),
+            require(c->seg[l].S == 0 || batch_ctx_supported(d_of(m), c->seg[l].format, c->seg[l].group),
                     "batched decode: context layer " + std::to_string(l) + " format " +
                         std::to_string(c->seg[l].format) + " with head_dim " +
                         std::to_string(d_of(m)) + " not supported",

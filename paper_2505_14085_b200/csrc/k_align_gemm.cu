@@ -343,6 +343,20 @@ CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int elem_bytes
     return m;
 }
 
+CUtensorMap make_map_1d(const void* base, CUtensorMapDataType dt, uint64_t n, uint32_t box) {
+    CUtensorMap m;
+    cuuint64_t dims[1] = {n};
+    cuuint64_t strides[1] = {0};
+    cuuint32_t bx[1] = {box};
+    cuuint32_t estr[1] = {1};
+    CUresult r = get_encode()(&m, dt, 1, const_cast<void*>(base), dims, strides, bx, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (1-D) failed (" + std::to_string((int)r) + ")",
+            EKV_ECUDA);
+    return m;
+}
+
 CUtensorMap make_map_3d_bf16(const void* base, uint64_t inner, uint64_t rows, uint64_t depth,
                              uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw) {
     CUtensorMap m;

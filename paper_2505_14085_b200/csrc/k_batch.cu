@@ -180,21 +180,24 @@ __global__ void batch_xprep_kernel(BatchXprep a) {
 namespace k10 {
 constexpr int BT = 128;        // sessions per CTA (MMA M)
 constexpr int CH = 128;        // context rows per chunk (MMA N of S = Q K^T; K of O = P V)
-constexpr int THREADS = 256;   // warp 0 TMA, 1 MMA, 2 TMEM alloc, 3 int8 expand helper, 4-7 softmax
+constexpr int THREADS = 256;   // warp 0 TMA, 1 MMA, 2-3 TMEM alloc + int8 expansion, 4-7 softmax
 constexpr int STAGES = 3;
 
-template <int D>
+template <int D, int FMT>
 struct Cfg {
     static constexpr int ROWB = D * 2;                  // bf16 row bytes (== swizzle width)
     static constexpr int Q_BYTES = BT * ROWB;           // one of Q hi / lo
     static constexpr int KV_BYTES = CH * ROWB;          // one K or V chunk (bf16)
     static constexpr int P_BYTES = BT * CH * 2;         // one of P hi / lo (2 panels of 64 rows)
-    static constexpr int STAGE_BYTES = 2 * KV_BYTES;    // K + V
-    static constexpr int CODE_BYTES = CH * D;           // int8 staging of one K or V chunk
-    static constexpr int SMEM = 2 * Q_BYTES + STAGES * STAGE_BYTES + 2 * P_BYTES + 1024 + 512;
+    static constexpr int CODE_BYTES = CH * D;           // int8 codes of one K or V chunk
+    // TMA stage: bf16 -> K, V tiles; int8 -> K, V codes + K, V row scales
+    static constexpr int STAGE_BYTES = FMT == 16 ? 2 * KV_BYTES : 2 * CODE_BYTES + 2 * CH * 4;
+    // int8: expanded bf16 K, V tiles (+ scales), double-buffered
+    static constexpr int XBUF_BYTES = FMT == 16 ? 0 : 2 * KV_BYTES + 2 * CH * 4;
+    static constexpr int NXBUF = FMT == 16 ? 0 : 2;
+    static constexpr int SMEM = 2 * Q_BYTES + STAGES * STAGE_BYTES + NXBUF * XBUF_BYTES + 2 * P_BYTES + 1024 + 512;
 };
 
-// swizzle helpers for the 128-byte-row K-major panels (D = 64 rows are exactly one atom)
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
@@ -202,26 +205,40 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 
 __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); }
 
-template <int D>
+// 4 signed int8 codes -> 2 words of 2 bf16 each (exact: |code| <= 127)
+__device__ __forceinline__ void i8x4_to_bf16x4(uint32_t w, uint32_t& lo, uint32_t& hi) {
+    const float f0 = (float)(int8_t)(w & 0xFF), f1 = (float)(int8_t)((w >> 8) & 0xFF);
+    const float f2 = (float)(int8_t)((w >> 16) & 0xFF), f3 = (float)(int8_t)(w >> 24);
+    lo = (__float_as_uint(f0) >> 16) | (__float_as_uint(f1) & 0xFFFF0000u);
+    hi = (__float_as_uint(f2) >> 16) | (__float_as_uint(f3) & 0xFFFF0000u);
+}
+
+template <int D, int FMT>
 __global__ void __launch_bounds__(THREADS, 1)
     batch_ctx_attn_kernel(const __grid_constant__ CUtensorMap map_k, const __grid_constant__ CUtensorMap map_v,
+                          const __grid_constant__ CUtensorMap map_ks, const __grid_constant__ CUtensorMap map_vs,
                           BatchCtxAttn a) {
     static_assert(D == 64, "batched context attention: head_dim 64");
-    using C = Cfg<D>;
+    static_assert(FMT == 16 || FMT == 8, "batched context attention: bf16 or int8 context");
+    using C = Cfg<D, FMT>;
+    constexpr bool Q8 = FMT == 8;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sQ = smem;                                   // hi, lo
-    uint8_t* sKV = sQ + 2 * C::Q_BYTES;                   // STAGES x (K, V)
-    uint8_t* sP = sKV + STAGES * C::STAGE_BYTES;          // hi (2 panels), lo (2 panels)
-    uint64_t* bars = (uint64_t*)(sP + 2 * C::P_BYTES);
-    uint64_t* full = bars;                 // [STAGES] TMA -> MMA
-    uint64_t* empty = bars + STAGES;       // [STAGES] MMA -> TMA
+    uint8_t* sP = sQ + 2 * C::Q_BYTES;                    // hi (2 panels), lo (2 panels)
+    uint8_t* sX = sP + 2 * C::P_BYTES;                    // int8: 2 x {K bf16, V bf16, ks, vs}
+    uint8_t* sKV = sX + C::NXBUF * C::XBUF_BYTES;         // STAGES x TMA stage
+    uint64_t* bars = (uint64_t*)(sKV + STAGES * C::STAGE_BYTES);
+    uint64_t* full = bars;                 // [STAGES] TMA -> MMA (bf16) / expanders (int8)
+    uint64_t* empty = bars + STAGES;       // [STAGES] MMA (bf16) / expanders (int8) -> TMA
     uint64_t* qready = bars + 2 * STAGES;  // softmax warps -> MMA (Q staged), count 4
     uint64_t* sfull = qready + 1;          // MMA -> softmax (S in TMEM)
     uint64_t* sfree = sfull + 1;           // softmax -> MMA (S read), count 4
     uint64_t* pready = sfree + 1;          // softmax -> MMA (P staged), count 4
     uint64_t* ofull = pready + 1;          // MMA -> softmax (O chunk in TMEM)
-    uint32_t* tmem_slot = (uint32_t*)(ofull + 1);
+    uint64_t* xready = ofull + 1;          // [2] expanders -> MMA + softmax, count 2
+    uint64_t* xfree = xready + 2;          // [2] MMA -> expanders
+    uint32_t* tmem_slot = (uint32_t*)(xfree + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int hd = blockIdx.x, split = blockIdx.y, bt = blockIdx.z;
@@ -235,13 +252,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_v) : "memory");
         for (int i = 0; i < STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], 1);
+            mbar_init(&empty[i], Q8 ? 2 : 1);
         }
         mbar_init(qready, 4);
         mbar_init(sfull, 1);
         mbar_init(sfree, 4);
         mbar_init(pready, 4);
         mbar_init(ofull, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&xready[i], 2);
+            mbar_init(&xfree[i], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc(tmem_slot, 256);
@@ -260,8 +281,15 @@ __global__ void __launch_bounds__(THREADS, 1)
                 mbar_expect_tx(&full[stage], C::STAGE_BYTES);
                 uint8_t* s = sKV + stage * C::STAGE_BYTES;
                 const int row = hd * a.S + c * CH;
-                tma_load_2d(&map_k, &full[stage], s, 0, row);
-                tma_load_2d(&map_v, &full[stage], s + C::KV_BYTES, 0, row);
+                if constexpr (Q8) {
+                    tma_load_2d(&map_k, &full[stage], s, 0, row);
+                    tma_load_2d(&map_v, &full[stage], s + C::CODE_BYTES, 0, row);
+                    tma_load_1d(&map_ks, &full[stage], s + 2 * C::CODE_BYTES, row);
+                    tma_load_1d(&map_vs, &full[stage], s + 2 * C::CODE_BYTES + CH * 4, row);
+                } else {
+                    tma_load_2d(&map_k, &full[stage], s, 0, row);
+                    tma_load_2d(&map_v, &full[stage], s + C::KV_BYTES, 0, row);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -279,10 +307,16 @@ __global__ void __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int i = 0; i < nloc; ++i) {
-                mbar_wait(&full[stage], phase);
+                uint32_t kb;
+                if constexpr (Q8) {
+                    mbar_wait(&xready[i & 1], (i >> 1) & 1);
+                    kb = smem_u32(sX + (i & 1) * C::XBUF_BYTES);
+                } else {
+                    mbar_wait(&full[stage], phase);
+                    kb = smem_u32(sKV + stage * C::STAGE_BYTES);
+                }
                 mbar_wait(sfree, (i & 1) ^ 1);  // S of the previous chunk consumed
                 fence_after();
-                const uint32_t kb = smem_u32(sKV + stage * C::STAGE_BYTES);
                 const uint32_t vb = kb + C::KV_BYTES;
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
@@ -303,14 +337,61 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mma_bf16(tO, desc_sw128(p1 + poff), vd, idO, 1);
                 }
                 mma_commit(ofull);
-                mma_commit(&empty[stage]);
+                if constexpr (Q8) {
+                    mma_commit(&xfree[i & 1]);
+                } else {
+                    mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp < 4) {
+        if constexpr (Q8) {
+            // expand int8 codes to bf16 K-major / MN-major SW128 tiles (identical physical layout)
+            const int t = threadIdx.x - 64;  // 0..63
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < nloc; ++i) {
+                mbar_wait(&full[stage], phase);
+                mbar_wait(&xfree[i & 1], ((i >> 1) & 1) ^ 1);
+                const uint8_t* s = sKV + stage * C::STAGE_BYTES;
+                uint8_t* x = sX + (i & 1) * C::XBUF_BYTES;
+                const uint32_t xb = smem_u32(x);
+#pragma unroll 4
+                for (int u = t; u < 2 * CH * (D / 16); u += 64) {
+                    const int kv = u / (CH * (D / 16));
+                    const int rem = u - kv * (CH * (D / 16));
+                    const int r = rem / (D / 16), q = rem - r * (D / 16);
+                    const uint4 w = *reinterpret_cast<const uint4*>(s + kv * C::CODE_BYTES + r * D + q * 16);
+                    uint32_t e[8];
+                    i8x4_to_bf16x4(w.x, e[0], e[1]);
+                    i8x4_to_bf16x4(w.y, e[2], e[3]);
+                    i8x4_to_bf16x4(w.z, e[4], e[5]);
+                    i8x4_to_bf16x4(w.w, e[6], e[7]);
+                    const uint32_t base = xb + kv * C::KV_BYTES;
+                    st_shared_v4(base + sw128_off(r, 2 * q), e[0], e[1], e[2], e[3]);
+                    st_shared_v4(base + sw128_off(r, 2 * q + 1), e[4], e[5], e[6], e[7]);
+                }
+                // row scales (K then V)
+                for (int u = t; u < 2 * CH / 4; u += 64)
+                    reinterpret_cast<uint4*>(x + 2 * C::KV_BYTES)[u] =
+                        reinterpret_cast<const uint4*>(s + 2 * C::CODE_BYTES)[u];
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&empty[stage]);
+                    mbar_arrive(&xready[i & 1]);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else {
         const int quad = warp - 4;
         const int r = quad * 32 + lane;             // session row of this CTA's tile
         const int b = bt * BT + r;
@@ -349,6 +430,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < nloc; ++i) {
             const int cbase = (c0 + i) * CH;
             const int valid = min(CH, a.S - cbase);
+            const float* ksc = nullptr;
+            const float* vsc = nullptr;
+            if constexpr (Q8) {
+                mbar_wait(&xready[i & 1], (i >> 1) & 1);
+                ksc = reinterpret_cast<const float*>(sX + (i & 1) * C::XBUF_BYTES + 2 * C::KV_BYTES);
+                vsc = ksc + CH;
+            }
             mbar_wait(sfull, i & 1);
             fence_after();
             float s[CH];
@@ -360,6 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             float mx = m;
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
+                if constexpr (Q8) s[j] *= ksc[j];  // scores of dequantised K = scale * (q . code)
                 if (j >= valid) s[j] = -INFINITY;
                 mx = fmaxf(mx, s[j]);
             }
@@ -372,7 +461,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int e = 0; e < 8; ++e) {
                     const float p = (c * 8 + e < valid) ? __expf(s[c * 8 + e] - mx) : 0.0f;
                     rs += p;
-                    split_bf16(p, hi[e], lo[e]);
+                    // O = sum p * (code * vscale): fold the V row scale into P
+                    const float pv = Q8 ? p * vsc[c * 8 + e] : p;
+                    split_bf16(pv, hi[e], lo[e]);
                 }
                 const uint32_t off = (c >> 3) * (BT * 128) + sw128_off(r, c & 7);
                 st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
@@ -599,21 +690,30 @@ int batch_ctx_splits(int S, int H, int B, int num_sms) {
     return ns;
 }
 
-bool batch_ctx_supported(int D, int fmt) { return D == 64 && fmt == EKV_KV_BF16; }
+bool batch_ctx_supported(int D, int fmt, int group) {
+    return D == 64 && (fmt == EKV_KV_BF16 || (fmt == EKV_KV_INT8 && group == D));
+}
 
-void launch_batch_ctx_attn(const CUtensorMap& map_k, const CUtensorMap& map_v, const BatchCtxAttn& a,
-                           cudaStream_t st) {
+template <int FMT>
+static void launch_ctx(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaStream_t st) {
     using namespace k10;
-    require(a.D == 64, "batched context attention supports head_dim 64", EKV_EUNSUPPORTED);
-    using Cf = Cfg<64>;
+    using Cf = Cfg<64, FMT>;
     static bool attr = false;
     if (!attr) {
-        EKV_CUDA(cudaFuncSetAttribute(batch_ctx_attn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Cf::SMEM));
+        EKV_CUDA(cudaFuncSetAttribute(batch_ctx_attn_kernel<64, FMT>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
         attr = true;
     }
     dim3 grid(a.H, a.nsplit, (a.B + BT - 1) / BT);
-    batch_ctx_attn_kernel<64><<<grid, THREADS, Cf::SMEM, st>>>(map_k, map_v, a);
+    batch_ctx_attn_kernel<64, FMT><<<grid, THREADS, Cf::SMEM, st>>>(mp.k, mp.v, mp.ks, mp.vs, a);
+}
+
+void launch_batch_ctx_attn(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaStream_t st) {
+    require(a.D == 64, "batched context attention supports head_dim 64", EKV_EUNSUPPORTED);
+    if (mp.fmt == EKV_KV_BF16)
+        launch_ctx<16>(mp, a, st);
+    else
+        launch_ctx<8>(mp, a, st);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }

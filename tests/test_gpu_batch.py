@@ -45,16 +45,19 @@ def check_sessions(oracle, f64, ck, cv, ue, pre, steps, which):
     return worst
 
 
-@pytest.mark.parametrize("B,L,H,S,U,T", [(5, 2, 4, 320, 3, 4),     # ragged last chunk
-                                         (3, 2, 4, 0, 2, 3),        # empty context (s = 0 bypass)
-                                         (8, 3, 4, 128, 0, 3),      # no user prompt
-                                         (33, 1, 4, 1000, 2, 2)])   # BN = 64, many chunks
-def test_batch_matches_oracle_per_session(ek, ctx, oracle, B, L, H, S, U, T):
+@pytest.mark.parametrize("B,fmts,H,S,U,T", [(5, [16, 16], 4, 320, 3, 4),    # ragged last chunk
+                                            (5, [16, 8], 4, 320, 3, 4),     # [local bf16 | cloud int8]
+                                            (3, [16, 16], 4, 0, 2, 3),      # empty context (s = 0 bypass)
+                                            (8, [8, 16, 8], 4, 128, 0, 3),  # no user prompt
+                                            (33, [8], 4, 1000, 2, 2),       # BN = 64, many chunks
+                                            (2, [16, 8], 8, 2048, 2, 2)])   # C2 context length
+def test_batch_matches_oracle_per_session(ek, ctx, oracle, B, fmts, H, S, U, T):
+    L = len(fmts)
     d = 64
-    h, max_pos = H * d, 2048
+    h, max_pos = H * d, S + U + T + 8
     bits, f64 = host_bf16_model(oracle, L, H, d, max_pos, seed=17 + S)
     model = upload_model(ek, ctx, bits, L, H, d, max_pos)
-    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, [16] * L, seed=19 + S)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, fmts, seed=19 + S)
     batch = ek.SessionBatch(model, kvc, B, U + T)
     ue = np.stack([oracle.generate_embeddings(1000 + b, max(U, 1), h)[:U] for b in range(B)]).astype(np.float32)
     pre, steps = ek.collaborative_decode_batch(batch, ue, T)
@@ -76,7 +79,7 @@ def test_batch_two_tiles_and_single_session_agreement(ek, ctx, oracle):
     h, max_pos = H * d, 512
     bits, f64 = host_bf16_model(oracle, L, H, d, max_pos, seed=23)
     model = upload_model(ek, ctx, bits, L, H, d, max_pos)
-    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, [16] * L, seed=29)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, [8] * L, seed=29)
     batch = ek.SessionBatch(model, kvc, B, U + T)
     ue = np.stack([oracle.generate_embeddings(2000 + b, U, h) for b in range(B)]).astype(np.float32)
     pre, steps = ek.collaborative_decode_batch(batch, ue, T)
@@ -94,7 +97,7 @@ def test_batch_sessions_are_independent(ek, ctx, oracle):
     h, max_pos = H * d, 512
     bits, _ = host_bf16_model(oracle, L, H, d, max_pos, seed=31)
     model = upload_model(ek, ctx, bits, L, H, d, max_pos)
-    kvc, _, _ = make_context(ek, ctx, oracle, model, S, [16] * L, seed=37)
+    kvc, _, _ = make_context(ek, ctx, oracle, model, S, [16, 8], seed=37)
     batch = ek.SessionBatch(model, kvc, B, U + T)
     ue = np.stack([oracle.generate_embeddings(3000 + b, U, h) for b in range(B)]).astype(np.float32)
     _, s1 = ek.collaborative_decode_batch(batch, ue, T)
@@ -117,3 +120,6 @@ def test_batch_errors(ek, ctx, oracle):
     other = ek.EdgeModel(ctx, 2, 8, 32, 64)
     with pytest.raises(ek.EkvError, match="align with head pruning"):
         ek.SessionBatch(other, kvc, 2, 4)
+    kv4 = ek.AssembledContext(model, 64, [16, 4], group=32)
+    with pytest.raises(ek.EkvError, match="not supported"):
+        ek.SessionBatch(model, kv4, 2, 4)
