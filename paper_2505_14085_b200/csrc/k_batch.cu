@@ -35,6 +35,28 @@ namespace ekv {
 
 using namespace tc;
 
+constexpr int kMaxSplitK = 16;
+
+// sum of the KS split-K partials of 4 consecutive floats (16-byte aligned); every
+// load is issued before the first add (the split loop is unrolled to kMaxSplitK
+// with a predicate), so the sum costs one memory round trip, not KS.
+__device__ __forceinline__ float4 sum_splits4(const float* p, size_t stride, int KS) {
+    float4 v[kMaxSplitK];
+#pragma unroll
+    for (int s = 0; s < kMaxSplitK; ++s)
+        if (s < KS) v[s] = *reinterpret_cast<const float4*>(p + s * stride);
+    float4 r = v[0];
+#pragma unroll
+    for (int s = 1; s < kMaxSplitK; ++s)
+        if (s < KS) {
+            r.x += v[s].x;
+            r.y += v[s].y;
+            r.z += v[s].z;
+            r.w += v[s].w;
+        }
+    return r;
+}
+
 // ============================================================================
 // K9: projection GEMM  out[ks][b][n] = sum_{k in split ks} W[w_row0 + n][k] * x[b][k]
 // ============================================================================
@@ -151,25 +173,34 @@ __global__ void batch_xprep_kernel(BatchXprep a) {
     const int h = a.h;
     const DevState st = *a.state;
     const int p = a.pos_offset + st.user_len;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < h; k += gridDim.x * blockDim.x) {
-        float x;
-        if (a.mode == 0) {
-            x = a.xin[(size_t)b * h + k];
-            const float pe = __uint_as_float((uint32_t)a.pos[(size_t)p * h + k] << 16);
-            x = a.gamma[k] * (x + pe) + a.bias[k];
-        } else {
-            x = 0.0f;
-            for (int s = 0; s < a.KS; ++s) x += a.part[((size_t)s * a.B + b) * h + k];
-        }
-        if (a.mode == 2) {
-            a.hist[((size_t)st.step * a.B + b) * h + k] = x;
-            a.xin[(size_t)b * h + k] = x;
-        } else {
-            uint16_t hi, lo;
-            split_bf16(x, hi, lo);
-            a.xhl[(size_t)b * h + k] = hi;
-            a.xhl[((size_t)a.B + b) * h + k] = lo;
-        }
+    const int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (k >= h) return;
+    float4 x;
+    if (a.mode == 0) {
+        x = *reinterpret_cast<const float4*>(a.xin + (size_t)b * h + k);
+        const uint2 pw = *reinterpret_cast<const uint2*>(a.pos + (size_t)p * h + k);
+        const float4 g = *reinterpret_cast<const float4*>(a.gamma + k);
+        const float4 bb = *reinterpret_cast<const float4*>(a.bias + k);
+        x.x = g.x * (x.x + bf16_lo(pw.x)) + bb.x;
+        x.y = g.y * (x.y + bf16_hi(pw.x)) + bb.y;
+        x.z = g.z * (x.z + bf16_lo(pw.y)) + bb.z;
+        x.w = g.w * (x.w + bf16_hi(pw.y)) + bb.w;
+    } else {
+        x = sum_splits4(a.part + (size_t)b * h + k, (size_t)a.B * h, a.KS);
+    }
+    if (a.mode == 2) {
+        *reinterpret_cast<float4*>(a.hist + ((size_t)st.step * a.B + b) * h + k) = x;
+        *reinterpret_cast<float4*>(a.xin + (size_t)b * h + k) = x;
+    } else {
+        uint16_t hi[4], lo[4];
+        split_bf16(x.x, hi[0], lo[0]);
+        split_bf16(x.y, hi[1], lo[1]);
+        split_bf16(x.z, hi[2], lo[2]);
+        split_bf16(x.w, hi[3], lo[3]);
+        *reinterpret_cast<uint2*>(a.xhl + (size_t)b * h + k) =
+            make_uint2(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16));
+        *reinterpret_cast<uint2*>(a.xhl + ((size_t)a.B + b) * h + k) =
+            make_uint2(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16));
     }
 }
 
@@ -180,7 +211,8 @@ __global__ void batch_xprep_kernel(BatchXprep a) {
 namespace k10 {
 constexpr int BT = 128;        // sessions per CTA (MMA M)
 constexpr int CH = 128;        // context rows per chunk (MMA N of S = Q K^T; K of O = P V)
-constexpr int THREADS = 256;   // warp 0 TMA, 1 MMA, 2-3 TMEM alloc + int8 expansion, 4-7 softmax
+constexpr int THREADS = 384;   // warp 0 TMA, 1 MMA, 2-3 TMEM alloc + int8 expansion, 4-11 softmax
+                               // (warp w: TMEM lanes 32*(w%4).., score columns / O columns half (w-4)/4)
 constexpr int STAGES = 3;
 
 template <int D, int FMT>
@@ -195,7 +227,9 @@ struct Cfg {
     // int8: expanded bf16 K, V tiles (+ scales), double-buffered
     static constexpr int XBUF_BYTES = FMT == 16 ? 0 : 2 * KV_BYTES + 2 * CH * 4;
     static constexpr int NXBUF = FMT == 16 ? 0 : 2;
-    static constexpr int SMEM = 2 * Q_BYTES + STAGES * STAGE_BYTES + NXBUF * XBUF_BYTES + 2 * P_BYTES + 1024 + 512;
+    static constexpr int XCH_BYTES = 2 * 2 * BT * 4 + 2 * BT * 4;  // row-max exchange (2 parities) + l exchange
+    static constexpr int SMEM = 2 * Q_BYTES + STAGES * STAGE_BYTES + NXBUF * XBUF_BYTES + 2 * P_BYTES + XCH_BYTES +
+                                1024 + 512;
 };
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -228,7 +262,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint8_t* sP = sQ + 2 * C::Q_BYTES;                    // hi (2 panels), lo (2 panels)
     uint8_t* sX = sP + 2 * C::P_BYTES;                    // int8: 2 x {K bf16, V bf16, ks, vs}
     uint8_t* sKV = sX + C::NXBUF * C::XBUF_BYTES;         // STAGES x TMA stage
-    uint64_t* bars = (uint64_t*)(sKV + STAGES * C::STAGE_BYTES);
+    float* xch = (float*)(sKV + STAGES * C::STAGE_BYTES);  // [2][2][BT] row max, [2][BT] row sum
+    uint64_t* bars = (uint64_t*)(xch + 6 * BT);
     uint64_t* full = bars;                 // [STAGES] TMA -> MMA (bf16) / expanders (int8)
     uint64_t* empty = bars + STAGES;       // [STAGES] MMA (bf16) / expanders (int8) -> TMA
     uint64_t* qready = bars + 2 * STAGES;  // softmax warps -> MMA (Q staged), count 4
@@ -254,10 +289,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], Q8 ? 2 : 1);
         }
-        mbar_init(qready, 4);
+        mbar_init(qready, 8);
         mbar_init(sfull, 1);
-        mbar_init(sfree, 4);
-        mbar_init(pready, 4);
+        mbar_init(sfree, 8);
+        mbar_init(pready, 8);
         mbar_init(ofull, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&xready[i], 2);
@@ -392,108 +427,163 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        const int quad = warp - 4;
+        const int quad = warp & 3;                  // TMEM lane quadrant of this warp
+        const int half = (warp - 4) >> 2;           // score columns [64h, 64h+64), O columns [32h, 32h+32)
         const int r = quad * 32 + lane;             // session row of this CTA's tile
         const int b = bt * BT + r;
         const bool live = b < a.B;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-        // ---- stage q (sum of the split-K partials of the QKV projection) as hi / lo ----
+        const int pair_bar = 1 + quad;              // named barrier of warps quad+4 and quad+8
+        // ---- stage q (sum of the split-K partials of the QKV projection) as hi / lo:
+        //      256 threads, coalesced 16-byte loads, 4 rows' loads in flight per thread ----
         {
             const uint32_t qh = smem_u32(sQ), ql = qh + C::Q_BYTES;
+            const int t = threadIdx.x - 128;
+            const size_t stride = (size_t)a.B * a.n_qkv;
+            constexpr int NU = BT * (D / 4) / 256;  // float4 units per thread (8)
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
-                uint16_t hi[8], lo[8];
+            for (int g = 0; g < NU / 4; ++g) {
+                float4 v[4][4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    float x = 0.0f;
-                    if (live) {
-                        const float* qp = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8 + e;
-                        for (int s = 0; s < a.KS; ++s) x += qp[(size_t)s * a.B * a.n_qkv];
-                    }
-                    split_bf16(x, hi[e], lo[e]);
+                for (int k = 0; k < 4; ++k) {
+                    const int u = t + (g * 4 + k) * 256;
+                    const int row = u / (D / 4), c4 = u - row * (D / 4);
+                    const int bb = bt * BT + row;
+                    const float* src = a.qkv + (size_t)bb * a.n_qkv + hd * D + c4 * 4;
+#pragma unroll
+                    for (int s2 = 0; s2 < 4; ++s2)
+                        v[k][s2] = (bb < a.B && s2 < a.KS) ? *reinterpret_cast<const float4*>(src + s2 * stride)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
-                const uint32_t off = sw128_off(r, c);
-                st_shared_v4(qh + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
-                             pack2(hi[6], hi[7]));
-                st_shared_v4(ql + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
-                             pack2(lo[6], lo[7]));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int u = t + (g * 4 + k) * 256;
+                    const int row = u / (D / 4), c4 = u - row * (D / 4);
+                    const int bb = bt * BT + row;
+                    float4 x = v[k][0];
+#pragma unroll
+                    for (int s2 = 1; s2 < 4; ++s2) {
+                        x.x += v[k][s2].x; x.y += v[k][s2].y; x.z += v[k][s2].z; x.w += v[k][s2].w;
+                    }
+                    for (int s2 = 4; s2 < a.KS && bb < a.B; ++s2) {  // rare: more than 4 splits
+                        const float4 y = *reinterpret_cast<const float4*>(
+                            a.qkv + (size_t)bb * a.n_qkv + hd * D + c4 * 4 + s2 * stride);
+                        x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+                    }
+                    uint16_t hi[4], lo[4];
+                    split_bf16(x.x, hi[0], lo[0]);
+                    split_bf16(x.y, hi[1], lo[1]);
+                    split_bf16(x.z, hi[2], lo[2]);
+                    split_bf16(x.w, hi[3], lo[3]);
+                    const uint32_t off = sw128_off(row, c4 >> 1) + (c4 & 1) * 8;
+                    asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(qh + off), "r"(pack2(hi[0], hi[1])),
+                                 "r"(pack2(hi[2], hi[3])) : "memory");
+                    asm volatile("st.shared.v2.b32 [%0], {%1,%2};" ::"r"(ql + off), "r"(pack2(lo[0], lo[1])),
+                                 "r"(pack2(lo[2], lo[3])) : "memory");
+                }
             }
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(qready);
         }
+        constexpr float L2E = 1.4426950408889634f;
         float m = -INFINITY, l = 0.0f;
-        float o[D];
+        float o[32];
 #pragma unroll
-        for (int i = 0; i < D; ++i) o[i] = 0.0f;
-        const uint32_t ph = smem_u32(sP), pl = ph + C::P_BYTES;
+        for (int i = 0; i < 32; ++i) o[i] = 0.0f;
+        const uint32_t ph = smem_u32(sP) + half * (BT * 128), pl = ph + C::P_BYTES;
         for (int i = 0; i < nloc; ++i) {
-            const int cbase = (c0 + i) * CH;
-            const int valid = min(CH, a.S - cbase);
+            const int cbase = (c0 + i) * CH + half * 64;
+            const int valid = min(64, a.S - cbase);  // may be <= 0 for the last chunk's upper half
             const float* ksc = nullptr;
             const float* vsc = nullptr;
             if constexpr (Q8) {
                 mbar_wait(&xready[i & 1], (i >> 1) & 1);
-                ksc = reinterpret_cast<const float*>(sX + (i & 1) * C::XBUF_BYTES + 2 * C::KV_BYTES);
+                ksc = reinterpret_cast<const float*>(sX + (i & 1) * C::XBUF_BYTES + 2 * C::KV_BYTES) + half * 64;
                 vsc = ksc + CH;
             }
             mbar_wait(sfull, i & 1);
             fence_after();
-            float s[CH];
+            // pass 1: row max over this warp's 64 columns, exchanged with the partner warp
+            float mx = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < CH / 32; ++c) tmem_ld32(tS + lane_off + c * 32, s + c * 32);
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(sfree);
-            float mx = m;
+            for (int c = 0; c < 2; ++c) {
+                float sv[32];
+                tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
 #pragma unroll
-            for (int j = 0; j < CH; ++j) {
-                if constexpr (Q8) s[j] *= ksc[j];  // scores of dequantised K = scale * (q . code)
-                if (j >= valid) s[j] = -INFINITY;
-                mx = fmaxf(mx, s[j]);
+                for (int e = 0; e < 32; ++e) {
+                    float x = sv[e];
+                    if constexpr (Q8) x *= ksc[c * 32 + e];  // scores of dequantised K = scale * (q . code)
+                    if (c * 32 + e < valid) mx = fmaxf(mx, x);
+                }
             }
-            const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
+            float* xm = xch + (i & 1) * 2 * BT;
+            xm[half * BT + r] = mx;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            mx = fmaxf(fmaxf(mx, xm[(half ^ 1) * BT + r]), m);
+            const float alpha = (m == -INFINITY) ? 0.0f : exp2f((m - mx) * L2E);
+            const float mxs = mx * L2E;
+            // pass 2: p = exp(s - max), P (times the V row scale for int8) as hi / lo bf16
             float rs = 0.0f;
 #pragma unroll
-            for (int c = 0; c < CH / 8; ++c) {
-                uint16_t hi[8], lo[8];
+            for (int c = 0; c < 2; ++c) {
+                float sv[32];
+                tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float p = (c * 8 + e < valid) ? __expf(s[c * 8 + e] - mx) : 0.0f;
-                    rs += p;
-                    // O = sum p * (code * vscale): fold the V row scale into P
-                    const float pv = Q8 ? p * vsc[c * 8 + e] : p;
-                    split_bf16(pv, hi[e], lo[e]);
+                for (int g = 0; g < 4; ++g) {
+                    uint16_t hi[8], lo[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int j = c * 32 + g * 8 + e;
+                        float x = sv[g * 8 + e];
+                        if constexpr (Q8) x *= ksc[j];
+                        float p;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"(fmaf(x, L2E, -mxs)));
+                        p = (j < valid) ? p : 0.0f;
+                        rs += p;
+                        // O = sum p * (code * vscale): fold the V row scale into P
+                        const float pv = Q8 ? p * vsc[j] : p;
+                        split_bf16(pv, hi[e], lo[e]);
+                    }
+                    const int cc = c * 4 + g;  // 16-byte chunk of this warp's 64-row P panel
+                    const uint32_t off = sw128_off(r, cc);
+                    st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
+                                 pack2(hi[6], hi[7]));
+                    st_shared_v4(pl + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
+                                 pack2(lo[6], lo[7]));
                 }
-                const uint32_t off = (c >> 3) * (BT * 128) + sw128_off(r, c & 7);
-                st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
-                             pack2(hi[6], hi[7]));
-                st_shared_v4(pl + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
-                             pack2(lo[6], lo[7]));
             }
             m = mx;
             l = l * alpha + rs;
             fence_async_smem();
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(pready);
+            if (lane == 0) {
+                mbar_arrive(sfree);
+                mbar_arrive(pready);
+            }
             mbar_wait(ofull, i & 1);
             fence_after();
-#pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
+            {
                 float v[32];
-                tmem_ld32(tO + lane_off + c * 32, v);
+                tmem_ld32(tO + lane_off + half * 32, v);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha + v[e];
+                for (int e = 0; e < 32; ++e) o[e] = o[e] * alpha + v[e];
             }
             fence_before();
         }
+        // row sum = both halves' partial sums (same running max in both warps)
+        float* xl = xch + 4 * BT;
+        xl[half * BT + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
         if (live) {
             float* w = a.part + (((size_t)b * a.H + hd) * a.nsplit + split) * (D + 2);
-            w[0] = m;
-            w[1] = l;
+            if (half == 0) {
+                w[0] = m;
+                w[1] = l + xl[BT + r];
+            }
 #pragma unroll
-            for (int e = 0; e < D; ++e) w[2 + e] = o[e];
+            for (int e = 0; e < 32; ++e) w[2 + half * 32 + e] = o[e];
         }
     }
     fence_before();
@@ -515,21 +605,37 @@ __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a)
     const int b = item / a.H, hd = item - b * a.H;
     const int h = a.H * D;
     const int ulen = a.state->user_len;
-    // this step's q, k, v: sum of the split-K partials
+    // this step's q, k, v: sum of the split-K partials (all loads in flight)
     float q[E], kc[E], vc[E];
+    {
+        const size_t stride = (size_t)a.B * a.n_qkv;
+        const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + lane * E;
+        float xs[3][E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int n = hd * D + lane * E + e;
-        float x0 = 0.0f, x1 = 0.0f, x2 = 0.0f;
-        for (int s = 0; s < a.KS; ++s) {
-            const float* p = a.qkv + ((size_t)s * a.B + b) * a.n_qkv;
-            x0 += p[n];
-            x1 += p[h + n];
-            x2 += p[2 * h + n];
+        for (int t = 0; t < 3; ++t)
+#pragma unroll
+            for (int e = 0; e < E; ++e) xs[t][e] = 0.0f;
+        float v[kMaxSplitK][3][E];
+#pragma unroll
+        for (int s = 0; s < kMaxSplitK; ++s)
+            if (s < a.KS)
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) v[s][t][e] = p0[s * stride + t * h + e];
+#pragma unroll
+        for (int s = 0; s < kMaxSplitK; ++s)
+            if (s < a.KS)
+#pragma unroll
+                for (int t = 0; t < 3; ++t)
+#pragma unroll
+                    for (int e = 0; e < E; ++e) xs[t][e] += v[s][t][e];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            q[e] = xs[0][e];
+            kc[e] = __bfloat162float(__float2bfloat16_rn(xs[1][e]));
+            vc[e] = __bfloat162float(__float2bfloat16_rn(xs[2][e]));
         }
-        q[e] = x0;
-        kc[e] = __bfloat162float(__float2bfloat16_rn(x1));
-        vc[e] = __bfloat162float(__float2bfloat16_rn(x2));
     }
     // append (cache_merge.cpp:189-199): row ulen of this session's user cache
     const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
@@ -647,7 +753,7 @@ int batch_proj_splits(int N_out, int K, int B, int num_sms) {
     const int kblocks = K / k9::BK;
     if (ks < 1) ks = 1;
     if (ks > kblocks) ks = kblocks;
-    if (ks > 16) ks = 16;
+    if (ks > kMaxSplitK) ks = kMaxSplitK;
     return ks;
 }
 
@@ -674,8 +780,8 @@ void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, c
 }
 
 void launch_batch_xprep(const BatchXprep& a, cudaStream_t st) {
-    dim3 grid((a.h + 255) / 256, a.B);
-    batch_xprep_kernel<<<grid, 256, 0, st>>>(a);
+    dim3 grid((a.h / 4 + 127) / 128, a.B);
+    batch_xprep_kernel<<<grid, 128, 0, st>>>(a);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }
@@ -684,7 +790,7 @@ int batch_ctx_splits(int S, int H, int B, int num_sms) {
     if (S <= 0) return 0;
     const int nchunks = (S + k10::CH - 1) / k10::CH;
     const int nbt = (B + k10::BT - 1) / k10::BT;
-    int ns = (num_sms + H * nbt - 1) / (H * nbt);
+    int ns = num_sms / (H * nbt);  // one wave: CTAs <= SMs (one CTA per SM)
     if (ns > nchunks) ns = nchunks;
     if (ns < 1) ns = 1;
     return ns;

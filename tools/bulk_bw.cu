@@ -4,6 +4,7 @@
 // given stage size / ring depth (design input for k_decode_mega.cu).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o bulk_bw tools/bulk_bw.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -72,8 +73,22 @@ void run(const uint8_t* src, size_t total, float* sink, int sms) {
            (double)per * sms * it / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
-int main() {
+int main(int argc, char** argv) {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (argc > 1) {  // aggregate bandwidth of only G streaming CTAs (one per SM)
+        const size_t total = (size_t)2 << 30;
+        uint8_t* src; float* sink;
+        cudaMalloc(&src, total); cudaMalloc(&sink, 4);
+        cudaMemset(src, 1, total);
+        for (int i = 1; i < argc; ++i) {
+            const int g = atoi(argv[i]);
+            printf("G=%d ", g);
+            run<16384, 12, 4>(src, total, sink, g);
+            printf("G=%d ", g);
+            run<32768, 6, 2>(src, total, sink, g);
+        }
+        return 0;
+    }
     const size_t total = (size_t)2 << 30;
     uint8_t* src; float* sink;
     cudaMalloc(&src, total); cudaMalloc(&sink, 4);
