@@ -427,6 +427,43 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), device="cuda")
     e2e_tok_s = world * e2e_calls * T_E2E / (e2e_ms * 1e-3)
 
+    # --- C3 (BASELINE configs[2]): B concurrent sessions per GPU over the shared context ---
+    conc = None
+    if not args.no_concurrency:
+        try:
+            Bc, Kc, Wc = args.sessions, 20, 3
+            capc = U + Wc + Kc + 2
+            batch = ek.SessionBatch(model, kvc, Bc, capc)
+            emb_c = torch.empty((Bc, U, h), dtype=torch.float32, device="cuda").uniform_(-1, 1)
+            batch.forward(emb_c)
+            batch.decode(Wc)
+            out_c = torch.empty((Kc, Bc, h), dtype=torch.float32, device="cuda")
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(st):
+                torch.cuda._sleep(200_000)
+            e0.record(st)
+            batch.decode(Kc, out_c, sync=False)
+            e1.record(st)
+            st.synchronize()
+            c_ms = max_over_ranks(e0.elapsed_time(e1), device="cuda")
+            rows_att = U + Wc + Kc / 2.0
+            c_bytes = L * (b_qkv + b_out) + (L - DEEP) * b_att_local + DEEP * b_att_deep + \
+                Bc * L * 2 * H * rows_att * d * 2
+            c_step_s = c_ms / Kc * 1e-3
+            conc = {"config": f"C3: {Bc} concurrent sessions per GPU ({Bc * world} total) sharing the "
+                              f"S={S} context, {U} user rows each, lock-step decode (ekv_batch_*)",
+                    "sessions_per_gpu": Bc, "value": world * Bc * Kc / (c_ms * 1e-3), "unit": "tok/s",
+                    "ms_per_step": c_ms / Kc, "steps": Kc, "warmup": Wc,
+                    "bytes_per_step": c_bytes, "achieved_gbs": c_bytes / c_step_s / 1e9,
+                    "frac": c_bytes / c_step_s / 1e9 / hbm,
+                    "outputs_finite": bool(torch.isfinite(out_c).all().item()),
+                    "splits": batch.info()}
+            del batch, emb_c, out_c
+        except Exception as e:  # noqa: BLE001
+            conc = {"error": str(e)[:300]}
+
     # --- CPU baseline (rank 0, N=1 only) ---
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -458,6 +495,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "align_compress": align,
+            "concurrency": conc,
             "kv_transfer": kv_transfer,
             "outputs_finite": finite,
         }
@@ -472,6 +510,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sessions", type=int, default=128, help="C3 sessions per GPU (batched path)")
+    ap.add_argument("--no-concurrency", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -324,6 +324,13 @@ int ekv_batch_info(ekv_batch_t b, int* sessions, int* rows, int* splits);
 int ekv_batch_forward(ekv_batch_t b, const float* emb_dev, int n, float* out_dev);
 /* `steps` decode steps of every session; out_dev (may be NULL) fp32 [steps][B][h]. */
 int ekv_batch_decode(ekv_batch_t b, int steps, float* out_dev);
+/* One real forward row of every session launched kernel by kernel with CUDA
+ * events in between (diagnostics / roofline attribution; advances the batch).
+ * kernel_ms[0] = layer-0 input transform; layer l: [1+5l] QKV projection,
+ * [2+5l] context attention (0 if the layer has no context), [3+5l] user
+ * segment + merge, [4+5l] output projection, [5+5l] split-K sum;
+ * [5L+1] = state advance.  Needs capacity >= 5L + 2. */
+int ekv_batch_profile_row(ekv_batch_t b, float* kernel_ms, int capacity, int* n_kernels);
 /* collaborative_decode of all B sessions with HOST buffers, synchronous:
  * user_emb fp32 [B][U][h]; prefill_out [U][B][h] (may be NULL);
  * step_out [steps][B][h].  Same errors as ekv_collaborative_decode. */

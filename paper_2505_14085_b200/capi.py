@@ -94,6 +94,7 @@ PROTOS = {
     "ekv_batch_info": [_vp, _ip, _ip, _ip],
     "ekv_batch_forward": [_vp, _vp, _i, _vp],
     "ekv_batch_decode": [_vp, _i, _vp],
+    "ekv_batch_profile_row": [_vp, _fp, _i, _ip],
     "ekv_collaborative_decode_batch": [_vp, _vp, _i, _i, _vp, _vp],
     "ekv_collaborative_decode": [_vp, _vp, _i, _i, _vp, _vp],
     "ekv_cache_source": [_i, _d, _d, _i, _i, _ip],

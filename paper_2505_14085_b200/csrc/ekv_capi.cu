@@ -434,7 +434,7 @@ struct ekv_batch_s {
     uint16_t* xhl = nullptr;  // [2][B][h]
     float* qkv = nullptr;     // [KSq][B][3h]
     float* xpart = nullptr;   // [KSo][B][h]
-    float* part = nullptr;    // [B][H][nsplit][D+2]
+    float* part = nullptr;    // [B][H][nsplit][D+4]: m, l, -, -, o[D]
     DevState* state = nullptr;
     CUtensorMap map_w{}, map_x{};
     std::vector<BatchCtxMaps> maps;   // per context layer
@@ -445,7 +445,14 @@ struct ekv_batch_s {
 
 namespace {
 
-void batch_row(ekv_batch_s* b, cudaStream_t st) {
+// one forward row of every session; ev (optional) gets 1 + 5L + 2 events:
+// [xprep0 | per layer: qkv, ctx, user, out, xprep | advance]
+void batch_row(ekv_batch_s* b, cudaStream_t st, cudaEvent_t* ev = nullptr) {
+    int ei = 0;
+    auto mark = [&] {
+        if (ev) EKV_CUDA(cudaEventRecord(ev[ei++], st));
+    };
+    mark();
     ekv_model_s* m = b->model;
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = d_of(m), h = m->h, B = b->B;
     BatchXprep x0{};
@@ -460,8 +467,10 @@ void batch_row(ekv_batch_s* b, cudaStream_t st) {
     x0.state = b->state;
     x0.xhl = b->xhl;
     launch_batch_xprep(x0, st);
+    mark();
     for (int l = 0; l < L; ++l) {
         launch_batch_proj(b->map_w, l * 4 * h, 3 * h, h, b->map_x, B, b->KSq, b->qkv, st);
+        mark();
         const ekv_segment& sg = b->kv->seg[l];
         const int ns = sg.S > 0 ? b->nsplit : 0;
         if (ns > 0) {
@@ -477,6 +486,7 @@ void batch_row(ekv_batch_s* b, cudaStream_t st) {
             a.part = b->part;
             launch_batch_ctx_attn(b->maps[l], a, st);
         }
+        mark();
         BatchUserMerge u{};
         u.B = B;
         u.H = H;
@@ -494,7 +504,9 @@ void batch_row(ekv_batch_s* b, cudaStream_t st) {
         u.state = b->state;
         u.xhl = b->xhl;
         launch_batch_user_merge(u, st);
+        mark();
         launch_batch_proj(b->map_w, l * 4 * h + 3 * h, h, h, b->map_x, B, b->KSo, b->xpart, st);
+        mark();
         BatchXprep xp{};
         xp.mode = (l == L - 1) ? 2 : 1;
         xp.B = B;
@@ -506,8 +518,10 @@ void batch_row(ekv_batch_s* b, cudaStream_t st) {
         xp.state = b->state;
         xp.xhl = b->xhl;
         launch_batch_xprep(xp, st);
+        mark();
     }
     launch_advance(b->state, 1, st);
+    mark();
 }
 
 void batch_free(ekv_batch_s* b) {
@@ -532,7 +546,7 @@ void batch_alloc(ekv_batch_s* b) {
     b->xhl = dalloc<uint16_t>((size_t)2 * B * h);
     b->qkv = dalloc<float>((size_t)b->KSq * B * 3 * h);
     b->xpart = dalloc<float>((size_t)b->KSo * B * h);
-    b->part = dalloc<float>((size_t)B * H * std::max(b->nsplit, 1) * (D + 2));
+    b->part = dalloc<float>((size_t)B * H * std::max(b->nsplit, 1) * (D + 4));
     b->state = dalloc<DevState>(1);
     EKV_CUDA(cudaMemset(b->uk, 0, sizeof(uint16_t) * ukv));
     EKV_CUDA(cudaMemset(b->uv, 0, sizeof(uint16_t) * ukv));
@@ -1669,6 +1683,32 @@ int ekv_batch_decode(ekv_batch_t b, int steps, float* out_dev) {
             EKV_CUDA(cudaMemcpyAsync(out_dev, b->hist + (size_t)r0 * b->B * b->model->h,
                                      sizeof(float) * steps * b->B * b->model->h, cudaMemcpyDeviceToDevice,
                                      st));
+    });
+}
+
+int ekv_batch_profile_row(ekv_batch_t b, float* kernel_ms, int capacity, int* n_kernels) {
+    return guard([&] {
+        require(b && kernel_ms && n_kernels, "ekv_batch_profile_row: null argument");
+        const int L = b->model->cfg.num_layers;
+        const int n = 5 * L + 2;
+        require(capacity >= n, "ekv_batch_profile_row: need room for " + std::to_string(n) + " kernel times");
+        batch_check(b, 1);
+        set_dev(b->model->ctx);
+        cudaStream_t st = b->model->ctx->stream;
+        std::vector<cudaEvent_t> ev(n + 1);
+        for (auto& e : ev) EKV_CUDA(cudaEventCreate(&e));
+        try {
+            batch_row(b, st, ev.data());
+            EKV_CUDA(cudaStreamSynchronize(st));
+            for (int i = 0; i < n; ++i) EKV_CUDA(cudaEventElapsedTime(&kernel_ms[i], ev[i], ev[i + 1]));
+        } catch (...) {
+            for (auto& e : ev) cudaEventDestroy(e);
+            throw;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        b->user_len += 1;
+        b->rows += 1;
+        *n_kernels = n;
     });
 }
 

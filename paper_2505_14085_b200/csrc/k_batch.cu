@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const bool live = b < a.B;
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const int pair_bar = 1 + quad;              // named barrier of warps quad+4 and quad+8
+        const bool warp_live = bt * BT + quad * 32 < a.B;  // some session row of this warp exists
         // ---- stage q (sum of the split-K partials of the QKV projection) as hi / lo:
         //      256 threads, coalesced 16-byte loads, 4 rows' loads in flight per thread ----
         {
@@ -504,6 +505,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             mbar_wait(sfull, i & 1);
             fence_after();
+            if (!warp_live) {  // no session in these 32 rows: their P rows and O rows are never used
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(sfree);
+                    mbar_arrive(pready);
+                }
+                mbar_wait(ofull, i & 1);
+                continue;
+            }
             // pass 1: row max over this warp's 64 columns, exchanged with the partner warp
             float mx = -INFINITY;
 #pragma unroll
@@ -577,13 +587,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         xl[half * BT + r] = l;
         asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
         if (live) {
-            float* w = a.part + (((size_t)b * a.H + hd) * a.nsplit + split) * (D + 2);
-            if (half == 0) {
-                w[0] = m;
-                w[1] = l + xl[BT + r];
-            }
+            float* w = a.part + (((size_t)b * a.H + hd) * a.nsplit + split) * (D + 4);
+            if (half == 0) *reinterpret_cast<float2*>(w) = make_float2(m, l + xl[BT + r]);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) w[2 + half * 32 + e] = o[e];
+            for (int e = 0; e < 32; e += 4)
+                *reinterpret_cast<float4*>(w + 4 + half * 32 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
         }
     }
     fence_before();
@@ -598,40 +606,59 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ============================================================================
 template <int D>
 __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a) {
-    constexpr int E = D / 32;  // dims per lane
+    constexpr int G = D / 8;         // lanes per row (8 dims = 16 bytes per lane)
+    constexpr int RPI = 32 / G;      // rows per warp-wide load
+    constexpr int NT = 32 / RPI;     // rows per lane per 32-row block
     const int lane = threadIdx.x & 31;
     const int item = blockIdx.x * 4 + (threadIdx.x >> 5);
     if (item >= a.B * a.H) return;
     const int b = item / a.H, hd = item - b * a.H;
+    const int grp = lane / G, c = lane - grp * G;  // row group, 8-dim chunk
     const int h = a.H * D;
     const int ulen = a.state->user_len;
-    // this step's q, k, v: sum of the split-K partials (all loads in flight)
-    float q[E], kc[E], vc[E];
+    // this step's q, k, v (8 dims per lane): sum of the split-K partials, all loads in flight
+    float q[8], kc[8], vc[8];
     {
         const size_t stride = (size_t)a.B * a.n_qkv;
-        const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + lane * E;
-        float xs[3][E];
+        const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
+        constexpr int NV = 4;  // splits held in flight; more are summed by a plain loop
+        float4 v[NV][3][2];
 #pragma unroll
-        for (int t = 0; t < 3; ++t)
+        for (int s = 0; s < NV; ++s)
 #pragma unroll
-            for (int e = 0; e < E; ++e) xs[t][e] = 0.0f;
-        float v[kMaxSplitK][3][E];
+            for (int t = 0; t < 3; ++t) {
+                if (s < a.KS) {
+                    v[s][t][0] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h);
+                    v[s][t][1] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h + 4);
+                } else {
+                    v[s][t][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    v[s][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+        for (int s = NV; s < a.KS; ++s)
 #pragma unroll
-        for (int s = 0; s < kMaxSplitK; ++s)
-            if (s < a.KS)
+            for (int t = 0; t < 3; ++t) {
+                const float4 y0 = *reinterpret_cast<const float4*>(p0 + s * stride + t * h);
+                const float4 y1 = *reinterpret_cast<const float4*>(p0 + s * stride + t * h + 4);
+                v[0][t][0].x += y0.x; v[0][t][0].y += y0.y; v[0][t][0].z += y0.z; v[0][t][0].w += y0.w;
+                v[0][t][1].x += y1.x; v[0][t][1].y += y1.y; v[0][t][1].z += y1.z; v[0][t][1].w += y1.w;
+            }
+        float xs[3][8];
 #pragma unroll
-                for (int t = 0; t < 3; ++t)
+        for (int t = 0; t < 3; ++t) {
+            xs[t][0] = v[0][t][0].x; xs[t][1] = v[0][t][0].y; xs[t][2] = v[0][t][0].z; xs[t][3] = v[0][t][0].w;
+            xs[t][4] = v[0][t][1].x; xs[t][5] = v[0][t][1].y; xs[t][6] = v[0][t][1].z; xs[t][7] = v[0][t][1].w;
+        }
 #pragma unroll
-                    for (int e = 0; e < E; ++e) v[s][t][e] = p0[s * stride + t * h + e];
+        for (int s = 1; s < NV; ++s)
 #pragma unroll
-        for (int s = 0; s < kMaxSplitK; ++s)
-            if (s < a.KS)
+            for (int t = 0; t < 3; ++t) {
+                xs[t][0] += v[s][t][0].x; xs[t][1] += v[s][t][0].y; xs[t][2] += v[s][t][0].z;
+                xs[t][3] += v[s][t][0].w; xs[t][4] += v[s][t][1].x; xs[t][5] += v[s][t][1].y;
+                xs[t][6] += v[s][t][1].z; xs[t][7] += v[s][t][1].w;
+            }
 #pragma unroll
-                for (int t = 0; t < 3; ++t)
-#pragma unroll
-                    for (int e = 0; e < E; ++e) xs[t][e] += v[s][t][e];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
+        for (int e = 0; e < 8; ++e) {
             q[e] = xs[0][e];
             kc[e] = __bfloat162float(__float2bfloat16_rn(xs[1][e]));
             vc[e] = __bfloat162float(__float2bfloat16_rn(xs[2][e]));
@@ -641,96 +668,126 @@ __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a)
     const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
     uint16_t* uk = a.uk + head_off;
     uint16_t* uv = a.uv + head_off;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        uk[(size_t)ulen * D + lane * E + e] = f32_to_bf16_bits(kc[e]);
-        uv[(size_t)ulen * D + lane * E + e] = f32_to_bf16_bits(vc[e]);
+    if (grp == 0) {
+        uint4 kw, vw;
+        kw.x = f32_to_bf16_bits(kc[0]) | ((uint32_t)f32_to_bf16_bits(kc[1]) << 16);
+        kw.y = f32_to_bf16_bits(kc[2]) | ((uint32_t)f32_to_bf16_bits(kc[3]) << 16);
+        kw.z = f32_to_bf16_bits(kc[4]) | ((uint32_t)f32_to_bf16_bits(kc[5]) << 16);
+        kw.w = f32_to_bf16_bits(kc[6]) | ((uint32_t)f32_to_bf16_bits(kc[7]) << 16);
+        vw.x = f32_to_bf16_bits(vc[0]) | ((uint32_t)f32_to_bf16_bits(vc[1]) << 16);
+        vw.y = f32_to_bf16_bits(vc[2]) | ((uint32_t)f32_to_bf16_bits(vc[3]) << 16);
+        vw.z = f32_to_bf16_bits(vc[4]) | ((uint32_t)f32_to_bf16_bits(vc[5]) << 16);
+        vw.w = f32_to_bf16_bits(vc[6]) | ((uint32_t)f32_to_bf16_bits(vc[7]) << 16);
+        *reinterpret_cast<uint4*>(uk + (size_t)ulen * D + c * 8) = kw;
+        *reinterpret_cast<uint4*>(uv + (size_t)ulen * D + c * 8) = vw;
     }
-    // user segment over rows [0, ulen) from the cache, then the current row
-    float m = -INFINITY, l = 0.0f, o[E];
+    // user segment over rows [0, ulen) in blocks of 32 rows (NT rows per lane), then the current row
+    float m = -INFINITY, l = 0.0f, o[8];
 #pragma unroll
-    for (int e = 0; e < E; ++e) o[e] = 0.0f;
+    for (int e = 0; e < 8; ++e) o[e] = 0.0f;
     for (int j0 = 0; j0 < ulen; j0 += 32) {
-        const int nj = min(32, ulen - j0);
-        float pp[32];
+        uint4 kr[NT], vr[NT];
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
+        for (int t = 0; t < NT; ++t) {
+            const int j = j0 + grp + RPI * t;
+            if (j < ulen) {
+                kr[t] = *reinterpret_cast<const uint4*>(uk + (size_t)j * D + c * 8);
+                vr[t] = *reinterpret_cast<const uint4*>(uv + (size_t)j * D + c * 8);
+            } else {
+                kr[t] = make_uint4(0, 0, 0, 0);
+                vr[t] = make_uint4(0, 0, 0, 0);
+            }
+        }
+        float sc[NT];
+        float bm = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const uint32_t w[4] = {kr[t].x, kr[t].y, kr[t].z, kr[t].w};
             float acc = 0.0f;
-            if (jj < nj) {
-                const uint16_t* kr = uk + (size_t)(j0 + jj) * D + lane * E;
 #pragma unroll
-                for (int e = 0; e < E; ++e) acc += q[e] * __uint_as_float((uint32_t)kr[e] << 16);
-            }
-            pp[jj] = acc;
+            for (int k = 0; k < 4; ++k) acc += q[2 * k] * bf16_lo(w[k]) + q[2 * k + 1] * bf16_hi(w[k]);
+#pragma unroll
+            for (int off = G / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            const int j = j0 + grp + RPI * t;
+            sc[t] = j < ulen ? acc : -INFINITY;
+            bm = fmaxf(bm, sc[t]);
         }
-        // butterfly reduce-scatter: lane jj ends with the full dot of row j0 + jj
-#pragma unroll
-        for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
-            const bool upper = lane & off;
-#pragma unroll
-            for (int i = 0; i < n / 2; ++i) {
-                const float send = upper ? pp[i] : pp[i + n / 2];
-                const float keep = upper ? pp[i + n / 2] : pp[i];
-                pp[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-            }
-        }
-        // lane -> row mapping of the butterfly: lane L holds row bitrev-free index L
-        const float s = lane < nj ? pp[0] : -INFINITY;
-        const float mx = fmaxf(m, warp_max(s));
+        const float mx = fmaxf(m, warp_max(bm));
         const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
-        const float p = lane < nj ? __expf(s - mx) : 0.0f;
-        l = l * alpha + warp_sum(p);
+        float ps = 0.0f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) o[e] *= alpha;
-        for (int jj = 0; jj < nj; ++jj) {
-            const float pj = __shfl_sync(0xffffffffu, p, jj);
-            const uint16_t* vr = uv + (size_t)(j0 + jj) * D + lane * E;
+        for (int e = 0; e < 8; ++e) o[e] *= alpha;
 #pragma unroll
-            for (int e = 0; e < E; ++e) o[e] += pj * __uint_as_float((uint32_t)vr[e] << 16);
+        for (int t = 0; t < NT; ++t) {
+            const float p = sc[t] == -INFINITY ? 0.0f : __expf(sc[t] - mx);
+            ps += p;
+            const uint32_t w[4] = {vr[t].x, vr[t].y, vr[t].z, vr[t].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                o[2 * k] += p * bf16_lo(w[k]);
+                o[2 * k + 1] += p * bf16_hi(w[k]);
+            }
         }
+        // block row sum: one copy per row group (lanes of a group hold identical p)
+#pragma unroll
+        for (int off = G; off < 32; off <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, off);
+        l = l * alpha + ps;
         m = mx;
     }
-    {
+    // fold the row groups' partial outputs (same running max in every lane)
+#pragma unroll
+    for (int off = G; off < 32; off <<= 1)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] += __shfl_xor_sync(0xffffffffu, o[e], off);
+    {   // the current row (attends to itself, causal)
         float acc = 0.0f;
 #pragma unroll
-        for (int e = 0; e < E; ++e) acc += q[e] * kc[e];
-        const float s = warp_sum(acc);
-        const float mx = fmaxf(m, s);
+        for (int e = 0; e < 8; ++e) acc += q[e] * kc[e];
+#pragma unroll
+        for (int off = G / 2; off >= 1; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        const float mx = fmaxf(m, acc);
         const float alpha = (m == -INFINITY) ? 0.0f : __expf(m - mx);
-        const float p = __expf(s - mx);
+        const float p = __expf(acc - mx);
         l = l * alpha + p;
 #pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = o[e] * alpha + p * vc[e];
+        for (int e = 0; e < 8; ++e) o[e] = o[e] * alpha + p * vc[e];
         m = mx;
     }
     // Eq. 5 generalised: log-sum-exp merge of the user partial with the context partials
     if (a.nsplit > 0) {
-        const float* w = a.part + ((size_t)b * a.H + hd) * a.nsplit * (D + 2);
+        const float* w = a.part + ((size_t)b * a.H + hd) * a.nsplit * (D + 4);
         float M = m;
-        for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, w[s * (D + 2)]);
+        for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, w[s * (D + 4)]);
         const float fu = __expf(m - M);
-        float Lt = l * fu, ot[E];
+        float Lt = l * fu, ot[8];
 #pragma unroll
-        for (int e = 0; e < E; ++e) ot[e] = o[e] * fu;
+        for (int e = 0; e < 8; ++e) ot[e] = o[e] * fu;
         for (int s = 0; s < a.nsplit; ++s) {
-            const float* ws = w + s * (D + 2);
-            const float f = ws[0] == -INFINITY ? 0.0f : __expf(ws[0] - M);
-            Lt += ws[1] * f;
-#pragma unroll
-            for (int e = 0; e < E; ++e) ot[e] += ws[2 + lane * E + e] * f;
+            const float* ws = w + s * (D + 4);
+            const float2 ml = *reinterpret_cast<const float2*>(ws);
+            const float4 o0 = *reinterpret_cast<const float4*>(ws + 4 + c * 8);
+            const float4 o1 = *reinterpret_cast<const float4*>(ws + 8 + c * 8);
+            const float f = ml.x == -INFINITY ? 0.0f : __expf(ml.x - M);
+            Lt += ml.y * f;
+            ot[0] += o0.x * f; ot[1] += o0.y * f; ot[2] += o0.z * f; ot[3] += o0.w * f;
+            ot[4] += o1.x * f; ot[5] += o1.y * f; ot[6] += o1.z * f; ot[7] += o1.w * f;
         }
         l = Lt;
 #pragma unroll
-        for (int e = 0; e < E; ++e) o[e] = ot[e];
+        for (int e = 0; e < 8; ++e) o[e] = ot[e];
     }
-    const float inv = 1.0f / l;
+    if (grp == 0) {
+        const float inv = 1.0f / l;
+        uint16_t hi[8], lo[8];
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-        uint16_t hi, lo;
-        split_bf16(o[e] * inv, hi, lo);
-        const size_t k = (size_t)b * h + hd * D + lane * E + e;
-        a.xhl[k] = hi;
-        a.xhl[(size_t)a.B * h + k] = lo;
+        for (int e = 0; e < 8; ++e) split_bf16(o[e] * inv, hi[e], lo[e]);
+        const size_t k = (size_t)b * h + hd * D + c * 8;
+        *reinterpret_cast<uint4*>(a.xhl + k) =
+            make_uint4(hi[0] | ((uint32_t)hi[1] << 16), hi[2] | ((uint32_t)hi[3] << 16),
+                       hi[4] | ((uint32_t)hi[5] << 16), hi[6] | ((uint32_t)hi[7] << 16));
+        *reinterpret_cast<uint4*>(a.xhl + (size_t)a.B * h + k) =
+            make_uint4(lo[0] | ((uint32_t)lo[1] << 16), lo[2] | ((uint32_t)lo[3] << 16),
+                       lo[4] | ((uint32_t)lo[5] << 16), lo[6] | ((uint32_t)lo[7] << 16));
     }
 }
 

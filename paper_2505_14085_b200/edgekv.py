@@ -444,6 +444,14 @@ class SessionBatch:
         self.model.ctx.synchronize()
         return out
 
+    def profile_row(self) -> np.ndarray:
+        """One real forward row with CUDA-event times per kernel (ms), see ekv_capi.h."""
+        n = 5 * self.model.L + 2
+        out = np.zeros(n, dtype=np.float32)
+        got = C.c_int()
+        call("ekv_batch_profile_row", self.hnd, out.ctypes.data_as(C.POINTER(C.c_float)), n, C.byref(got))
+        return out[:got.value]
+
     def decode(self, steps: int, out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
         if out is None:
             out = torch.empty((steps, self.B, self.model.h), dtype=torch.float32,

@@ -11,6 +11,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 from paper_2505_14085_b200 import edgekv as ek  # noqa: E402
@@ -36,7 +37,7 @@ def main():
     st = ctx.stream
     h = H * d
     for B in [int(x) for x in a.sessions.split(",")]:
-        cap = U + a.warmup + a.steps + 2
+        cap = U + a.warmup + a.steps + 4
         model = ek.EdgeModel(ctx, L, H, d, S + cap + 8)
         model.synthesize(seed=1234)
         kvc = ek.AssembledContext(model, S, [16] * (L - DEEP) + [8] * DEEP, group=d)
@@ -58,9 +59,14 @@ def main():
         ms = e0.elapsed_time(e1) / a.steps
         rows = U + a.warmup + a.steps / 2.0
         gb = step_bytes(B, rows) / 1e9
+        prof = np.mean([batch.profile_row() for _ in range(2)], axis=0) * 1e3  # us
+        Lr = (len(prof) - 2) // 5
+        parts = {k: float(prof[1 + i:1 + 5 * Lr:5].sum()) for i, k in
+                 enumerate(["qkv_us", "ctx_us", "user_us", "out_us", "sum_us"])}
+        parts["xprep0_us"] = float(prof[0])
         print(json.dumps({"B": B, "ms_per_step": ms, "tok_s": B / ms * 1e3, "GB_per_step": gb,
                           "GB_s": gb / ms * 1e3, "finite": bool(torch.isfinite(out).all().item()),
-                          **batch.info()}), flush=True)
+                          "kernels_per_step_us": parts, **batch.info()}), flush=True)
         del batch, model, kvc
 
 
