@@ -50,7 +50,8 @@ def check_sessions(oracle, f64, ck, cv, ue, pre, steps, which):
                                             (3, [16, 16], 4, 0, 2, 3),      # empty context (s = 0 bypass)
                                             (8, [8, 16, 8], 4, 128, 0, 3),  # no user prompt
                                             (33, [8], 4, 1000, 2, 2),       # BN = 64, many chunks
-                                            (2, [16, 8], 8, 2048, 2, 2)])   # C2 context length
+                                            (2, [16, 8], 8, 2048, 2, 2),    # C2 context length
+                                            (3, [16, 8], 4, 32768, 2, 2)])  # C4 context length
 def test_batch_matches_oracle_per_session(ek, ctx, oracle, B, fmts, H, S, U, T):
     L = len(fmts)
     d = 64

@@ -174,18 +174,18 @@ def test_shared_context_two_consumers_identical(ek, ctx, oracle):
     assert np.array_equal(ra[1], rb[1]) and np.array_equal(ra[0], rb[0])
 
 
-def test_full_ce_lslm_path_config1(ek, ctx, oracle):
-    """The end-to-end composition of Artifacts (sim.cpp:100-265) at BASELINE
-    configs[0]'s shape: cloud 8L d=512 (8x64), edge 4L d=256 (8x32), S=512,
-    U=16, T=64 (decode steps checked 16 here), lambda 0.5, 2 deep layers.
+def run_full_ce_lslm_path(ek, ctx, oracle, Lc=8, Le=4, deep=2, bits=8):
+    """The end-to-end composition of Artifacts (sim.cpp:100-265): cloud Lc layers
+    d=512 (8x64), edge Le layers d=256 (8x32), S=512, U=16, T=16 decode steps,
+    lambda 0.5, `deep` deep layers compressed to `bits`-bit codes.
       1. layer map: probe prefill (oracle fp64) -> GPU-host match_layers == oracle
       2. alignment: K1 (tcgen05) + K2 norms on the bf16 cloud X_lc / W_Q / K ->
          mask == oracle select_channels on the same bf16 inputs (bit-exact)
       3. compression: K3 int8 codes of the pruned cloud KV (bit-exact)
       4. decode: collaborative_decode over [local bf16 | cloud int8] context
     """
-    Lc, Hc, dc, Le, He, de = 8, 8, 64, 4, 8, 32
-    hc, he, S, U, T, deep = Hc * dc, He * de, 512, 16, 16, 2
+    Hc, dc, He, de = 8, 64, 8, 32
+    hc, he, S, U, T = Hc * dc, He * de, 512, 16, 16
     max_pos = S + U + T
     # models (random scaled init, bf16-exact values, B200 layout)
     cbits, cf = host_bf16_model(oracle, Lc, Hc, dc, max_pos, seed=11)
@@ -230,8 +230,9 @@ def test_full_ce_lslm_path_config1(ek, ctx, oracle):
     assert kept.tolist() == want_kept.tolist()
     # 3+4. assemble [local bf16 | cloud int8] and decode
     edge = upload_model(ek, ctx, ebits, Le, He, de, max_pos)
-    fmts = [16] * boundary + [8] * deep
-    kvc = ek.AssembledContext(edge, S, fmts, group=de)
+    fmts = [16] * boundary + [bits] * deep
+    group = de if bits == 8 else 32
+    kvc = ek.AssembledContext(edge, S, fmts, group=group)
     ck = np.zeros((Le, He, S, de)); cv = np.zeros((Le, He, S, de))
     for l in range(boundary):
         kb = f32_to_bf16_bits(e_k[l].astype(np.float32)); vb = f32_to_bf16_bits(e_v[l].astype(np.float32))
@@ -241,12 +242,12 @@ def test_full_ce_lslm_path_config1(ek, ctx, oracle):
     for le, lc in deep_match.items():
         i = lcs.index(lc)
         for src, dst in ((Kd, ck), (Vd, cv)):
-            wc, ws = oracle.kv_compress(bits_of(src[i]).reshape(Hc * S, dc), want_kept, 8, de)
-            dst[le] = oracle.kv_dequant_f64(wc, ws, de, 8, de).reshape(He, S, de)
+            wc, ws = oracle.kv_compress(bits_of(src[i]).reshape(Hc * S, dc), want_kept, bits, group)
+            dst[le] = oracle.kv_dequant_f64(wc, ws, de, bits, group).reshape(He, S, de)
     sess = ek.Session(edge, kvc, U + T)
     useed = oracle.mix(42, 0x55E20000)
     ue = oracle.generate_embeddings(useed, U, he).astype(np.float32)
-    for path in ("mega", "graph"):
+    for path in (("mega", "graph") if bits == 8 else ("graph",)):
         assert sess.set_decode_path(path) == path
         pre, steps = ek.collaborative_decode(sess, ue, T)
         teacher = np.vstack([pre[-1:], steps[:-1]]).astype(np.float64)
@@ -254,3 +255,45 @@ def test_full_ce_lslm_path_config1(ek, ctx, oracle):
                                               user_kv_bf16=True)
         assert max(normwise(pre[r], wp[r]) for r in range(U)) <= TOL
         assert max(normwise(steps[t], ws_[t]) for t in range(T)) <= TOL, path
+
+
+def test_full_ce_lslm_path_config1(ek, ctx, oracle):
+    """The end-to-end composition of Artifacts (sim.cpp:100-265) at BASELINE
+    configs[0]'s shape: cloud 8L d=512 (8x64), edge 4L d=256 (8x32), S=512,
+    U=16, T=64 (decode steps checked 16 here), lambda 0.5, 2 deep layers.
+      1. layer map: probe prefill (oracle fp64) -> GPU-host match_layers == oracle
+      2. alignment: K1 (tcgen05) + K2 norms on the bf16 cloud X_lc / W_Q / K ->
+         mask == oracle select_channels on the same bf16 inputs (bit-exact)
+      3. compression: K3 int8 codes of the pruned cloud KV (bit-exact)
+      4. decode: collaborative_decode over [local bf16 | cloud int8] context
+    """
+    run_full_ce_lslm_path(ek, ctx, oracle)
+
+
+def test_long_context_32k_decode(ek, ctx, oracle):
+    """BASELINE configs[3]'s context length: S = 32768 reused rows ([local bf16 | cloud
+    int8] layers), both decode paths, against the oracle."""
+    L, H, d, S, U, T = 2, 4, 64, 32768, 4, 3
+    formats = [16, 8]
+    max_pos = S + U + T + 1
+    bits, f64 = host_bf16_model(oracle, L, H, d, max_pos, seed=71)
+    model = upload_model(ek, ctx, bits, L, H, d, max_pos)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, formats, seed=73)
+    sess = ek.Session(model, kvc, U + T)
+    ue = oracle.generate_embeddings(79, U, H * d).astype(np.float32)
+    for path in ("mega", "graph"):
+        assert sess.set_decode_path(path) == path
+        pre, steps = ek.collaborative_decode(sess, ue, T)
+        teacher = np.vstack([pre[-1:], steps[:-1]]).astype(np.float64)
+        wp, ws = oracle.collaborative_decode(f64, ck, cv, ue.astype(np.float64), T, teacher=teacher,
+                                             user_kv_bf16=True)
+        assert max(normwise(pre[r], wp[r]) for r in range(U)) <= TOL, path
+        assert max(normwise(steps[t], ws[t]) for t in range(T)) <= TOL, path
+
+
+@pytest.mark.parametrize("Lc,Le,deep,bits", [(16, 4, 2, 8), (16, 4, 2, 4), (8, 4, 2, 4)])
+def test_full_ce_lslm_path_compression_sweep(ek, ctx, oracle, Lc, Le, deep, bits):
+    """BASELINE configs[4] at reduced size: int8 vs int4 KV and cloud:edge layer ratios
+    4:1 (16 -> 4 layers) and 2:1 (8 -> 4), the whole path (layer map, mask, codes,
+    decode) against the oracle."""
+    run_full_ce_lslm_path(ek, ctx, oracle, Lc, Le, deep, bits)
