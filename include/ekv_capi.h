@@ -301,6 +301,29 @@ int ekv_session_user_kv(ekv_session_t s, int layer, void** k_dev, void** v_dev, 
 int ekv_collaborative_decode(ekv_session_t s, const float* user_emb_host, int U, int steps,
                              float* prefill_out_host, float* step_out_host);
 
+/* Eq. 20 pipelined prefill (cost_model.cpp:73-100 pipeline_schedule; the
+ * simulator's per-layer transfer/compute overlap, sim.cpp:652-683, 909-933):
+ * the context layers listed in `uploads` arrive from HOST memory (pinned, the
+ * emulated cloud->edge link) on the context's copy stream while the user rows
+ * are forwarded on the compute stream; layer l's attention waits only for
+ * layer l's upload, so upload l overlaps the compute of layers < l.
+ * uploads[L]: per layer, host K/V in the layer's storage format (bf16 [H][S][d]
+ * or codes) and fp32 scales for quantised layers; k_host == NULL = resident.
+ * overlap = 0 runs the sequential schedule (all uploads, then compute) for
+ * comparison.  Outputs: out_dev fp32 [n][h] (may be NULL), t_comm_ms[L]
+ * (upload time of each layer on the copy stream), t_comp_ms[L] (compute of each
+ * layer, measured by a kernel-by-kernel re-run with the context resident),
+ * total_ms (first upload -> last output).  Synchronous. */
+typedef struct {
+    const void* k_host;
+    const void* v_host;
+    const float* k_scales_host;
+    const float* v_scales_host;
+} ekv_layer_upload;
+int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
+                                  const ekv_layer_upload* uploads, int overlap, float* t_comm_ms,
+                                  float* t_comp_ms, float* total_ms);
+
 /* ------------------------------------------------------------------ */
 /* Batched sessions (BASELINE configs[2], concurrent edge sessions)     */
 /* ------------------------------------------------------------------ */

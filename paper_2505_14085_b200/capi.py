@@ -88,6 +88,7 @@ PROTOS = {
     "ekv_session_trace_step": [_vp, C.POINTER(C.c_uint64), _i, _ip],
     "ekv_session_profile_step": [_vp, _fp, _i, _ip],
     "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
+    "ekv_session_forward_pipelined": [_vp, _vp, _i, _vp, _vp, _i, _fp, _fp, _fp],
     "ekv_batch_create": [_vp, _vp, _i, _i, _pp],
     "ekv_batch_destroy": [_vp],
     "ekv_batch_reset": [_vp],

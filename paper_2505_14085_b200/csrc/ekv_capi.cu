@@ -67,6 +67,7 @@ struct ekv_ctx_s {
     int num_sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t capture = nullptr;  // graphs are captured here, launched on `stream`
+    cudaStream_t copy = nullptr;     // context uploads of the pipelined prefill (Eq. 20)
     bool own_stream = false;
 };
 
@@ -144,7 +145,8 @@ int d_of(const ekv_model_s* m) { return m->cfg.head_dim; }
 // cache_merge.cpp:156-226).  `in` holds the R input rows (fp32 [R][h]);
 // `out_hist`/`hist_row_dev` receive the final-layer rows.
 void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
-                   const int* hist_row_dev, cudaStream_t st, cudaEvent_t* ev = nullptr) {
+                   const int* hist_row_dev, cudaStream_t st, cudaEvent_t* ev = nullptr,
+                   const cudaEvent_t* ready = nullptr) {
     ekv_model_s* m = s->model;
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
     int ei = 0;
@@ -176,6 +178,9 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
         g.user_base_dev = &s->state->user_len;
         launch_gemv(g, st);
         mark();
+        // pipelined prefill: this layer's context must have arrived (Eq. 20: the
+        // upload of layer l overlaps the compute of layers < l)
+        if (ready && ready[l]) EKV_CUDA(cudaStreamWaitEvent(st, ready[l], 0));
 
         AttnArgs a{};
         a.R = R;
@@ -218,6 +223,81 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
     mark();
     launch_advance(s->state, R, st);
     mark();
+}
+
+// merged_forward of n user rows in LAYER-major order (every row through layer l
+// before any row enters layer l+1), rows in chunks of <= 8; positions and user
+// rows from host-side bases (base0 = user rows before the first new row).  Used by
+// the Eq. 20 pipelined prefill, where layer l may only start once its context
+// has arrived (ready[l]).  scratch: 2*n*h floats.  lev (optional): L+1 events
+// around the layers.  Results are identical to forward_chunk's.
+void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, cudaStream_t st,
+                         const cudaEvent_t* ready, float* scratch, cudaEvent_t* lev) {
+    ekv_model_s* m = s->model;
+    const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
+    float* X = scratch;               // layer outputs [n][h]
+    float* Y = scratch + (size_t)n * h;  // attention outputs [n][h]
+    for (int l = 0; l < L; ++l) {
+        if (lev) EKV_CUDA(cudaEventRecord(lev[l], st));
+        for (int r0 = 0; r0 < n; r0 += 8) {
+            const int R = std::min(8, n - r0);
+            GemvArgs g{};
+            g.N = 3 * h;
+            g.K = h;
+            g.R = R;
+            g.W = m->wqkvT(l);
+            g.x = (l == 0) ? emb + (size_t)r0 * h : X + (size_t)r0 * h;
+            if (l == 0) {
+                g.gamma = m->gamma;
+                g.bias = m->bias;
+                g.pos = m->pos;
+                g.pos_offset = s->kv->S;
+                g.pos_base = base0 + r0;
+            }
+            g.mode = 1;
+            g.qkv_d = d;
+            g.qkv_H = H;
+            g.q_out = s->q;
+            g.uk = s->uk + (size_t)l * s->ukv_layer();
+            g.uv = s->uv + (size_t)l * s->ukv_layer();
+            g.ucap = s->cap;
+            g.user_base = base0 + r0;
+            launch_gemv(g, st);
+            if (r0 == 0 && ready && ready[l]) EKV_CUDA(cudaStreamWaitEvent(st, ready[l], 0));
+            AttnArgs a{};
+            a.R = R;
+            a.H = H;
+            a.D = d;
+            a.q = s->q;
+            const ekv_segment& sg = s->kv->seg[l];
+            a.fmt = sg.format;
+            a.S = sg.S;
+            a.group = sg.group;
+            a.ck = sg.k;
+            a.cv = sg.v;
+            a.cks = sg.k_scales;
+            a.cvs = sg.v_scales;
+            a.uk = g.uk;
+            a.uv = g.uv;
+            a.ucap = s->cap;
+            a.user_base = base0 + r0;
+            a.out = Y + (size_t)r0 * h;
+            a.ws = s->ws;
+            a.counters = s->counters;
+            launch_decode_attention(a, st);
+            GemvArgs o{};
+            o.N = h;
+            o.K = h;
+            o.R = R;
+            o.W = m->woT(l);
+            o.x = Y + (size_t)r0 * h;
+            o.mode = 0;
+            o.y = X + (size_t)r0 * h;
+            if (l == L - 1) o.y_hist = s->pre_out + (size_t)(base0 + r0) * h;
+            launch_gemv(o, st);
+        }
+    }
+    if (lev) EKV_CUDA(cudaEventRecord(lev[L], st));
 }
 
 size_t attn_ws_floats(int R, int H, int S, int d, int ucap) {
@@ -325,12 +405,13 @@ void check_overflow(ekv_session_s* s, int n) {
 
 // rows [0, n) of emb_dev through merged_forward in chunks of <= 8 rows;
 // final-layer rows land in s->pre_out[user_row].
-void session_forward(ekv_session_s* s, const float* emb_dev, int n, cudaStream_t st) {
+void session_forward(ekv_session_s* s, const float* emb_dev, int n, cudaStream_t st,
+                     const cudaEvent_t* ready = nullptr) {
     check_overflow(s, n);
     for (int r0 = 0; r0 < n; r0 += 8) {
         const int R = std::min(8, n - r0);
         forward_chunk(s, emb_dev + (size_t)r0 * s->model->h, R, s->pre_out,
-                      &s->state->user_len, st);
+                      &s->state->user_len, st, nullptr, r0 == 0 ? ready : nullptr);
         s->user_len += R;
     }
     // decode feeds back the last row: place it in xa[0]; steps count from 0
@@ -664,6 +745,7 @@ int ekv_ctx_create(int device, void* stream, ekv_ctx_t* out) {
             c->own_stream = true;
         }
         EKV_CUDA(cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking));
+        EKV_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
         *out = c;
     });
 }
@@ -675,6 +757,7 @@ int ekv_ctx_destroy(ekv_ctx_t c) {
         cudaStreamSynchronize(c->stream);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         cudaStreamDestroy(c->capture);
+        if (c->copy) cudaStreamDestroy(c->copy);
         delete c;
     });
 }
@@ -1739,6 +1822,100 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb, int U, 
         batch_decode(b, steps, st);
         EKV_CUDA(cudaMemcpyAsync(step_out, b->hist + (size_t)U * B * h, sizeof(float) * steps * B * h,
                                  cudaMemcpyDeviceToHost, st));
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+
+// ---------------------------------------------------------------- Eq. 20 pipelined prefill
+int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
+                                  const ekv_layer_upload* uploads, int overlap, float* t_comm_ms,
+                                  float* t_comp_ms, float* total_ms) {
+    return guard([&] {
+        require(s && emb_dev && uploads && t_comm_ms && t_comp_ms && total_ms,
+                "ekv_session_forward_pipelined: null argument");
+        require(n >= 1, "ekv_session_forward_pipelined: n must be >= 1");
+        ekv_model_s* m = s->model;
+        ekv_ctx_s* c = m->ctx;
+        const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m);
+        check_overflow(s, n);
+        set_dev(c);
+        cudaStream_t st = c->stream, cp = c->copy;
+        std::vector<cudaEvent_t> up(L + 1, nullptr), ready(L, nullptr), cs(L + 1, nullptr);
+        auto cleanup = [&] {
+            for (auto* v : {&up, &ready, &cs})
+                for (auto& e : *v)
+                    if (e) cudaEventDestroy(e);
+        };
+        try {
+            for (auto& e : up) EKV_CUDA(cudaEventCreate(&e));
+            for (auto& e : cs) EKV_CUDA(cudaEventCreate(&e));
+            // start both streams from the same point
+            EKV_CUDA(cudaEventRecord(up[0], st));
+            EKV_CUDA(cudaStreamWaitEvent(cp, up[0], 0));
+            EKV_CUDA(cudaEventRecord(up[0], cp));
+            for (int l = 0; l < L; ++l) {
+                const ekv_layer_upload& u = uploads[l];
+                const ekv_segment& sg = s->kv->seg[l];
+                if (u.k_host && sg.S > 0) {
+                    const size_t rows = (size_t)H * sg.S;
+                    const size_t row_b = sg.format == EKV_KV_BF16 ? (size_t)d * 2 : (size_t)d * sg.format / 8;
+                    require(u.v_host != nullptr, "upload: layer " + std::to_string(l) + " has K but no V");
+                    EKV_CUDA(cudaMemcpyAsync((void*)sg.k, u.k_host, rows * row_b, cudaMemcpyHostToDevice, cp));
+                    EKV_CUDA(cudaMemcpyAsync((void*)sg.v, u.v_host, rows * row_b, cudaMemcpyHostToDevice, cp));
+                    if (sg.format != EKV_KV_BF16) {
+                        require(u.k_scales_host && u.v_scales_host,
+                                "upload: quantised layer " + std::to_string(l) + " needs scales");
+                        const size_t sb = rows * (d / sg.group) * sizeof(float);
+                        EKV_CUDA(cudaMemcpyAsync((void*)sg.k_scales, u.k_scales_host, sb, cudaMemcpyHostToDevice, cp));
+                        EKV_CUDA(cudaMemcpyAsync((void*)sg.v_scales, u.v_scales_host, sb, cudaMemcpyHostToDevice, cp));
+                    }
+                    EKV_CUDA(cudaEventCreateWithFlags(&ready[l], cudaEventDisableTiming));
+                    EKV_CUDA(cudaEventRecord(ready[l], cp));
+                }
+                EKV_CUDA(cudaEventRecord(up[l + 1], cp));
+            }
+            if (!overlap) {  // sequential reference schedule: every upload before any compute
+                EKV_CUDA(cudaStreamWaitEvent(st, up[L], 0));
+            }
+            const int prev_len = s->user_len;
+            float* scratch = nullptr;
+            EKV_CUDA(cudaMallocAsync((void**)&scratch, sizeof(float) * 2 * n * m->h, st));
+            EKV_CUDA(cudaEventRecord(cs[0], st));
+            forward_layer_major(s, emb_dev, n, prev_len, st, overlap ? ready.data() : nullptr, scratch, nullptr);
+            EKV_CUDA(cudaEventRecord(cs[L], st));
+            // state: n more user rows; decode continues from the last row (xa[0]), step 0
+            launch_advance(s->state, n, st);
+            EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
+            EKV_CUDA(cudaMemcpyAsync(s->xa, scratch + (size_t)(n - 1) * m->h, sizeof(float) * m->h,
+                                     cudaMemcpyDeviceToDevice, st));
+            if (out_dev)
+                EKV_CUDA(cudaMemcpyAsync(out_dev, s->pre_out + (size_t)prev_len * m->h,
+                                         sizeof(float) * n * m->h, cudaMemcpyDeviceToDevice, st));
+            EKV_CUDA(cudaStreamSynchronize(cp));
+            EKV_CUDA(cudaStreamSynchronize(st));
+            for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comm_ms[l], up[l], up[l + 1]));
+            float tot = 0.f;
+            EKV_CUDA(cudaEventElapsedTime(&tot, up[0], cs[L]));
+            *total_ms = tot;
+            // per-layer compute: the same rows again, layer by layer with the context resident
+            // (diagnostic; rewrites the same user-cache rows and outputs with identical values)
+            {
+                std::vector<cudaEvent_t> lev(L + 1);
+                for (auto& e : lev) EKV_CUDA(cudaEventCreate(&e));
+                forward_layer_major(s, emb_dev, n, prev_len, st, nullptr, scratch, lev.data());
+                EKV_CUDA(cudaStreamSynchronize(st));
+                for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comp_ms[l], lev[l], lev[l + 1]));
+                for (auto& e : lev) cudaEventDestroy(e);
+            }
+            EKV_CUDA(cudaFreeAsync(scratch, st));
+            s->user_len += n;
+            s->steps = 0;
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
         EKV_CUDA(cudaStreamSynchronize(st));
     });
 }

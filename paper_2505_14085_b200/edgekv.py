@@ -344,6 +344,10 @@ class AssembledContext:
             pass
 
 
+class _LayerUpload(C.Structure):
+    _fields_ = [("k", C.c_void_p), ("v", C.c_void_p), ("ks", C.c_void_p), ("vs", C.c_void_p)]
+
+
 class Session:
     """ekv_session: one request's user/generated KV cache + decode state."""
 
@@ -364,6 +368,27 @@ class Session:
         call("ekv_session_forward", self.hnd, _ptr(emb), emb.shape[0], _ptr(out))
         self.model.ctx.synchronize()
         return out
+
+    def forward_pipelined(self, emb: torch.Tensor, uploads: dict, overlap: bool = True):
+        """Eq. 20 pipelined prefill: `uploads` = {layer: (k, v, k_scales, v_scales)} pinned host
+        tensors (scales None for bf16 layers) copied into the context while the rows are
+        forwarded.  Returns (out [n][h], t_comm_ms [L], t_comp_ms [L], total_ms)."""
+        emb = emb.contiguous().float()
+        out = torch.empty_like(emb)
+        L = self.model.L
+        arr = (_LayerUpload * L)()
+        keep = []
+        for l, (k, v, ks, vs) in uploads.items():
+            keep += [k, v, ks, vs]
+            arr[l].k = k.data_ptr(); arr[l].v = v.data_ptr()
+            arr[l].ks = ks.data_ptr() if ks is not None else None
+            arr[l].vs = vs.data_ptr() if vs is not None else None
+        tc = np.zeros(L, np.float32); tp = np.zeros(L, np.float32); tot = C.c_float()
+        _sync_in()
+        call("ekv_session_forward_pipelined", self.hnd, _ptr(emb), emb.shape[0], _ptr(out),
+             C.cast(arr, C.c_void_p), 1 if overlap else 0, tc.ctypes.data_as(C.POINTER(C.c_float)),
+             tp.ctypes.data_as(C.POINTER(C.c_float)), C.byref(tot))
+        return out, tc, tp, tot.value
 
     def decode(self, steps: int, out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
         if out is None:

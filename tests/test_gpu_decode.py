@@ -297,3 +297,56 @@ def test_full_ce_lslm_path_compression_sweep(ek, ctx, oracle, Lc, Le, deep, bits
     4:1 (16 -> 4 layers) and 2:1 (8 -> 4), the whole path (layer map, mask, codes,
     decode) against the oracle."""
     run_full_ce_lslm_path(ek, ctx, oracle, Lc, Le, deep, bits)
+
+
+def _layer_bytes(seg, H, d):
+    rows = H * seg.S
+    row_b = d * 2 if seg.format == 16 else d * seg.format // 8
+    return rows * row_b, (rows * (d // seg.group) * 4 if seg.format != 16 else 0)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_pipelined_prefill_eq20(ek, ctx, oracle, overlap):
+    """Eq. 20 (pipeline_schedule, cost_model.cpp:73-100) on the device: the context
+    layers arrive from pinned host memory on the copy stream while the user rows
+    are forwarded; the result equals the resident-context forward bit for bit (and
+    the oracle), and decode continues from it."""
+    import ctypes as C
+    from paper_2505_14085_b200.capi import call
+    L, H, d, S, U, T = 3, 4, 64, 512, 11, 3
+    formats = [16, 8, 8]
+    max_pos = S + U + T + 1
+    bits, f64 = host_bf16_model(oracle, L, H, d, max_pos, seed=91)
+    model = upload_model(ek, ctx, bits, L, H, d, max_pos)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, formats, seed=93)
+    ue = torch.from_numpy(oracle.generate_embeddings(97, U, H * d).astype(np.float32)).cuda()
+    ref = ek.Session(model, kvc, U + T)
+    want = ref.forward(ue).cpu().numpy()
+    want_steps = ref.decode(T).cpu().numpy()
+    # host copies of every context layer, then wipe the device storage
+    uploads = {}
+    for l in range(L):
+        seg = kvc.segment(l)
+        nb, ns = _layer_bytes(seg, H, d)
+        hk = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        hv = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        call("ekv_copy", ctx.h, C.c_void_p(hk.data_ptr()), C.c_void_p(seg.k), nb, 1)
+        call("ekv_copy", ctx.h, C.c_void_p(hv.data_ptr()), C.c_void_p(seg.v), nb, 1)
+        call("ekv_memset", ctx.h, C.c_void_p(seg.k), 0, nb)
+        call("ekv_memset", ctx.h, C.c_void_p(seg.v), 0, nb)
+        hks = hvs = None
+        if ns:
+            hks = torch.empty(ns // 4, dtype=torch.float32).pin_memory()
+            hvs = torch.empty(ns // 4, dtype=torch.float32).pin_memory()
+            call("ekv_copy", ctx.h, C.c_void_p(hks.data_ptr()), C.c_void_p(seg.k_scales), ns, 1)
+            call("ekv_copy", ctx.h, C.c_void_p(hvs.data_ptr()), C.c_void_p(seg.v_scales), ns, 1)
+        uploads[l] = (hk, hv, hks, hvs)
+    sess = ek.Session(model, kvc, U + T)
+    out, tcomm, tcomp, total = sess.forward_pipelined(ue, uploads, overlap=overlap)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert np.all(tcomm > 0) and np.all(tcomp > 0) and total > 0
+    st = sess.decode(T).cpu().numpy()
+    assert np.array_equal(st, want_steps)
+    wp, _ = oracle.collaborative_decode(f64, ck, cv, ue.cpu().numpy().astype(np.float64), 1,
+                                        user_kv_bf16=True)
+    assert max(normwise(want[r], wp[r]) for r in range(U)) <= TOL
