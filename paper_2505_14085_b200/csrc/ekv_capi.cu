@@ -617,6 +617,8 @@ void batch_alloc(ekv_batch_s* b) {
     const int G = m->ctx->num_sms;
     b->KSq = batch_proj_splits(3 * h, h, B, G);
     b->KSo = batch_proj_splits(h, h, B, G);
+    if (const char* e = getenv("EKV_BATCH_KSQ")) b->KSq = std::max(1, std::min(8, atoi(e)));  // experiments
+    if (const char* e = getenv("EKV_BATCH_KSO")) b->KSo = std::max(1, std::min(16, atoi(e)));
     b->nsplit = batch_ctx_splits(b->kv->S, H, B, G);
     const size_t ukv = (size_t)B * L * H * b->cap * D;
     b->uk = dalloc<uint16_t>(ukv);

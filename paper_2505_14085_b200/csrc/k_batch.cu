@@ -37,6 +37,13 @@ using namespace tc;
 
 constexpr int kMaxSplitK = 16;
 
+// Programmatic dependent launch: every kernel of the batched row is launched with
+// programmatic stream serialization, so the next kernel's CTAs are scheduled while
+// this one drains; pdl_wait() blocks until the previous kernel has completed and its
+// writes are visible.  Only static data (weights, context) is read before it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // sum of the KS split-K partials of 4 consecutive floats (16-byte aligned); every
 // load is issued before the first add (the split loop is unrolled to kMaxSplitK
 // with a predicate), so the sum costs one memory round trip, not KS.
@@ -102,9 +109,22 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int kb = kb0; kb < kb1; ++kb) {
+            // weight tiles of the first ring slots do not depend on the previous kernel:
+            // issue them before waiting for it, then the activation tiles
+            const int npre = min(stages, kb1 - kb0);
+            for (int i = 0; i < npre; ++i) {
+                mbar_expect_tx(&full[i], stage_bytes);
+                tma_load_2d(&map_w, &full[i], smem + i * stage_bytes, (kb0 + i) * BK, w_row0 + mt * BM);
+            }
+            pdl_wait();
+            for (int i = 0; i < npre; ++i) {
+                uint8_t* s = smem + i * stage_bytes;
+                tma_load_3d(&map_x, &full[i], s + A_BYTES, (kb0 + i) * BK, nt * BN, 0);
+                tma_load_3d(&map_x, &full[i], s + A_BYTES + x_bytes, (kb0 + i) * BK, nt * BN, 1);
+            }
+            int stage = npre == stages ? 0 : npre;
+            uint32_t phase = npre == stages ? 1 : 0;
+            for (int kb = kb0 + npre; kb < kb1; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 mbar_expect_tx(&full[stage], stage_bytes);
                 uint8_t* s = smem + stage * stage_bytes;
@@ -142,6 +162,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp >= 4) {
         const int quad = warp - 4;
+        pdl_wait();  // the partial buffer may still be read by the previous kernel's consumers
         mbar_wait(tfull, 0);
         fence_after();
         const int n = mt * BM + quad * 32 + lane;
@@ -156,6 +177,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (b0 + i < B && n < N_out) o[(size_t)(b0 + i) * N_out] = v[i];
         }
     }
+    pdl_trigger();
     fence_before();
     __syncthreads();
     fence_after();
@@ -169,6 +191,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // final layer (mode 2): x -> hist[step][b] and xin[b].  Writes hi/lo bf16.
 // ============================================================================
 __global__ void batch_xprep_kernel(BatchXprep a) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.y;
     const int h = a.h;
     const DevState st = *a.state;
@@ -435,6 +459,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
         const int pair_bar = 1 + quad;              // named barrier of warps quad+4 and quad+8
         const bool warp_live = bt * BT + quad * 32 < a.B;  // some session row of this warp exists
+        pdl_wait();  // q comes from the previous kernel (the context K/V are static)
         // ---- stage q (sum of the split-K partials of the QKV projection) as hi / lo:
         //      256 threads, coalesced 16-byte loads, 4 rows' loads in flight per thread ----
         {
@@ -594,6 +619,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 *reinterpret_cast<float4*>(w + 4 + half * 32 + e) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
         }
     }
+    pdl_trigger();
     fence_before();
     __syncthreads();
     fence_after();
@@ -605,36 +631,61 @@ __global__ void __launch_bounds__(THREADS, 1)
 // K11: user segment + append + Eq. 5 merge, one warp per (session, head).
 // ============================================================================
 template <int D>
-__global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a) {
+__global__ void __launch_bounds__(128, 3) batch_user_merge_kernel(BatchUserMerge a) {
     constexpr int G = D / 8;         // lanes per row (8 dims = 16 bytes per lane)
     constexpr int RPI = 32 / G;      // rows per warp-wide load
     constexpr int NT = 32 / RPI;     // rows per lane per 32-row block
+    constexpr int NP = 4;            // context partials whose loads are issued up front
     const int lane = threadIdx.x & 31;
     const int item = blockIdx.x * 4 + (threadIdx.x >> 5);
+    pdl_wait();
+    pdl_trigger();
     if (item >= a.B * a.H) return;
     const int b = item / a.H, hd = item - b * a.H;
     const int grp = lane / G, c = lane - grp * G;  // row group, 8-dim chunk
     const int h = a.H * D;
+    const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
+    uint16_t* uk = a.uk + head_off;
+    uint16_t* uv = a.uv + head_off;
+    // ---- every independent load issued before the first use: the user-row count,
+    //      this step's q/k/v partials, the first 32 user rows, the context partials ----
     const int ulen = a.state->user_len;
-    // this step's q, k, v (8 dims per lane): sum of the split-K partials, all loads in flight
+    constexpr int NV = 3;  // split-K partials held in flight; more are summed by a plain loop
+    const size_t stride = (size_t)a.B * a.n_qkv;
+    const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
+    float4 v[NV][3][2];
+#pragma unroll
+    for (int s = 0; s < NV; ++s)
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            if (s < a.KS) {
+                v[s][t][0] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h);
+                v[s][t][1] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h + 4);
+            } else {
+                v[s][t][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                v[s][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    uint4 kr[NT], vr[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {  // rows < cap are allocated; rows >= ulen are masked below
+        const int j = grp + RPI * t;
+        if (j < a.cap) {
+            kr[t] = *reinterpret_cast<const uint4*>(uk + (size_t)j * D + c * 8);
+            vr[t] = *reinterpret_cast<const uint4*>(uv + (size_t)j * D + c * 8);
+        } else {
+            kr[t] = make_uint4(0, 0, 0, 0);
+            vr[t] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    const float* wpart = a.part + ((size_t)b * a.H + hd) * a.nsplit * (D + 4);
+    float2 pml[NP];
+#pragma unroll
+    for (int s = 0; s < NP; ++s)
+        if (s < a.nsplit) pml[s] = *reinterpret_cast<const float2*>(wpart + s * (D + 4));
+    // ---- q, k, v (k, v rounded to bf16 as stored) ----
     float q[8], kc[8], vc[8];
     {
-        const size_t stride = (size_t)a.B * a.n_qkv;
-        const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
-        constexpr int NV = 4;  // splits held in flight; more are summed by a plain loop
-        float4 v[NV][3][2];
-#pragma unroll
-        for (int s = 0; s < NV; ++s)
-#pragma unroll
-            for (int t = 0; t < 3; ++t) {
-                if (s < a.KS) {
-                    v[s][t][0] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h);
-                    v[s][t][1] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h + 4);
-                } else {
-                    v[s][t][0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    v[s][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
-            }
         for (int s = NV; s < a.KS; ++s)
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
@@ -665,9 +716,6 @@ __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a)
         }
     }
     // append (cache_merge.cpp:189-199): row ulen of this session's user cache
-    const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
-    uint16_t* uk = a.uk + head_off;
-    uint16_t* uv = a.uv + head_off;
     if (grp == 0) {
         uint4 kw, vw;
         kw.x = f32_to_bf16_bits(kc[0]) | ((uint32_t)f32_to_bf16_bits(kc[1]) << 16);
@@ -686,16 +734,14 @@ __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a)
 #pragma unroll
     for (int e = 0; e < 8; ++e) o[e] = 0.0f;
     for (int j0 = 0; j0 < ulen; j0 += 32) {
-        uint4 kr[NT], vr[NT];
+        if (j0 > 0) {
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            const int j = j0 + grp + RPI * t;
-            if (j < ulen) {
-                kr[t] = *reinterpret_cast<const uint4*>(uk + (size_t)j * D + c * 8);
-                vr[t] = *reinterpret_cast<const uint4*>(uv + (size_t)j * D + c * 8);
-            } else {
-                kr[t] = make_uint4(0, 0, 0, 0);
-                vr[t] = make_uint4(0, 0, 0, 0);
+            for (int t = 0; t < NT; ++t) {
+                const int j = j0 + grp + RPI * t;
+                if (j < ulen) {
+                    kr[t] = *reinterpret_cast<const uint4*>(uk + (size_t)j * D + c * 8);
+                    vr[t] = *reinterpret_cast<const uint4*>(uv + (size_t)j * D + c * 8);
+                }
             }
         }
         float sc[NT];
@@ -755,15 +801,33 @@ __global__ void __launch_bounds__(128) batch_user_merge_kernel(BatchUserMerge a)
     }
     // Eq. 5 generalised: log-sum-exp merge of the user partial with the context partials
     if (a.nsplit > 0) {
-        const float* w = a.part + ((size_t)b * a.H + hd) * a.nsplit * (D + 4);
         float M = m;
-        for (int s = 0; s < a.nsplit; ++s) M = fmaxf(M, w[s * (D + 4)]);
+#pragma unroll
+        for (int s = 0; s < NP; ++s)
+            if (s < a.nsplit) M = fmaxf(M, pml[s].x);
+        for (int s = NP; s < a.nsplit; ++s) M = fmaxf(M, wpart[s * (D + 4)]);
         const float fu = __expf(m - M);
         float Lt = l * fu, ot[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) ot[e] = o[e] * fu;
-        for (int s = 0; s < a.nsplit; ++s) {
-            const float* ws = w + s * (D + 4);
+        float4 po[NP][2];
+#pragma unroll
+        for (int s = 0; s < NP; ++s)
+            if (s < a.nsplit) {
+                po[s][0] = *reinterpret_cast<const float4*>(wpart + s * (D + 4) + 4 + c * 8);
+                po[s][1] = *reinterpret_cast<const float4*>(wpart + s * (D + 4) + 8 + c * 8);
+            }
+#pragma unroll
+        for (int s = 0; s < NP; ++s)
+            if (s < a.nsplit) {
+                const float f = pml[s].x == -INFINITY ? 0.0f : __expf(pml[s].x - M);
+                Lt += pml[s].y * f;
+                ot[0] += po[s][0].x * f; ot[1] += po[s][0].y * f; ot[2] += po[s][0].z * f;
+                ot[3] += po[s][0].w * f; ot[4] += po[s][1].x * f; ot[5] += po[s][1].y * f;
+                ot[6] += po[s][1].z * f; ot[7] += po[s][1].w * f;
+            }
+        for (int s = NP; s < a.nsplit; ++s) {
+            const float* ws = wpart + s * (D + 4);
             const float2 ml = *reinterpret_cast<const float2*>(ws);
             const float4 o0 = *reinterpret_cast<const float4*>(ws + 4 + c * 8);
             const float4 o1 = *reinterpret_cast<const float4*>(ws + 8 + c * 8);
@@ -814,6 +878,22 @@ int batch_proj_splits(int N_out, int K, int B, int num_sms) {
     return ks;
 }
 
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EKV_CUDA(cudaLaunchKernelEx(&cfg, fn, args...));
+}
+
 void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, const CUtensorMap& map_x,
                        int B, int KS, float* out, cudaStream_t st) {
     using namespace k9;
@@ -830,15 +910,15 @@ void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, c
         attr = 227 * 1024;
     }
     dim3 grid(N_out / BM, (B + BN - 1) / BN, KS);
-    batch_proj_kernel<<<grid, THREADS, smem, st>>>(map_w, map_x, w_row0, N_out, K, B, BN, KS, stages,
-                                                    idesc_bf16(BM, BN), out);
+    launch_pdl(batch_proj_kernel, grid, dim3(THREADS), smem, st, map_w, map_x, w_row0, N_out, K, B, BN, KS,
+               stages, idesc_bf16(BM, BN), out);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }
 
 void launch_batch_xprep(const BatchXprep& a, cudaStream_t st) {
     dim3 grid((a.h / 4 + 127) / 128, a.B);
-    batch_xprep_kernel<<<grid, 128, 0, st>>>(a);
+    launch_pdl(batch_xprep_kernel, grid, dim3(128), 0, st, a);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }
@@ -868,7 +948,7 @@ static void launch_ctx(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaStream
         attr = true;
     }
     dim3 grid(a.H, a.nsplit, (a.B + BT - 1) / BT);
-    batch_ctx_attn_kernel<64, FMT><<<grid, THREADS, Cf::SMEM, st>>>(mp.k, mp.v, mp.ks, mp.vs, a);
+    launch_pdl(batch_ctx_attn_kernel<64, FMT>, grid, dim3(THREADS), Cf::SMEM, st, mp.k, mp.v, mp.ks, mp.vs, a);
 }
 
 void launch_batch_ctx_attn(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaStream_t st) {
@@ -885,9 +965,9 @@ void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st) {
     const int items = a.B * a.H;
     const int grid = (items + 3) / 4;
     switch (a.D) {
-        case 32: batch_user_merge_kernel<32><<<grid, 128, 0, st>>>(a); break;
-        case 64: batch_user_merge_kernel<64><<<grid, 128, 0, st>>>(a); break;
-        case 128: batch_user_merge_kernel<128><<<grid, 128, 0, st>>>(a); break;
+        case 32: launch_pdl(batch_user_merge_kernel<32>, dim3(grid), dim3(128), 0, st, a); break;
+        case 64: launch_pdl(batch_user_merge_kernel<64>, dim3(grid), dim3(128), 0, st, a); break;
+        case 128: launch_pdl(batch_user_merge_kernel<128>, dim3(grid), dim3(128), 0, st, a); break;
         default: require(false, "batched decode: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
     }
     EKV_CUDA(cudaGetLastError());
