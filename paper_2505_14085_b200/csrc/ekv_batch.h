@@ -19,9 +19,29 @@ struct BatchXprep {
     const float* bias;
     const uint16_t* pos;   // [max_pos][h]
     int pos_offset;        // S: position of user row u is S + u
+    int pos_per_row;       // 1: row b sits at position S + user_len + row0 + b (prefill rows of one session)
+    int row0;
     const DevState* state;
     uint16_t* xhl;         // [2][B][h] bf16 hi, lo (projection operand)
 };
+
+// Prefill projections on the tensor cores (R >= 2 rows of one session): the
+// finish step of K9's split-K partials.  mode 0 (QKV, N = 3h): q -> q_out
+// fp32 [R][h], k/v rounded to bf16 into the user cache rows user_len + r
+// (layout [H][cap][d]); mode 1 (out-proj, N = h): y [R][h] and, if y_hist,
+// y_hist[user_len + r].
+struct PrefillFinish {
+    int mode, R, N, KS, H, d, cap;
+    int row0;              // rows of this chunk start at user_len + row0
+    const float* part;     // [KS][R][N]
+    float* q_out;
+    uint16_t* uk;
+    uint16_t* uv;
+    float* y;
+    float* y_hist;
+    const DevState* state;
+};
+void launch_prefill_finish(const PrefillFinish& a, cudaStream_t st);
 
 struct BatchCtxAttn {
     int B, H, D, S, nsplit, KS, n_qkv;

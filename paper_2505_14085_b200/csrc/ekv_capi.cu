@@ -117,6 +117,12 @@ struct ekv_session_s {
     uint64_t* mega_ll = nullptr;     // tagged words of the dataflow (MegaArgs::ll_*)
     unsigned* mega_sync = nullptr;   // [0] launch epoch
     MegaArgs mega{};
+    // tensor-core prefill projections (R >= 2 rows; h % 128 == 0)
+    bool tc_prefill = false;
+    uint16_t* pxhl = nullptr;      // [2][8][h] bf16 hi / lo operand
+    float* ppart = nullptr;        // [max(KSq*3h, KSo*h)][8] split-K partials
+    int pKSq = 1, pKSo = 1;
+    CUtensorMap pmap_w{}, pmap_x{};
     size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
 };
 
@@ -141,6 +147,84 @@ void set_dev(ekv_ctx_s* c) { EKV_CUDA(cudaSetDevice(c->device)); }
 
 int d_of(const ekv_model_s* m) { return m->cfg.head_dim; }
 
+// Tensor-core projections of R >= 2 rows of one session (K9 + split-K finish):
+// QKV of layer l from `in` (fp32 [R][h]; layer 0 gets the input transform at
+// positions S + user_len + row0 + r) -> q to s->q, k/v appended to the user
+// cache at rows user_len + row0 + r; and the output projection x (fp32 [R][h])
+// -> y (fp32 [R][h]) (+ y_hist[user_len + row0 + r] if non-null).
+void tc_qkv_rows(ekv_session_s* s, int l, const float* in, int R, int row0, const CUtensorMap& pmap_x,
+                 cudaStream_t st) {
+    ekv_model_s* m = s->model;
+    const int h = m->h;
+    BatchXprep xp{};
+    xp.B = R;
+    xp.h = h;
+    xp.state = s->state;
+    xp.xhl = s->pxhl;
+    xp.row0 = row0;
+    if (l == 0) {
+        xp.mode = 0;
+        xp.xin = const_cast<float*>(in);
+        xp.gamma = m->gamma;
+        xp.bias = m->bias;
+        xp.pos = m->pos;
+        xp.pos_offset = s->kv->S;
+        xp.pos_per_row = 1;
+    } else {
+        xp.mode = 1;
+        xp.KS = 1;
+        xp.part = in;
+    }
+    launch_batch_xprep(xp, st);
+    launch_batch_proj(s->pmap_w, l * 4 * h, 3 * h, h, pmap_x, R, s->pKSq, s->ppart, st);
+    PrefillFinish f{};
+    f.mode = 0;
+    f.R = R;
+    f.N = 3 * h;
+    f.KS = s->pKSq;
+    f.H = m->cfg.num_heads;
+    f.d = m->cfg.head_dim;
+    f.cap = s->cap;
+    f.row0 = row0;
+    f.part = s->ppart;
+    f.q_out = s->q;
+    f.uk = s->uk + (size_t)l * s->ukv_layer();
+    f.uv = s->uv + (size_t)l * s->ukv_layer();
+    f.state = s->state;
+    launch_prefill_finish(f, st);
+}
+
+void tc_out_rows(ekv_session_s* s, int l, const float* x, float* y, float* y_hist, int R, int row0,
+                 const CUtensorMap& pmap_x, cudaStream_t st) {
+    const int h = s->model->h;
+    BatchXprep xp{};
+    xp.mode = 1;
+    xp.B = R;
+    xp.h = h;
+    xp.KS = 1;
+    xp.part = x;
+    xp.state = s->state;
+    xp.xhl = s->pxhl;
+    launch_batch_xprep(xp, st);
+    launch_batch_proj(s->pmap_w, l * 4 * h + 3 * h, h, h, pmap_x, R, s->pKSo, s->ppart, st);
+    PrefillFinish f{};
+    f.mode = 1;
+    f.R = R;
+    f.N = h;
+    f.KS = s->pKSo;
+    f.row0 = row0;
+    f.part = s->ppart;
+    f.y = y;
+    f.y_hist = y_hist;
+    f.state = s->state;
+    launch_prefill_finish(f, st);
+}
+
+CUtensorMap tc_operand_map(ekv_session_s* s, int R) {
+    return make_map_3d_bf16(s->pxhl, (uint64_t)s->model->h, (uint64_t)R, 2, 64, (uint32_t)batch_proj_bn(R),
+                            CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 // One forward chunk of R <= 8 rows through every layer (merged_forward,
 // cache_merge.cpp:156-226).  `in` holds the R input rows (fp32 [R][h]);
 // `out_hist`/`hist_row_dev` receive the final-layer rows.
@@ -153,8 +237,12 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
     auto mark = [&] {
         if (ev) EKV_CUDA(cudaEventRecord(ev[ei++], st));
     };
+    const bool tc = s->tc_prefill && R >= 2 && !ev;
+    CUtensorMap pmap_x{};
+    if (tc) pmap_x = tc_operand_map(s, R);
     for (int l = 0; l < L; ++l) {
         mark();
+        if (tc) tc_qkv_rows(s, l, l == 0 ? in : s->xa, R, 0, pmap_x, st);
         GemvArgs g{};
         g.N = 3 * h;
         g.K = h;
@@ -176,7 +264,7 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
         g.uv = s->uv + (size_t)l * s->ukv_layer();
         g.ucap = s->cap;
         g.user_base_dev = &s->state->user_len;
-        launch_gemv(g, st);
+        if (!tc) launch_gemv(g, st);
         mark();
         // pipelined prefill: this layer's context must have arrived (Eq. 20: the
         // upload of layer l overlaps the compute of layers < l)
@@ -218,7 +306,15 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
             o.y_hist = out_hist;
             o.hist_row_dev = hist_row_dev;
         }
-        launch_gemv(o, st);
+        if (tc) {
+            // the prefill's final rows land in pre_out[user_len + r] (hist_row_dev is
+            // &state->user_len for the prefill, the only caller with R >= 2)
+            require(!(l == L - 1 && out_hist) || hist_row_dev == &s->state->user_len,
+                    "tensor-core prefill: unexpected history row");
+            tc_out_rows(s, l, s->xb, s->xa, (l == L - 1) ? out_hist : nullptr, R, 0, pmap_x, st);
+        } else {
+            launch_gemv(o, st);
+        }
     }
     mark();
     launch_advance(s->state, R, st);
@@ -241,6 +337,11 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
         if (lev) EKV_CUDA(cudaEventRecord(lev[l], st));
         for (int r0 = 0; r0 < n; r0 += 8) {
             const int R = std::min(8, n - r0);
+            const bool tc = s->tc_prefill && R >= 2;
+            CUtensorMap pmap_x{};
+            if (tc) pmap_x = tc_operand_map(s, R);
+            if (tc) tc_qkv_rows(s, l, (l == 0) ? emb + (size_t)r0 * h : X + (size_t)r0 * h, R, base0 + r0 - s->user_len,
+                                pmap_x, st);
             GemvArgs g{};
             g.N = 3 * h;
             g.K = h;
@@ -262,7 +363,7 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             g.uv = s->uv + (size_t)l * s->ukv_layer();
             g.ucap = s->cap;
             g.user_base = base0 + r0;
-            launch_gemv(g, st);
+            if (!tc) launch_gemv(g, st);
             if (r0 == 0 && ready && ready[l]) EKV_CUDA(cudaStreamWaitEvent(st, ready[l], 0));
             AttnArgs a{};
             a.R = R;
@@ -294,7 +395,11 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             o.mode = 0;
             o.y = X + (size_t)r0 * h;
             if (l == L - 1) o.y_hist = s->pre_out + (size_t)(base0 + r0) * h;
-            launch_gemv(o, st);
+            if (tc)
+                tc_out_rows(s, l, Y + (size_t)r0 * h, X + (size_t)r0 * h,
+                            (l == L - 1) ? s->pre_out : nullptr, R, base0 + r0 - s->user_len, pmap_x, st);
+            else
+                launch_gemv(o, st);
         }
     }
     if (lev) EKV_CUDA(cudaEventRecord(lev[L], st));
@@ -323,6 +428,17 @@ void session_alloc(ekv_session_s* s) {
         ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim, s->cap));
     s->ws = dalloc<float>(ws);
     s->counters = dalloc<unsigned>((size_t)8 * m->cfg.num_heads);
+    if (m->h % 128 == 0 && !getenv("EKV_NO_TC_PREFILL")) {
+        const int G = m->ctx->num_sms, h = m->h;
+        s->tc_prefill = true;
+        s->pKSq = batch_proj_splits(3 * h, h, 8, G);
+        s->pKSo = batch_proj_splits(h, h, 8, G);
+        s->pxhl = dalloc<uint16_t>((size_t)2 * 8 * h);
+        s->ppart = dalloc<float>(std::max((size_t)s->pKSq * 3 * h, (size_t)s->pKSo * h) * 8);
+        s->pmap_w = make_map_2d(m->weights, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)h,
+                                (uint64_t)m->cfg.num_layers * 4 * h, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+        // the operand map is re-encoded per chunk size R (rows >= R read as zeros)
+    }
     {
         const int L = m->cfg.num_layers, H = m->cfg.num_heads, D = m->cfg.head_dim;
         const char* env = getenv("EKV_DECODE_PATH");
@@ -1485,7 +1601,7 @@ int ekv_session_create(ekv_model_t m, ekv_kvctx_t c, int max_user_rows, ekv_sess
         } catch (...) {
             for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                             (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
-                            (void*)s->ws, (void*)s->counters})
+                            (void*)s->ws, (void*)s->counters, (void*)s->pxhl, (void*)s->ppart})
                 cudaFree(p);
             delete s;
             throw;
@@ -1502,7 +1618,8 @@ int ekv_session_destroy(ekv_session_t s) {
         if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
         for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                         (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
-                        (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync})
+                        (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync,
+                        (void*)s->pxhl, (void*)s->ppart})
             cudaFree(p);
         delete s;
     });
@@ -1886,11 +2003,6 @@ int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, 
             EKV_CUDA(cudaEventRecord(cs[0], st));
             forward_layer_major(s, emb_dev, n, prev_len, st, overlap ? ready.data() : nullptr, scratch, nullptr);
             EKV_CUDA(cudaEventRecord(cs[L], st));
-            // state: n more user rows; decode continues from the last row (xa[0]), step 0
-            launch_advance(s->state, n, st);
-            EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
-            EKV_CUDA(cudaMemcpyAsync(s->xa, scratch + (size_t)(n - 1) * m->h, sizeof(float) * m->h,
-                                     cudaMemcpyDeviceToDevice, st));
             if (out_dev)
                 EKV_CUDA(cudaMemcpyAsync(out_dev, s->pre_out + (size_t)prev_len * m->h,
                                          sizeof(float) * n * m->h, cudaMemcpyDeviceToDevice, st));
@@ -1910,6 +2022,11 @@ int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, 
                 for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comp_ms[l], lev[l], lev[l + 1]));
                 for (auto& e : lev) cudaEventDestroy(e);
             }
+            // state: n more user rows; decode continues from the last row (xa[0]), step 0
+            launch_advance(s->state, n, st);
+            EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
+            EKV_CUDA(cudaMemcpyAsync(s->xa, scratch + (size_t)(n - 1) * m->h, sizeof(float) * m->h,
+                                     cudaMemcpyDeviceToDevice, st));
             EKV_CUDA(cudaFreeAsync(scratch, st));
             s->user_len += n;
             s->steps = 0;

@@ -196,7 +196,7 @@ __global__ void batch_xprep_kernel(BatchXprep a) {
     const int b = blockIdx.y;
     const int h = a.h;
     const DevState st = *a.state;
-    const int p = a.pos_offset + st.user_len;
+    const int p = a.pos_offset + st.user_len + (a.pos_per_row ? a.row0 + b : 0);
     const int k = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (k >= h) return;
     float4 x;
@@ -957,6 +957,42 @@ void launch_batch_ctx_attn(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaSt
         launch_ctx<16>(mp, a, st);
     else
         launch_ctx<8>(mp, a, st);
+    EKV_CUDA(cudaGetLastError());
+    count_launches(1);
+}
+
+// ============================================================================
+// Prefill finish: split-K sum of K9's partials + the consumer's layout
+// ============================================================================
+__global__ void prefill_finish_kernel(PrefillFinish a) {
+    pdl_wait();
+    pdl_trigger();
+    const int r = blockIdx.y;
+    const int n = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (n >= a.N) return;
+    const float4 x = sum_splits4(a.part + (size_t)r * a.N + n, (size_t)a.R * a.N, a.KS);
+    const int base = a.state->user_len + a.row0;
+    if (a.mode == 0) {
+        const int h = a.N / 3;
+        if (n < h) {
+            *reinterpret_cast<float4*>(a.q_out + (size_t)r * h + n) = x;
+        } else {
+            const int nn = n < 2 * h ? n - h : n - 2 * h;
+            const int head = nn / a.d, c = nn - head * a.d;
+            uint16_t* dst = (n < 2 * h ? a.uk : a.uv) + ((size_t)head * a.cap + base + r) * a.d + c;
+            *reinterpret_cast<uint2*>(dst) =
+                make_uint2(f32_to_bf16_bits(x.x) | ((uint32_t)f32_to_bf16_bits(x.y) << 16),
+                           f32_to_bf16_bits(x.z) | ((uint32_t)f32_to_bf16_bits(x.w) << 16));
+        }
+    } else {
+        *reinterpret_cast<float4*>(a.y + (size_t)r * a.N + n) = x;
+        if (a.y_hist) *reinterpret_cast<float4*>(a.y_hist + (size_t)(base + r) * a.N + n) = x;
+    }
+}
+
+void launch_prefill_finish(const PrefillFinish& a, cudaStream_t st) {
+    dim3 grid((a.N / 4 + 127) / 128, a.R);
+    launch_pdl(prefill_finish_kernel, grid, dim3(128), 0, st, a);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }
