@@ -468,7 +468,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     #     emulated link (pinned host -> HBM on a copy stream) while the user prompt is
     #     forwarded (Eq. 20 overlap, ekv_session_forward_pipelined) ---
     c4 = None
-    if not args.no_c4:
+    if not args.no_c4 and rank == 0:  # a per-host measurement (pinned-host link), rank 0 only
         try:
             import ctypes as C
             S4 = 32768

@@ -29,15 +29,25 @@ def broadcast_packed_kv(tensors: list[torch.Tensor], src: int = 0, group=None) -
     Tensors are updated in place on every rank.  Returns {bytes, seconds}."""
     nbytes = int(sum(t.numel() * t.element_size() for t in tensors))
     if dist.is_initialized() and dist.get_world_size(group) > 1:
+        cuda = bool(tensors) and tensors[0].is_cuda
+        # communicator set-up is not link time: one small warm-up collective first
+        warm = torch.zeros(1, device=tensors[0].device if tensors else None)
+        dist.broadcast(warm, src=src, group=group)
         dist.barrier(group)
-        if tensors and tensors[0].is_cuda:
+        if cuda:
             torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         t0 = time.perf_counter()
         for t in tensors:
             dist.broadcast(t, src=src, group=group)
-        if tensors and tensors[0].is_cuda:
+        if cuda:
+            e1.record()
             torch.cuda.synchronize()
-        return {"bytes": nbytes, "seconds": time.perf_counter() - t0}
+            sec = max_over_ranks(e0.elapsed_time(e1) * 1e-3, device=tensors[0].device, group=group)
+        else:
+            sec = time.perf_counter() - t0
+        return {"bytes": nbytes, "seconds": sec}
     return {"bytes": nbytes, "seconds": 0.0}
 
 
