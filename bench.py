@@ -452,6 +452,25 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             c_bytes = L * (b_qkv + b_out) + (L - DEEP) * b_att_local + DEEP * b_att_deep + \
                 Bc * L * 2 * H * rows_att * d * 2
             c_step_s = c_ms / Kc * 1e-3
+            # the configs[2] sweep (64-1024 sessions on this GPU), shorter runs
+            sweep = []
+            for Bs in args.sweep:
+                if Bs == Bc:
+                    continue
+                bt = ek.SessionBatch(model, kvc, Bs, U + 3 + 10 + 2)
+                bt.forward(torch.empty((Bs, U, h), dtype=torch.float32, device="cuda").uniform_(-1, 1))
+                bt.decode(3)
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0.record(st)
+                bt.decode(10, sync=False)
+                e1.record(st)
+                st.synchronize()
+                s_ms = max_over_ranks(e0.elapsed_time(e1), device="cuda")
+                sweep.append({"sessions_per_gpu": Bs, "tok_s": world * Bs * 10 / (s_ms * 1e-3),
+                              "ms_per_step": s_ms / 10})
+                del bt
             conc = {"config": f"C3: {Bc} concurrent sessions per GPU ({Bc * world} total) sharing the "
                               f"S={S} context, {U} user rows each, lock-step decode (ekv_batch_*)",
                     "sessions_per_gpu": Bc, "value": world * Bc * Kc / (c_ms * 1e-3), "unit": "tok/s",
@@ -459,7 +478,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                     "bytes_per_step": c_bytes, "achieved_gbs": c_bytes / c_step_s / 1e9,
                     "frac": c_bytes / c_step_s / 1e9 / hbm,
                     "outputs_finite": bool(torch.isfinite(out_c).all().item()),
-                    "splits": batch.info()}
+                    "splits": batch.info(), "sweep": sweep}
             del batch, emb_c, out_c
         except Exception as e:  # noqa: BLE001
             conc = {"error": str(e)[:300]}
@@ -569,6 +588,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sessions", type=int, default=128, help="C3 sessions per GPU (batched path)")
     ap.add_argument("--no-concurrency", action="store_true")
+    ap.add_argument("--sweep", type=lambda v: [int(x) for x in v.split(",") if x], default=[64, 256, 512, 1024],
+                    help="other C3 session counts per GPU measured briefly")
     ap.add_argument("--no-c4", action="store_true", help="skip the 32k pipelined-prefill block")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
