@@ -361,6 +361,43 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb_host, in
                                    float* prefill_out_host, float* step_out_host);
 
 /* ------------------------------------------------------------------ */
+/* Packed-KV wire / disk format ("EKVPACK1")                            */
+/* ------------------------------------------------------------------ */
+/* The compressed cloud layers as one self-describing, checksummed byte
+ * stream: what crosses the cloud -> edge link (the transfer the reference
+ * simulates in Sim::submit_transfer, sim.cpp:417-449, sized by
+ * deep_layer_bytes, sim.cpp:714) or is kept as the historical cache.
+ * Layout (little-endian):
+ *   header 64 B: magic "EKVPACK1", u32 version (1), n_layers, H, S, d_e,
+ *     d_c, bits, group, header_bytes, 3 x u32 reserved, u64 header_fnv
+ *   i32 edge_layer[n], i32 cloud_layer[n] (the layer map), i32 kept[d_e]
+ *   (the channel mask), u64 layer_fnv[n], zero padding to header_bytes
+ *   (a multiple of 256)
+ *   per layer: K codes [H][S][d_e*bits/8], V codes, K scales fp32
+ *   [H][S][d_e/group], V scales
+ * Checksums are FNV-1a 64 (the reference's fnv1a64, rng.cpp:7-15): the
+ * header (with header_fnv = 0) and each layer's payload. */
+typedef struct {
+    int n_layers, H, S, d_e, d_c, bits, group;
+    size_t bytes;
+} ekv_kvpack_info;
+int ekv_fnv1a64(const void* data, size_t len, uint64_t seed, uint64_t* out);
+int ekv_kvpack_size(int n_layers, int H, int S, int d_e, int bits, int group, size_t* bytes);
+/* Serialise compressed layers `layers[n]` of the context (with their cloud
+ * layers and the channel mask kept[d_e]) into host memory. */
+int ekv_kvpack_export(ekv_kvctx_t c, const int* layers, const int* cloud_layers, int n, const int* kept,
+                      int d_c, void* host_dst, size_t capacity);
+/* Validate a pack (magic, version, sizes, every checksum) and read its
+ * description; layers / cloud_layers [n_layers] and kept [d_e] may be NULL.
+ * Host only. Errors: "bad magic", "header checksum mismatch", "checksum
+ * mismatch in layer N", "truncated ...". */
+int ekv_kvpack_parse(const void* host_src, size_t bytes, ekv_kvpack_info* info, int* layers,
+                     int* cloud_layers, int* kept);
+/* Validate and copy the pack's layers into the context's storage (formats,
+ * H, S and d_e must match: "kvpack: dim mismatch"). */
+int ekv_kvpack_import(ekv_kvctx_t c, const void* host_src, size_t bytes);
+
+/* ------------------------------------------------------------------ */
 /* Scheduler interface (cost_model.hpp:53-84)                          */
 /* ------------------------------------------------------------------ */
 

@@ -29,6 +29,11 @@ class ekv_segment(C.Structure):
                 ("v", C.c_void_p), ("k_scales", C.c_void_p), ("v_scales", C.c_void_p)]
 
 
+class ekv_kvpack_info(C.Structure):
+    _fields_ = [("n_layers", C.c_int), ("H", C.c_int), ("S", C.c_int), ("d_e", C.c_int), ("d_c", C.c_int),
+                ("bits", C.c_int), ("group", C.c_int), ("bytes", C.c_size_t)]
+
+
 class ekv_model_config(C.Structure):
     _fields_ = [("num_layers", C.c_int), ("num_heads", C.c_int), ("head_dim", C.c_int),
                 ("max_positions", C.c_int)]
@@ -90,6 +95,11 @@ PROTOS = {
     "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
     "ekv_session_forward_pipelined": [_vp, _vp, _i, _vp, _vp, _i, _fp, _fp, _fp],
     "ekv_batch_create": [_vp, _vp, _i, _i, _pp],
+    "ekv_fnv1a64": [_vp, C.c_size_t, _u64, C.POINTER(C.c_uint64)],
+    "ekv_kvpack_size": [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_size_t)],
+    "ekv_kvpack_export": [_vp, _ip, _ip, _i, _ip, _i, _vp, C.c_size_t],
+    "ekv_kvpack_parse": [_vp, C.c_size_t, C.POINTER(ekv_kvpack_info), _ip, _ip, _ip],
+    "ekv_kvpack_import": [_vp, _vp, C.c_size_t],
     "ekv_batch_destroy": [_vp],
     "ekv_batch_reset": [_vp],
     "ekv_batch_info": [_vp, _ip, _ip, _ip],

@@ -559,3 +559,49 @@ def compress_batched(ctx: Context, n: int, src_ptrs, rows: int, d_c: int, kept_t
     call("ekv_kv_compress_batched", ctx.h, n, C.cast(src_ptrs, C.POINTER(C.c_void_p)), rows, d_c,
          _ptr(kept_t), d_e, bits, group, C.cast(code_ptrs, C.POINTER(C.c_void_p)),
          C.cast(scale_ptrs, C.POINTER(C.c_void_p)))
+
+# ------------------------------------------------------------------ packed-KV wire format
+def fnv1a64(data: bytes | np.ndarray, seed: int = 14695981039346656037) -> int:
+    """The reference's fnv1a64 (rng.cpp:7-15) through the C ABI (host)."""
+    buf = np.ascontiguousarray(np.frombuffer(bytes(data), np.uint8) if isinstance(data, (bytes, bytearray))
+                               else data).view(np.uint8)
+    out = C.c_uint64()
+    call("ekv_fnv1a64", buf.ctypes.data_as(C.c_void_p), buf.nbytes, seed, C.byref(out))
+    return out.value
+
+
+def kvpack_size(n_layers: int, H: int, S: int, d_e: int, bits: int, group: int) -> int:
+    out = C.c_size_t()
+    call("ekv_kvpack_size", n_layers, H, S, d_e, bits, group, C.byref(out))
+    return out.value
+
+
+def kvpack_export(context: "AssembledContext", layers, cloud_layers, kept, d_c: int) -> torch.Tensor:
+    """The compressed `layers` of the context as one EKVPACK1 byte stream (pinned host uint8)."""
+    seg = context.segment(int(layers[0]))
+    m = context.model
+    n = len(layers)
+    size = kvpack_size(n, m.H, seg.S, m.d, seg.format, seg.group)
+    buf = torch.empty(size, dtype=torch.uint8).pin_memory()
+    ly = np.ascontiguousarray(layers, np.int32); cl = np.ascontiguousarray(cloud_layers, np.int32)
+    kp = np.ascontiguousarray(kept, np.int32)
+    call("ekv_kvpack_export", context.hnd, _ip(ly), _ip(cl), n, _ip(kp), d_c, C.c_void_p(buf.data_ptr()), size)
+    return buf
+
+
+def kvpack_parse(buf) -> dict:
+    """Validate a pack (host) and return its description."""
+    a = np.ascontiguousarray(buf.numpy() if isinstance(buf, torch.Tensor) else buf).view(np.uint8)
+    info = capi.ekv_kvpack_info()
+    call("ekv_kvpack_parse", a.ctypes.data_as(C.c_void_p), a.nbytes, C.byref(info), None, None, None)
+    n, de = info.n_layers, info.d_e
+    ly = np.zeros(n, np.int32); cl = np.zeros(n, np.int32); kp = np.zeros(de, np.int32)
+    call("ekv_kvpack_parse", a.ctypes.data_as(C.c_void_p), a.nbytes, C.byref(info), _ip(ly), _ip(cl), _ip(kp))
+    return {"n_layers": n, "H": info.H, "S": info.S, "d_e": de, "d_c": info.d_c, "bits": info.bits,
+            "group": info.group, "bytes": info.bytes, "layers": ly.tolist(), "cloud_layers": cl.tolist(),
+            "kept": kp.tolist()}
+
+
+def kvpack_import(context: "AssembledContext", buf) -> None:
+    a = buf if isinstance(buf, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(buf))
+    call("ekv_kvpack_import", context.hnd, C.c_void_p(a.data_ptr()), a.numel())
