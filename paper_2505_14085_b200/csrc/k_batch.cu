@@ -291,9 +291,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* full = bars;                 // [STAGES] TMA -> MMA (bf16) / expanders (int8)
     uint64_t* empty = bars + STAGES;       // [STAGES] MMA (bf16) / expanders (int8) -> TMA
     uint64_t* qready = bars + 2 * STAGES;  // softmax warps -> MMA (Q staged), count 4
-    uint64_t* sfull = qready + 1;          // MMA -> softmax (S in TMEM)
-    uint64_t* sfree = sfull + 1;           // softmax -> MMA (S read), count 4
-    uint64_t* pready = sfree + 1;          // softmax -> MMA (P staged), count 4
+    uint64_t* sfull = qready + 1;          // [2] MMA -> softmax (S buffer b in TMEM)
+    uint64_t* sfree = sfull + 2;           // [2] softmax -> MMA (S buffer b read), count 8
+    uint64_t* pready = sfree + 2;          // softmax -> MMA (P staged), count 8
     uint64_t* ofull = pready + 1;          // MMA -> softmax (O chunk in TMEM)
     uint64_t* xready = ofull + 1;          // [2] expanders -> MMA + softmax, count 2
     uint64_t* xfree = xready + 2;          // [2] MMA -> expanders
@@ -314,8 +314,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_init(&empty[i], Q8 ? 2 : 1);
         }
         mbar_init(qready, 8);
-        mbar_init(sfull, 1);
-        mbar_init(sfree, 8);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sfull[i], 1);
+            mbar_init(&sfree[i], 8);
+        }
         mbar_init(pready, 8);
         mbar_init(ofull, 1);
         for (int i = 0; i < 2; ++i) {
@@ -324,12 +326,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 256);
+    if (warp == 2) tmem_alloc(tmem_slot, 512);
     fence_before();
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t tS = tmem, tO = tmem + CH;  // S: 128 columns, O: D columns
+    // two S buffers (QK^T of chunk i+1 runs while chunk i is in the softmax) + O
+    const uint32_t tO = tmem + 2 * CH;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -363,29 +366,44 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t p0 = smem_u32(sP), p1 = p0 + C::P_BYTES;
             mbar_wait(qready, 0);
             fence_after();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int i = 0; i < nloc; ++i) {
-                uint32_t kb;
+            // K (and V) tiles of chunk j: the TMA stage (bf16) or the expanded buffer (int8)
+            auto kv_of = [&](int j) -> uint32_t {
                 if constexpr (Q8) {
-                    mbar_wait(&xready[i & 1], (i >> 1) & 1);
-                    kb = smem_u32(sX + (i & 1) * C::XBUF_BYTES);
+                    mbar_wait(&xready[j & 1], (j >> 1) & 1);
+                    return smem_u32(sX + (j & 1) * C::XBUF_BYTES);
                 } else {
-                    mbar_wait(&full[stage], phase);
-                    kb = smem_u32(sKV + stage * C::STAGE_BYTES);
+                    mbar_wait(&full[j % STAGES], (j / STAGES) & 1);
+                    return smem_u32(sKV + (j % STAGES) * C::STAGE_BYTES);
                 }
-                mbar_wait(sfree, (i & 1) ^ 1);  // S of the previous chunk consumed
+            };
+            auto issue_qk = [&](int j, uint32_t kb) {
+                mbar_wait(&sfree[j & 1], ((j >> 1) & 1) ^ 1);  // S buffer of chunk j-2 consumed
                 fence_after();
-                const uint32_t vb = kb + C::KV_BYTES;
+                const uint32_t tS = tmem + (j & 1) * CH;
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
                     const uint64_t bd = desc_sw128(kb + k * 32);
                     mma_bf16(tS, desc_sw128(q0 + k * 32), bd, idS, k > 0);
                     mma_bf16(tS, desc_sw128(q1 + k * 32), bd, idS, 1);
                 }
-                mma_commit(sfull);
+                mma_commit(&sfull[j & 1]);
+            };
+            uint32_t kb_cur = 0;
+            if (nloc > 0) {
+                kb_cur = kv_of(0);
+                issue_qk(0, kb_cur);
+            }
+            for (int i = 0; i < nloc; ++i) {
+                // S of the next chunk first: it runs on the tensor pipe while this chunk's
+                // softmax is computed
+                uint32_t kb_next = 0;
+                if (i + 1 < nloc) {
+                    kb_next = kv_of(i + 1);
+                    issue_qk(i + 1, kb_next);
+                }
                 mbar_wait(pready, i & 1);
                 fence_after();
+                const uint32_t vb = kb_cur + C::KV_BYTES;
                 // O = P V: K dimension = the 128 chunk rows (2 panels of 64), 16 per MMA;
                 // V rows are 128-byte MN-major rows, 8-row atoms 1024 B apart.
 #pragma unroll
@@ -396,15 +414,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mma_bf16(tO, desc_sw128(p1 + poff), vd, idO, 1);
                 }
                 mma_commit(ofull);
-                if constexpr (Q8) {
-                    mma_commit(&xfree[i & 1]);
-                } else {
-                    mma_commit(&empty[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
+                if constexpr (Q8) mma_commit(&xfree[i & 1]);
+                else mma_commit(&empty[i % STAGES]);
+                kb_cur = kb_next;
             }
         }
     } else if (warp < 4) {
@@ -518,6 +530,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) o[i] = 0.0f;
         const uint32_t ph = smem_u32(sP) + half * (BT * 128), pl = ph + C::P_BYTES;
+        float alpha_prev = 0.0f;
         for (int i = 0; i < nloc; ++i) {
             const int cbase = (c0 + i) * CH + half * 64;
             const int valid = min(64, a.S - cbase);  // may be <= 0 for the last chunk's upper half
@@ -528,15 +541,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 ksc = reinterpret_cast<const float*>(sX + (i & 1) * C::XBUF_BYTES + 2 * C::KV_BYTES) + half * 64;
                 vsc = ksc + CH;
             }
-            mbar_wait(sfull, i & 1);
+            mbar_wait(&sfull[i & 1], (i >> 1) & 1);
             fence_after();
+            const uint32_t tS = tmem + (i & 1) * CH;
             if (!warp_live) {  // no session in these 32 rows: their P rows and O rows are never used
+                if (i > 0) mbar_wait(ofull, (i - 1) & 1);  // P is rewritten below
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(sfree);
+                    mbar_arrive(&sfree[i & 1]);
                     mbar_arrive(pready);
                 }
-                mbar_wait(ofull, i & 1);
                 continue;
             }
             // pass 1: row max over this warp's 64 columns, exchanged with the partner warp
@@ -558,6 +572,17 @@ __global__ void __launch_bounds__(THREADS, 1)
             mx = fmaxf(fmaxf(mx, xm[(half ^ 1) * BT + r]), m);
             const float alpha = (m == -INFINITY) ? 0.0f : exp2f((m - mx) * L2E);
             const float mxs = mx * L2E;
+            // the previous chunk's O (deferred: its PV ran while this chunk's S was read);
+            // P of this chunk may be written only once that PV has finished
+            if (i > 0) {
+                mbar_wait(ofull, (i - 1) & 1);
+                fence_after();
+                float v[32];
+                tmem_ld32(tO + lane_off + half * 32, v);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] = o[e] * alpha_prev + v[e];
+                fence_before();
+            }
             // pass 2: p = exp(s - max), P (times the V row scale for int8) as hi / lo bf16
             float rs = 0.0f;
 #pragma unroll
@@ -590,21 +615,22 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             m = mx;
             l = l * alpha + rs;
+            alpha_prev = alpha;
             fence_async_smem();
             fence_before();
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(sfree);
+                mbar_arrive(&sfree[i & 1]);
                 mbar_arrive(pready);
             }
-            mbar_wait(ofull, i & 1);
+        }
+        if (nloc > 0 && warp_live) {  // the last chunk's O
+            mbar_wait(ofull, (nloc - 1) & 1);
             fence_after();
-            {
-                float v[32];
-                tmem_ld32(tO + lane_off + half * 32, v);
+            float v[32];
+            tmem_ld32(tO + lane_off + half * 32, v);
 #pragma unroll
-                for (int e = 0; e < 32; ++e) o[e] = o[e] * alpha + v[e];
-            }
+            for (int e = 0; e < 32; ++e) o[e] = o[e] * alpha_prev + v[e];
             fence_before();
         }
         // row sum = both halves' partial sums (same running max in both warps)
@@ -623,7 +649,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     fence_before();
     __syncthreads();
     fence_after();
-    if (warp == 2) tmem_dealloc(tmem, 256);
+    if (warp == 2) tmem_dealloc(tmem, 512);
 }
 }  // namespace k10
 
