@@ -44,6 +44,43 @@ constexpr int kMaxSplitK = 16;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 / FMUL2), IEEE per lane
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x f2pack(float lo, float hi) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float f2lo(f2x v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return lo;
+}
+__device__ __forceinline__ float f2hi(f2x v) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return hi;
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2x fadd2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// a bf16 pair word -> {low element, high element} as fp32
+__device__ __forceinline__ f2x bf16x2_to_f2(uint32_t w) {
+    return f2pack(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+}
+
 // sum of the KS split-K partials of 4 consecutive floats (16-byte aligned); every
 // load is issued before the first add (the split loop is unrolled to kMaxSplitK
 // with a predicate), so the sum costs one memory round trip, not KS.
@@ -585,32 +622,71 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             // pass 2: p = exp(s - max), P (times the V row scale for int8) as hi / lo bf16
             float rs = 0.0f;
+            if (valid >= 64) {
+                // full 64 columns: packed fp32x2 arithmetic, hi / lo split two at a time
+                const f2x l2e2 = f2pack(L2E, L2E), nm2 = f2pack(-mxs, -mxs), neg2 = f2pack(-1.0f, -1.0f);
+                f2x rs2 = 0ull;
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                float sv[32];
-                tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
+                for (int c = 0; c < 2; ++c) {
+                    float sv[32];
+                    tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
 #pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint16_t hi[8], lo[8];
+                    for (int g = 0; g < 4; ++g) {
+                        uint32_t hw[4], lw[4];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int j = c * 32 + g * 8 + e;
-                        float x = sv[g * 8 + e];
-                        if constexpr (Q8) x *= ksc[j];
-                        float p;
-                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"(fmaf(x, L2E, -mxs)));
-                        p = (j < valid) ? p : 0.0f;
-                        rs += p;
-                        // O = sum p * (code * vscale): fold the V row scale into P
-                        const float pv = Q8 ? p * vsc[j] : p;
-                        split_bf16(pv, hi[e], lo[e]);
+                        for (int e = 0; e < 8; e += 2) {
+                            const int j = c * 32 + g * 8 + e;
+                            f2x x2 = f2pack(sv[g * 8 + e], sv[g * 8 + e + 1]);
+                            if constexpr (Q8) x2 = fmul2(x2, f2pack(ksc[j], ksc[j + 1]));
+                            const f2x a2 = ffma2(x2, l2e2, nm2);
+                            float p0, p1;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(f2lo(a2)));
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(f2hi(a2)));
+                            f2x p2 = f2pack(p0, p1);
+                            rs2 = fadd2(rs2, p2);
+                            if constexpr (Q8) p2 = fmul2(p2, f2pack(vsc[j], vsc[j + 1]));
+                            uint32_t h;
+                            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(f2hi(p2)), "f"(f2lo(p2)));
+                            const f2x r2 = ffma2(bf16x2_to_f2(h), neg2, p2);  // exact residual
+                            uint32_t lo2;
+                            asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo2) : "f"(f2hi(r2)), "f"(f2lo(r2)));
+                            hw[e / 2] = h;
+                            lw[e / 2] = lo2;
+                        }
+                        const uint32_t off = sw128_off(r, c * 4 + g);
+                        st_shared_v4(ph + off, hw[0], hw[1], hw[2], hw[3]);
+                        st_shared_v4(pl + off, lw[0], lw[1], lw[2], lw[3]);
                     }
-                    const int cc = c * 4 + g;  // 16-byte chunk of this warp's 64-row P panel
-                    const uint32_t off = sw128_off(r, cc);
-                    st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
-                                 pack2(hi[6], hi[7]));
-                    st_shared_v4(pl + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
-                                 pack2(lo[6], lo[7]));
+                }
+                rs = f2lo(rs2) + f2hi(rs2);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float sv[32];
+                    tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        uint16_t hi[8], lo[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int j = c * 32 + g * 8 + e;
+                            float x = sv[g * 8 + e];
+                            if constexpr (Q8) x *= ksc[j];
+                            float p;
+                            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p) : "f"(fmaf(x, L2E, -mxs)));
+                            p = (j < valid) ? p : 0.0f;
+                            rs += p;
+                            // O = sum p * (code * vscale): fold the V row scale into P
+                            const float pv = Q8 ? p * vsc[j] : p;
+                            split_bf16(pv, hi[e], lo[e]);
+                        }
+                        const int cc = c * 4 + g;  // 16-byte chunk of this warp's 64-row P panel
+                        const uint32_t off = sw128_off(r, cc);
+                        st_shared_v4(ph + off, pack2(hi[0], hi[1]), pack2(hi[2], hi[3]), pack2(hi[4], hi[5]),
+                                     pack2(hi[6], hi[7]));
+                        st_shared_v4(pl + off, pack2(lo[0], lo[1]), pack2(lo[2], lo[3]), pack2(lo[4], lo[5]),
+                                     pack2(lo[6], lo[7]));
+                    }
                 }
             }
             m = mx;
