@@ -592,16 +592,23 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             // pass 1: row max over this warp's 64 columns, exchanged with the partner warp
             float mx = -INFINITY;
+            {
+                float mq[8];  // 8 independent max chains (short dependency chains)
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                float sv[32];
-                tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
+                for (int e = 0; e < 8; ++e) mq[e] = -INFINITY;
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    float x = sv[e];
-                    if constexpr (Q8) x *= ksc[c * 32 + e];  // scores of dequantised K = scale * (q . code)
-                    if (c * 32 + e < valid) mx = fmaxf(mx, x);
+                for (int c = 0; c < 2; ++c) {
+                    float sv[32];
+                    tmem_ld32(tS + lane_off + half * 64 + c * 32, sv);
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        float x = sv[e];
+                        if constexpr (Q8) x *= ksc[c * 32 + e];  // scores of dequantised K = scale * (q . code)
+                        if (valid >= 64 || c * 32 + e < valid) mq[e & 7] = fmaxf(mq[e & 7], x);
+                    }
                 }
+                mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                           fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
             }
             float* xm = xch + (i & 1) * 2 * BT;
             xm[half * BT + r] = mx;
