@@ -979,7 +979,7 @@ int batch_proj_bn(int B) {
 
 int batch_proj_splits(int N_out, int K, int B, int num_sms) {
     const int tiles = (N_out / k9::BM) * ((B + batch_proj_bn(B) - 1) / batch_proj_bn(B));
-    int ks = (num_sms + tiles / 2) / tiles;
+    int ks = num_sms / tiles;  // floor: a second partial wave costs more than fewer splits
     const int kblocks = K / k9::BK;
     if (ks < 1) ks = 1;
     if (ks > kblocks) ks = kblocks;
