@@ -739,8 +739,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 // ============================================================================
 // K11: user segment + append + Eq. 5 merge, one warp per (session, head).
 // ============================================================================
-template <int D>
-__global__ void __launch_bounds__(128, 3) batch_user_merge_kernel(BatchUserMerge a) {
+template <int D, int NV>  // NV: split-K partials of the QKV projection held in flight
+__global__ void __launch_bounds__(128, NV == 1 ? 4 : 3) batch_user_merge_kernel(BatchUserMerge a) {
     constexpr int G = D / 8;         // lanes per row (8 dims = 16 bytes per lane)
     constexpr int RPI = 32 / G;      // rows per warp-wide load
     constexpr int NT = 32 / RPI;     // rows per lane per 32-row block
@@ -759,7 +759,6 @@ __global__ void __launch_bounds__(128, 3) batch_user_merge_kernel(BatchUserMerge
     // ---- every independent load issued before the first use: the user-row count,
     //      this step's q/k/v partials, the first 32 user rows, the context partials ----
     const int ulen = a.state->user_len;
-    constexpr int NV = 3;  // split-K partials held in flight; more are summed by a plain loop
     const size_t stride = (size_t)a.B * a.n_qkv;
     const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
     float4 v[NV][3][2];
@@ -1110,9 +1109,18 @@ void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st) {
     const int items = a.B * a.H;
     const int grid = (items + 3) / 4;
     switch (a.D) {
-        case 32: launch_pdl(batch_user_merge_kernel<32>, dim3(grid), dim3(128), 0, st, a); break;
-        case 64: launch_pdl(batch_user_merge_kernel<64>, dim3(grid), dim3(128), 0, st, a); break;
-        case 128: launch_pdl(batch_user_merge_kernel<128>, dim3(grid), dim3(128), 0, st, a); break;
+        case 32:
+            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<32, 1>, dim3(grid), dim3(128), 0, st, a);
+            else launch_pdl(batch_user_merge_kernel<32, 3>, dim3(grid), dim3(128), 0, st, a);
+            break;
+        case 64:
+            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<64, 1>, dim3(grid), dim3(128), 0, st, a);
+            else launch_pdl(batch_user_merge_kernel<64, 3>, dim3(grid), dim3(128), 0, st, a);
+            break;
+        case 128:
+            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<128, 1>, dim3(grid), dim3(128), 0, st, a);
+            else launch_pdl(batch_user_merge_kernel<128, 3>, dim3(grid), dim3(128), 0, st, a);
+            break;
         default: require(false, "batched decode: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
     }
     EKV_CUDA(cudaGetLastError());
