@@ -202,16 +202,28 @@ __global__ void __launch_bounds__(THREADS, 1)
         pdl_wait();  // the partial buffer may still be read by the previous kernel's consumers
         mbar_wait(tfull, 0);
         fence_after();
-        const int n = mt * BM + quad * 32 + lane;
         const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16);
-        float* o = out + (size_t)ks * B * N_out + n;
+        // 32 sessions at a time through shared memory (the drained ring), transposed so
+        // each session's 128 outputs leave as 16-byte stores
+        constexpr int TS = BM + 4;
+        float* tile = reinterpret_cast<float*>(smem);  // [32][TS]
+        const int t = threadIdx.x - 128;
+        float* o = out + (size_t)ks * B * N_out + mt * BM;
         for (int c = 0; c < BN / 32; ++c) {
             float v[32];
             tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) tile[i * TS + quad * 32 + lane] = v[i];
+            asm volatile("bar.sync 1, 128;" ::: "memory");
             const int b0 = nt * BN + c * 32;
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (b0 + i < B && n < N_out) o[(size_t)(b0 + i) * N_out] = v[i];
+            for (int k = 0; k < 8; ++k) {
+                const int i = t / 32 + 4 * k, n4 = t % 32;
+                if (b0 + i < B)
+                    *reinterpret_cast<float4*>(o + (size_t)(b0 + i) * N_out + n4 * 4) =
+                        *reinterpret_cast<const float4*>(tile + i * TS + n4 * 4);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
         }
     }
     pdl_trigger();
