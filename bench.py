@@ -22,8 +22,12 @@ Also reported (same run): e2e through the reference-facing C-ABI call
 ekv_collaborative_decode with pinned HOST buffers (H2D of the user prompt and
 D2H of every output row inside the timed region), the roofline of the dominant
 kernel (CUDA events on its stream), align+compress (K1 tensor-pipe, K3 HBM),
-clocks sampled by NVML during the timed region, the kernel-launch count, and
-the CPU baseline (the reference compiled from source, oracle/_ref).
+clocks sampled by NVML during the timed region, the kernel-launch count, the
+CPU baseline (the reference compiled from source, oracle/_ref), and two
+secondary configurations: `concurrency` (configs[2]: --sessions concurrent
+sessions per GPU on the batched path, plus a --sweep of other counts) and
+`long_context_pipeline` (configs[3]: S = 32768, the cloud layers streamed from
+pinned host memory while the prompt is forwarded; rank 0 only).
 """
 from __future__ import annotations
 
