@@ -4,6 +4,8 @@
 // All of these are HBM-bound byte/integer work: 128-bit or row-wide coalesced
 // loads, one warp per row, warp-shuffle reductions, grid sized to a multiple
 // of the SM count (grid-stride loops).  No tensor cores.
+#include <string>
+
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
 
@@ -63,18 +65,25 @@ struct TileCfg {
     static constexpr int TILE = 8192 / DC;              // rows per stage (16 KB)
     static constexpr int BYTES = TILE * DC * 2;         // 16 KB
 };
+template <int DC, int TB>
+struct TileCfgB {                                       // TB-byte stages
+    static constexpr int TILE = TB / (2 * DC);
+    static constexpr int BYTES = TILE * DC * 2;
+};
 constexpr int kCompressStages = 2;
+// 8 KB stages: more CTAs per SM beat deeper rings (C2, 11 layers x K/V, measured:
+// 8 KB x 2 = 4.75-4.80 TB/s; 16 KB x 2 4.61; 8 KB x 3 4.70; 4 KB x 2 4.22; 16 KB x 4 3.33)
+constexpr int kCompressTileBytes = 8192;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-template <int DC, int DE, int BITS>
+template <int DC, int DE, int BITS, int TB = kCompressTileBytes, int NS = kCompressStages>
 __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs, int n_jobs, int64_t rows,
                                                                const int* __restrict__ kept,
                                                                int group) {
-    using TC = TileCfg<DC>;
-    constexpr int NS = kCompressStages;
+    using TC = TileCfgB<DC, TB>;
     constexpr int LPR = DE / 8, RPW = 32 / LPR, NWARP = 4;
     constexpr int PASSES = TC::TILE / (RPW * NWARP);
     constexpr float Q = BITS == 8 ? 127.0f : 7.0f;
@@ -224,7 +233,7 @@ static int grid_for(int64_t work, int per_block) {
     return (int)b;
 }
 
-template <int DC, int DE, int BITS>
+template <int DC, int DE, int BITS, int TB = kCompressTileBytes, int NS = kCompressStages>
 static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c, const int* kept,
                      int d_e, int group, cudaStream_t st) {
     if (d_c != DC || d_e != DE) return false;
@@ -235,9 +244,10 @@ static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c
     for (int i = 0; i < n_jobs; ++i)  // bulk copies need 16-byte aligned sources
         if (((uintptr_t)jobs.job[i].src & 15) || ((uintptr_t)jobs.job[i].codes & 7))
             return false;
-    const int64_t total = (rows + TileCfg<DC>::TILE - 1) / TileCfg<DC>::TILE * n_jobs;
-    auto fn = kv_compress_tile_kernel<DC, DE, BITS>;
-    const int smem = kCompressStages * TileCfg<DC>::BYTES + 64;
+    using TC = TileCfgB<DC, TB>;
+    const int64_t total = (rows + TC::TILE - 1) / TC::TILE * n_jobs;
+    auto fn = kv_compress_tile_kernel<DC, DE, BITS, TB, NS>;
+    const int smem = NS * TC::BYTES + 64;
     static int occ = 0, sms = 0;
     if (!occ) {
         EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
