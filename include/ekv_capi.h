@@ -281,7 +281,8 @@ int ekv_session_set_decode_path(ekv_session_t s, int path, int* active);
  * the consumer warps in the QKV, attention and output-projection phases.
  * out[(L*G + g)*16 + k]: 0 CTA start, 1/2 producer start/end (ns), 3 stages
  * issued, 4 producer cycles waiting for free ring slots, 5 producer cycles.
- * Needs capacity >= 16*(L+1)*G. */
+ * G = the persistent kernel's grid (the largest multiple of H <= the SM count);
+ * n_out = 16*(L+1)*G.  Needs capacity >= 16*(L+1)*(SM count). */
 int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_out);
 /* One decode step launched kernel by kernel with CUDA events between the
  * launches (diagnostics / roofline attribution; the step is real and advances

@@ -36,6 +36,8 @@
 // data are neighbours, and each CTA touches at most two heads per phase.
 #include <math_constants.h>
 
+#include <cstdlib>
+
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
 #include "ekv_mega.h"
@@ -1293,7 +1295,20 @@ static void launch_d(const MegaArgs& a, int grid, int kc, cudaStream_t st) {
     }
 }
 
+// Grid = the largest multiple of the head count that fits the SMs: every head then
+// gets the same number of attention CTAs, so no head's merge waits for a CTA that
+// carries a larger share (C2, 32 heads: 128 CTAs = 3149 tok/s vs 148 CTAs = 2840).
+int mega_grid(int H, int num_sms) {
+    int g = H <= num_sms ? num_sms / H * H : num_sms;
+    if (const char* e = getenv("EKV_MEGA_GRID")) {  // experiments
+        const int v = atoi(e);
+        if (v >= 1 && v < g) g = v;
+    }
+    return g;
+}
+
 void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st) {
+    num_sms = mega_grid(a.H, num_sms);
     require(num_sms <= 160, "decode megakernel: at most 160 SMs", EKV_EUNSUPPORTED);
     require(a.H * a.D >= num_sms, "decode megakernel: hidden size below the SM count", EKV_EUNSUPPORTED);
     const int kc = a.H * a.D / 256;

@@ -414,7 +414,7 @@ class Session:
         got = C.c_int()
         call("ekv_session_trace_step", self.hnd, out.ctypes.data_as(C.POINTER(C.c_uint64)), n,
              C.byref(got))
-        return out
+        return out[:got.value]  # [L+1][G][16], G = the kernel's grid
 
     def profile_step(self) -> np.ndarray:
         """One real decode step with CUDA-event times (ms).  Graph path: [3l] QKV projection,

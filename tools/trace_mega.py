@@ -12,7 +12,9 @@ kvc = ek.AssembledContext(m, S, [16] * (L - DEEP) + [8] * DEEP, group=d); kvc.sy
 sess = ek.Session(m, kvc, 128)
 sess.forward(torch.zeros((16, H * d), device="cuda"))
 sess.decode(3)
-t = sess.trace_step(G).astype(np.int64).reshape(L + 1, G, 16)
+t = sess.trace_step(G).astype(np.int64)
+G = t.size // (16 * (L + 1))  # the kernel's grid (a multiple of the head count)
+t = t.reshape(L + 1, G, 16)
 st = t[:L, :, :8]
 start = t[L, :, 0]
 t0 = start.min()
