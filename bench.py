@@ -27,7 +27,9 @@ CPU baseline (the reference compiled from source, oracle/_ref), and two
 secondary configurations: `concurrency` (configs[2]: --sessions concurrent
 sessions per GPU on the batched path, plus a --sweep of other counts) and
 `long_context_pipeline` (configs[3]: S = 32768, the cloud layers streamed from
-pinned host memory while the prompt is forwarded; rank 0 only).
+pinned host memory while the prompt is forwarded; rank 0 only) and
+`compression_sweep` (configs[4]: int8 / int4 codes at 2:1 and 4:1 cloud:edge
+layer ratios -- K3 compression GB/s and K8 decode tok/s; rank 0 only).
 """
 from __future__ import annotations
 
@@ -543,6 +545,69 @@ def run_b200(args, rank: int, world: int, local_rank: int):
         except Exception as e:  # noqa: BLE001
             c4 = {"error": str(e)[:300]}
 
+    # --- C5 (BASELINE configs[4]): int8 vs int4 codes and 2:1 / 4:1 cloud:edge layer ratios
+    #     (Llama-3-8B-shaped cloud 32L x 32x128 -> 1B-shaped edge 32x64 with 16 or 8 layers,
+    #     half of them from the cloud): K3 compression of the deep layers and K8 decode ---
+    c5 = None
+    if not args.no_c5 and rank == 0:
+        try:
+            import ctypes as C
+            rows_c5 = []
+            Kd = 200
+            for Le, bits in ((16, 8), (16, 4), (8, 8), (8, 4)):
+                deep = Le // 2
+                grp = d if bits == 8 else 32
+                m5 = ek.EdgeModel(ctx, Le, H, d, S + U + Kd + 16)
+                m5.synthesize(seed=77)
+                fm = [ek.EKV_KV_BF16] * (Le - deep) + [bits] * deep
+                kv5 = ek.AssembledContext(m5, S, fm, group=grp)
+                kv5.synthesize(seed=78)
+                # compression of the deep layers from 128-wide cloud heads (mask 128 -> 64)
+                srcs = [torch.empty((Hc, S, dc), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+                for j, t in enumerate(srcs):
+                    ctx.fill_uniform_bf16(t, 79, j, -1.0, 1.0)
+                kept5 = torch.arange(0, dc, 2, dtype=torch.int32, device="cuda")
+                sp, cp, scp = [], [], []
+                for le in range(Le - deep, Le):
+                    seg = kv5.segment(le)
+                    sp += [srcs[0].data_ptr(), srcs[1].data_ptr()]
+                    cp += [seg.k, seg.v]
+                    scp += [seg.k_scales, seg.v_scales]
+                arr = lambda xs: (C.c_void_p * len(xs))(*xs)
+                js, jc, jsc = arr(sp), arr(cp), arr(scp)
+                ctx.synchronize()
+                times = []
+                for it in range(4):
+                    torch.cuda.synchronize()
+                    with torch.cuda.stream(st):
+                        torch.cuda._sleep(200_000)
+                    e0.record(st)
+                    ek.compress_batched(ctx, len(sp), js, Hc * S, dc, kept5, d, bits, grp, jc, jsc)
+                    e1.record(st)
+                    st.synchronize()
+                    if it:
+                        times.append(e0.elapsed_time(e1))
+                k3ms = statistics.median(times)
+                k3b = deep * 2 * (Hc * S * dc * 2 + Hc * S * d * bits // 8 + Hc * S * (d // grp) * 4)
+                s5 = ek.Session(m5, kv5, U + Kd + 8)
+                s5.forward(torch.empty((U, h), dtype=torch.float32, device="cuda").uniform_(-1, 1))
+                s5.decode(5)
+                torch.cuda.synchronize()
+                e0.record(st)
+                s5.decode(Kd, sync=False)
+                e1.record(st)
+                st.synchronize()
+                dms = e0.elapsed_time(e1) / Kd
+                rows_c5.append({"edge_layers": Le, "cloud_layers": CLOUD["L"], "ratio": f"{CLOUD['L'] // Le}:1",
+                                "deep_layers": deep, "bits": bits, "group": grp,
+                                "compress_gbs": k3b / (k3ms * 1e-3) / 1e9,
+                                "compress_frac": k3b / (k3ms * 1e-3) / 1e9 / hbm,
+                                "decode_tok_s": 1e3 / dms, "decode_path": s5.set_decode_path("mega")})
+                del s5, kv5, m5, srcs
+            c5 = rows_c5
+        except Exception as e:  # noqa: BLE001
+            c5 = {"error": str(e)[:300]}
+
     # --- CPU baseline (rank 0, N=1 only) ---
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -576,6 +641,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             "align_compress": align,
             "concurrency": conc,
             "long_context_pipeline": c4,
+            "compression_sweep": c5,
             "kv_transfer": kv_transfer,
             "outputs_finite": finite,
         }
@@ -595,6 +661,7 @@ def main():
     ap.add_argument("--sweep", type=lambda v: [int(x) for x in v.split(",") if x], default=[64, 256, 512, 1024],
                     help="other C3 session counts per GPU measured briefly")
     ap.add_argument("--no-c4", action="store_true", help="skip the 32k pipelined-prefill block")
+    ap.add_argument("--no-c5", action="store_true", help="skip the int8/int4, 2:1/4:1 block")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
