@@ -46,12 +46,20 @@ void launch_prefill_finish(const PrefillFinish& a, cudaStream_t st);
 struct BatchCtxAttn {
     int B, H, D, S, nsplit, KS, n_qkv;
     const float* qkv;      // [KS][B][n_qkv] partials of the QKV projection (q at column 0)
-    float* part;           // [B][H][nsplit][D + 2]  (m, l, o[D]) unnormalised
+    float* part;           // [B][H][nsplit][D + 4]  (m, l, -, -, o[D]) unnormalised
+    // finalisation of this row's q / k / v (optional, qfin != null): q summed into
+    // qfin [B][h]; k, v summed, rounded to bf16 and appended to the user caches
+    float* qfin;
+    uint16_t* uk;          // [B][L][H][cap][D]
+    uint16_t* uv;
+    int L, layer, cap;
+    const DevState* state;
 };
 
 struct BatchUserMerge {
     int B, H, D, L, layer, cap, KS, n_qkv, nsplit;
     const float* qkv;      // [KS][B][3h]
+    const float* qfin;     // non-null: q from qfin [B][h], k / v already appended by K10
     const float* part;     // context partials (nsplit may be 0)
     uint16_t* uk;          // [B][L][H][cap][D]
     uint16_t* uv;

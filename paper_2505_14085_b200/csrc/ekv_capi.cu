@@ -632,6 +632,8 @@ struct ekv_batch_s {
     float* qkv = nullptr;     // [KSq][B][3h]
     float* xpart = nullptr;   // [KSo][B][h]
     float* part = nullptr;    // [B][H][nsplit][D+4]: m, l, -, -, o[D]
+    float* qfin = nullptr;    // [B][h] this row's q (finalised by the context kernel)
+    bool use_qfin = true;     // K10 finalises q/k/v (worth it while the QKV projection is split)
     DevState* state = nullptr;
     CUtensorMap map_w{}, map_x{};
     std::vector<BatchCtxMaps> maps;   // per context layer
@@ -681,6 +683,13 @@ void batch_row(ekv_batch_s* b, cudaStream_t st, cudaEvent_t* ev = nullptr) {
             a.n_qkv = 3 * h;
             a.qkv = b->qkv;
             a.part = b->part;
+            a.qfin = b->use_qfin ? b->qfin : nullptr;
+            a.uk = b->uk;
+            a.uv = b->uv;
+            a.L = L;
+            a.layer = l;
+            a.cap = b->cap;
+            a.state = b->state;
             launch_batch_ctx_attn(b->maps[l], a, st);
         }
         mark();
@@ -695,6 +704,7 @@ void batch_row(ekv_batch_s* b, cudaStream_t st, cudaEvent_t* ev = nullptr) {
         u.n_qkv = 3 * h;
         u.nsplit = ns;
         u.qkv = b->qkv;
+        u.qfin = (ns > 0 && b->use_qfin) ? b->qfin : nullptr;
         u.part = b->part;
         u.uk = b->uk;
         u.uv = b->uv;
@@ -723,7 +733,8 @@ void batch_row(ekv_batch_s* b, cudaStream_t st, cudaEvent_t* ev = nullptr) {
 
 void batch_free(ekv_batch_s* b) {
     for (void* p : {(void*)b->uk, (void*)b->uv, (void*)b->xin, (void*)b->hist, (void*)b->emb,
-                    (void*)b->xhl, (void*)b->qkv, (void*)b->xpart, (void*)b->part, (void*)b->state})
+                    (void*)b->xhl, (void*)b->qkv, (void*)b->xpart, (void*)b->part, (void*)b->qfin,
+                    (void*)b->state})
         if (p) cudaFree(p);
 }
 
@@ -746,6 +757,9 @@ void batch_alloc(ekv_batch_s* b) {
     b->qkv = dalloc<float>((size_t)b->KSq * B * 3 * h);
     b->xpart = dalloc<float>((size_t)b->KSo * B * h);
     b->part = dalloc<float>((size_t)B * H * std::max(b->nsplit, 1) * (D + 4));
+    b->qfin = dalloc<float>((size_t)B * h);
+    b->use_qfin = b->KSq > 1;
+    if (const char* e = getenv("EKV_BATCH_QFIN")) b->use_qfin = atoi(e) != 0;  // experiments
     b->state = dalloc<DevState>(1);
     EKV_CUDA(cudaMemset(b->uk, 0, sizeof(uint16_t) * ukv));
     EKV_CUDA(cudaMemset(b->uv, 0, sizeof(uint16_t) * ukv));

@@ -557,6 +557,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                             a.qkv + (size_t)bb * a.n_qkv + hd * D + c4 * 4 + s2 * stride);
                         x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
                     }
+                    if (a.qfin && split == 0 && bb < a.B)
+                        *reinterpret_cast<float4*>(a.qfin + (size_t)bb * (a.n_qkv / 3) + hd * D + c4 * 4) = x;
                     uint16_t hi[4], lo[4];
                     split_bf16(x.x, hi[0], lo[0]);
                     split_bf16(x.y, hi[1], lo[1]);
@@ -572,6 +574,33 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(qready);
+        }
+        // this row's k / v of head hd for this split's share of the session tile: split-K
+        // sum, bf16 rounding, append to the user caches (K11 then reads them back)
+        if (a.qfin) {
+            const int t = threadIdx.x - 128;
+            const int h = a.n_qkv / 3;
+            const size_t stride = (size_t)a.B * a.n_qkv;
+            const int ulen = a.state->user_len;
+            const int rA = split * BT / a.nsplit, rB = (split + 1) * BT / a.nsplit;
+            for (int u = t; u < (rB - rA) * 2 * (D / 4); u += 256) {
+                const int row = rA + u / (2 * (D / 4));
+                const int rem = u - (row - rA) * 2 * (D / 4);
+                const int kv = rem / (D / 4), c4 = rem - kv * (D / 4);
+                const int bb = bt * BT + row;
+                if (bb >= a.B) continue;
+                const float* src = a.qkv + (size_t)bb * a.n_qkv + (1 + kv) * h + hd * D + c4 * 4;
+                float4 x = *reinterpret_cast<const float4*>(src);
+                for (int s2 = 1; s2 < a.KS; ++s2) {
+                    const float4 y = *reinterpret_cast<const float4*>(src + s2 * stride);
+                    x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+                }
+                uint16_t* dst = (kv == 0 ? a.uk : a.uv) +
+                                ((((size_t)bb * a.L + a.layer) * a.H + hd) * a.cap + ulen) * D + c4 * 4;
+                *reinterpret_cast<uint2*>(dst) =
+                    make_uint2(f32_to_bf16_bits(x.x) | ((uint32_t)f32_to_bf16_bits(x.y) << 16),
+                               f32_to_bf16_bits(x.z) | ((uint32_t)f32_to_bf16_bits(x.w) << 16));
+            }
         }
         constexpr float L2E = 1.4426950408889634f;
         float m = -INFINITY, l = 0.0f;
@@ -774,11 +803,12 @@ __global__ void __launch_bounds__(128, NV == 1 ? 4 : 3) batch_user_merge_kernel(
     const size_t stride = (size_t)a.B * a.n_qkv;
     const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
     float4 v[NV][3][2];
+    const int ksl = a.qfin ? 0 : a.KS;  // partials to load (none when K10 finalised q/k/v)
 #pragma unroll
     for (int s = 0; s < NV; ++s)
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
-            if (s < a.KS) {
+            if (s < ksl) {
                 v[s][t][0] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h);
                 v[s][t][1] = *reinterpret_cast<const float4*>(p0 + s * stride + t * h + 4);
             } else {
@@ -805,7 +835,19 @@ __global__ void __launch_bounds__(128, NV == 1 ? 4 : 3) batch_user_merge_kernel(
         if (s < a.nsplit) pml[s] = *reinterpret_cast<const float2*>(wpart + s * (D + 4));
     // ---- q, k, v (k, v rounded to bf16 as stored) ----
     float q[8], kc[8], vc[8];
-    {
+    if (a.qfin) {  // finalised by the context kernel: q from qfin, k / v already in the cache
+        const float4 q0 = *reinterpret_cast<const float4*>(a.qfin + (size_t)b * h + hd * D + c * 8);
+        const float4 q1 = *reinterpret_cast<const float4*>(a.qfin + (size_t)b * h + hd * D + c * 8 + 4);
+        q[0] = q0.x; q[1] = q0.y; q[2] = q0.z; q[3] = q0.w; q[4] = q1.x; q[5] = q1.y; q[6] = q1.z; q[7] = q1.w;
+        const uint4 kw = *reinterpret_cast<const uint4*>(uk + (size_t)ulen * D + c * 8);
+        const uint4 vw = *reinterpret_cast<const uint4*>(uv + (size_t)ulen * D + c * 8);
+        const uint32_t kk[4] = {kw.x, kw.y, kw.z, kw.w}, vv[4] = {vw.x, vw.y, vw.z, vw.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            kc[2 * k] = bf16_lo(kk[k]); kc[2 * k + 1] = bf16_hi(kk[k]);
+            vc[2 * k] = bf16_lo(vv[k]); vc[2 * k + 1] = bf16_hi(vv[k]);
+        }
+    } else {
         for (int s = NV; s < a.KS; ++s)
 #pragma unroll
             for (int t = 0; t < 3; ++t) {
@@ -836,7 +878,7 @@ __global__ void __launch_bounds__(128, NV == 1 ? 4 : 3) batch_user_merge_kernel(
         }
     }
     // append (cache_merge.cpp:189-199): row ulen of this session's user cache
-    if (grp == 0) {
+    if (grp == 0 && !a.qfin) {
         uint4 kw, vw;
         kw.x = f32_to_bf16_bits(kc[0]) | ((uint32_t)f32_to_bf16_bits(kc[1]) << 16);
         kw.y = f32_to_bf16_bits(kc[2]) | ((uint32_t)f32_to_bf16_bits(kc[3]) << 16);
@@ -1122,15 +1164,15 @@ void launch_batch_user_merge(const BatchUserMerge& a, cudaStream_t st) {
     const int grid = (items + 3) / 4;
     switch (a.D) {
         case 32:
-            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<32, 1>, dim3(grid), dim3(128), 0, st, a);
+            if (a.KS == 1 || a.qfin) launch_pdl(batch_user_merge_kernel<32, 1>, dim3(grid), dim3(128), 0, st, a);
             else launch_pdl(batch_user_merge_kernel<32, 3>, dim3(grid), dim3(128), 0, st, a);
             break;
         case 64:
-            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<64, 1>, dim3(grid), dim3(128), 0, st, a);
+            if (a.KS == 1 || a.qfin) launch_pdl(batch_user_merge_kernel<64, 1>, dim3(grid), dim3(128), 0, st, a);
             else launch_pdl(batch_user_merge_kernel<64, 3>, dim3(grid), dim3(128), 0, st, a);
             break;
         case 128:
-            if (a.KS == 1) launch_pdl(batch_user_merge_kernel<128, 1>, dim3(grid), dim3(128), 0, st, a);
+            if (a.KS == 1 || a.qfin) launch_pdl(batch_user_merge_kernel<128, 1>, dim3(grid), dim3(128), 0, st, a);
             else launch_pdl(batch_user_merge_kernel<128, 3>, dim3(grid), dim3(128), 0, st, a);
             break;
         default: require(false, "batched decode: head_dim must be 32, 64 or 128", EKV_EUNSUPPORTED);
