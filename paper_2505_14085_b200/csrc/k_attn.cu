@@ -299,6 +299,11 @@ int attn_items(int R, int H, int S, int* rows_per_item) {
     }
     // aim for ~4 CTAs per SM over the context items
     int target = (148 * 4 + H * R - 1) / (H * R);
+    if (R > 1) {  // prefill chunks: a power-of-two item count splits S into equal items
+        int p2 = 1;
+        while (p2 < target) p2 <<= 1;
+        target = p2;  // (R = 8, S = 2048: 4 items of 512 rows: 2.77 ms vs 2.99 ms for 3 of 768/512)
+    }
     if (target < 1) target = 1;
     int rpi = (S + target - 1) / target;
     rpi = ((rpi + kSub - 1) / kSub) * kSub;
