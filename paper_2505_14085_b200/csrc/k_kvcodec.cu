@@ -72,7 +72,9 @@ struct TileCfgB {                                       // TB-byte stages
 };
 constexpr int kCompressStages = 2;
 // 8 KB stages: more CTAs per SM beat deeper rings (C2, 11 layers x K/V, measured:
-// 8 KB x 2 = 4.75-4.80 TB/s; 16 KB x 2 4.61; 8 KB x 3 4.70; 4 KB x 2 4.22; 16 KB x 4 3.33)
+// 8 KB x 2 = 4.75-4.80 TB/s; 16 KB x 2 4.61; 8 KB x 3 4.70; 4 KB x 2 4.22; 16 KB x 4 3.33).
+// Per-warp stage release through an "empty" mbarrier instead of the CTA barrier measured
+// slower (8 KB x 2 4.52, 8 KB x 3 4.43, 4 KB x 4 3.83 TB/s; profiles/r01s6_k3_release_ab.txt).
 constexpr int kCompressTileBytes = 8192;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
