@@ -7,6 +7,8 @@ Bars:
 * floating point: normwise  max|gpu - ref| / max|ref|  <= 1e-3 with fp32 outputs,
   the oracle fed the identical bf16 / dequantised inputs.
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -204,3 +206,31 @@ def test_decode_attention_rejects_bad_arguments(ek, ctx):
         ek.decode_attention(ctx, torch.zeros((1, H, 48), device="cuda"), seg,
                             torch.zeros((H, 4, 48), dtype=torch.bfloat16, device="cuda"),
                             torch.zeros((H, 4, 48), dtype=torch.bfloat16, device="cuda"), 0)
+
+
+@pytest.mark.parametrize("n_jobs,rows,nbits,group", [
+    (22, 32 * 2048, 8, 64),   # the bench's C2 launch: K and V of 11 deep layers, 32 heads x 2048 tokens
+    (16, 32 * 2048, 4, 32),   # configs[4] int4
+    (5, 1003, 8, 64),         # ragged: rows not a multiple of the 32-row tile
+    (3, 17, 4, 32),           # fewer rows than one tile
+])
+def test_kv_compress_batched_launch_bit_exact(ek, ctx, oracle, n_jobs, rows, nbits, group):
+    """K3's multi-job persistent launch (`ekv_kv_compress_batched`, the launch bench.py times)
+    at full C2 size: every job's codes and scales equal the oracle's."""
+    d_c, d_e = 128, 64
+    srcs = [rand_bf16(ctx, (rows, d_c), 900 + j, rows, -2.0, 2.0) for j in range(n_jobs)]
+    srcs[0][rows // 3] = 0
+    rng = np.random.default_rng(n_jobs * rows)
+    kept = np.sort(rng.choice(d_c, d_e, replace=False)).astype(np.int32)
+    kept_t = torch.from_numpy(kept).cuda()
+    cw = d_e * nbits // 8
+    codes = [torch.empty((rows, cw), dtype=torch.uint8, device="cuda") for _ in range(n_jobs)]
+    scales = [torch.empty((rows, d_e // group), dtype=torch.float32, device="cuda") for _ in range(n_jobs)]
+    P = ctypes.c_void_p * n_jobs
+    ek.compress_batched(ctx, n_jobs, P(*[s.data_ptr() for s in srcs]), rows, d_c, kept_t, d_e, nbits,
+                        group, P(*[c.data_ptr() for c in codes]), P(*[s.data_ptr() for s in scales]))
+    ctx.synchronize()
+    for j in range(n_jobs):
+        want_c, want_s = oracle.kv_compress(bits(srcs[j]), kept, nbits, group)
+        assert np.array_equal(codes[j].cpu().numpy(), want_c), j
+        assert np.array_equal(scales[j].cpu().numpy().view(np.uint32), want_s.view(np.uint32)), j
