@@ -674,9 +674,15 @@ def main():
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # keep stdout to the one JSON line: NCCL logs (its version banner is printed even at
-        # NCCL_DEBUG=WARN) go to stderr
+        # keep stdout to the one JSON line: NCCL's logs (its version banner included) go to
+        # stderr, and so does anything native code writes to fd 1; sys.stdout (the JSON line)
+        # keeps the original stdout
+        os.environ.setdefault("NCCL_DEBUG", "WARN")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        sys.stdout.flush()
+        out_fd = os.dup(1)
+        os.dup2(2, 1)
+        sys.stdout = os.fdopen(out_fd, "w", buffering=1)
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     run_b200(args, rank, world, local_rank)
