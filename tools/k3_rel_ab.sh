@@ -1,3 +1,5 @@
+# RECORD ONLY: the EKV_K3_CFG switch and the per-warp release variants were reverted after
+# this A/B (profiles/r01s6_k3_release_ab.txt); the script no longer selects anything.
 # A/B of K3 stage release: 0 = CTA barrier (default), 1/2/3 = per-warp mbarrier release with
 # 2x8 KB / 3x8 KB / 4x4 KB stages.  Then the K3 parity tests under each setting.
 for r in 1 2; do for c in 0 1 2 3; do
