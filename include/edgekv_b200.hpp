@@ -17,15 +17,26 @@
 //   assemble_context        include/edgekv/cache_merge.hpp:58-61
 //   collaborative_decode    include/edgekv/cache_merge.hpp:73-75
 //   match_layers            include/edgekv/layer_match.hpp:53-55
+//   FlopCounts / QkvRows    include/edgekv/transformer.hpp:36-53, 90-92
+//   project_qkv             include/edgekv/transformer.hpp:94
+//   PrefillResult/prefill   include/edgekv/transformer.hpp:108-118
+//   decode_step             include/edgekv/transformer.hpp:120-124
+//   forward_rows            include/edgekv/transformer.hpp:129-131
 //   cache_source            include/edgekv/cost_model.hpp:61
 //   pipeline_schedule       include/edgekv/cost_model.hpp:80-81
 //
-// Precision contract of the B200 path (DESIGN.md s.5): tensors cross into HBM
-// as bf16 (weights, K/V, Q/K stacks), accumulation is fp32, outputs come back
-// as fp64; prune_cache is an exact copy; merge_attention, cache_source,
-// pipeline_schedule and match_layers run in fp64 on the host exactly as the
-// reference.  Operations that have no kernel for a shape throw
-// std::invalid_argument (there is no CPU fallback for device work).
+// Precision contract of the B200 path (DESIGN.md s.5):
+//  * exact / reference bits, fp64 on the device in the reference's operation
+//    order: project_qkv (bit-identical matmul), segment_attention (libm exp
+//    aside), select_channels' column norms (fp64), match_layers (K7,
+//    bit-identical CKA/RSA), prune_cache (exact copy), dequantize (exact);
+//  * the B200 compute path, bf16 storage with fp32 accumulation (normwise 1e-3):
+//    forward_rows / prefill / decode_step / collaborative_decode (the edge
+//    forward), b200::build_deep_kv's channel scores (K1 on the tensor cores);
+//  * host fp64 scalar arithmetic exactly as the reference: merge_attention,
+//    cache_source, pipeline_schedule.
+// Operations that have no kernel for a shape throw std::invalid_argument (there
+// is no CPU fallback for device work).
 #pragma once
 
 #include <cstddef>
@@ -102,6 +113,49 @@ struct Model {
     Matrix pos_embedding;  // max_positions x hidden_size
 };
 
+// Exact floating-op counts split by stage (transformer.hpp:36-53); the B200
+// forward fills them with the reference's closed forms (transformer.cpp:267-283).
+struct FlopCounts {
+    std::int64_t proj = 0;
+    std::int64_t score = 0;
+    std::int64_t softmax = 0;
+    std::int64_t value = 0;
+    std::int64_t out_proj = 0;
+    std::int64_t attention() const { return score + softmax + value; }
+    std::int64_t total() const { return proj + score + softmax + value + out_proj; }
+    FlopCounts& operator+=(const FlopCounts& o) {
+        proj += o.proj;
+        score += o.score;
+        softmax += o.softmax;
+        value += o.value;
+        out_proj += o.out_proj;
+        return *this;
+    }
+};
+
+struct QkvRows {
+    Matrix q, k, v;
+};
+
+// Q = x*W_Q etc. for the addressed head, fp64 on the device, bit-identical to
+// the reference (x is n x hidden_size).
+QkvRows project_qkv(const Model& model, const Matrix& x, int layer, int head);
+
+struct PrefillResult {
+    KVCache cache;
+    std::vector<Matrix> layer_outputs;  // per layer, n x hidden_size
+};
+
+// The edge/cloud forward on the device (bf16 weights and KV, fp32 accumulate):
+// the new rows attend to every cached row and causally to each other; K/V of
+// the new rows are appended to `cache`, per-layer outputs returned.
+std::vector<Matrix> forward_rows(const Model& model, KVCache& cache, const Matrix& embeddings,
+                                 PositionKind kind, FlopCounts* fc);
+PrefillResult prefill(const Model& model, const Matrix& embeddings, FlopCounts* fc = nullptr,
+                      PositionKind kind = PositionKind::context);
+Vec decode_step(const Model& model, KVCache& cache, const Vec& embedding, FlopCounts* fc = nullptr,
+                PositionKind kind = PositionKind::generated);
+
 // ---- alignment / projection (head_prune.hpp) --------------------------------
 struct PruneSpec {
     double lambda = 0.0;
@@ -118,8 +172,8 @@ struct ChannelMask {
     static ChannelMask full(int head_dim);
 };
 
-// Column norms of the stacked Q and K rows on the GPU (bf16 in, fp32 -> fp64
-// sums), ranking with the reference rule on the host.
+// Column norms of the stacked Q and K rows on the GPU in fp64, ranking with the
+// reference rule (stable descending, ties to the lower index).
 ChannelMask select_channels(const Matrix& q, const Matrix& k, const PruneSpec& spec);
 
 // Exact column slice of every K/V matrix (fp64 gather on the GPU).
@@ -143,7 +197,8 @@ struct MergedAttention {
     MergeWeights weights;
 };
 
-// One query over one segment on the GPU (K4, bf16 K/V, head_dim 32/64/128).
+// One query over one segment on the GPU in fp64: o, sigma = sum exp(l - max),
+// shift = max logit, as the reference (cache_merge.cpp:12-57).
 SegmentAttention segment_attention(const Vec& q, const Matrix& k, const Matrix& v);
 
 // Eq. 5 merge of two segments (scalar arithmetic, fp64, host).
@@ -247,8 +302,23 @@ struct QuantizedLayer {
 };
 std::vector<QuantizedLayer> compress_cache(const KVCache& cache, const ChannelMask& mask, int bits,
                                            int group = 0);
-// The dequantised context as fp64 K/V (code * scale), e.g. for assemble_context.
+// The dequantised context as fp64 K/V (code * scale, exact, on the device), e.g.
+// for assemble_context.
 LayerKV dequantize(const QuantizedLayer& q, int num_heads);
+// Artifacts::build_deep_kv (sim.cpp:217-265) with the Q re-projection on the
+// tensor cores (K1) instead of project_qkv in fp64 on the host: the channel mask
+// over the stacked Q/K rows of every distinct matched cloud layer (the layer
+// inputs x0 = gamma*(ctx_emb + pos) + b or cloud_prefill.layer_outputs[lc - 1],
+// the cached K of cloud_prefill.cache), and deep_kv[le] = the pruned cloud KV of
+// match[le] (an exact column slice).
+struct DeepKV {
+    ChannelMask mask;
+    double cut_margin = 0.0;  // relative score gap at the cut (near-tie audit)
+    std::map<int, LayerKV> deep_kv;
+};
+DeepKV build_deep_kv(const Model& cloud_model, const PrefillResult& cloud_prefill,
+                     const Matrix& ctx_emb_cloud, const std::map<int, int>& match,
+                     const PruneSpec& spec);
 
 }  // namespace b200
 }  // namespace edgekv

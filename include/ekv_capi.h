@@ -120,13 +120,13 @@ int ekv_kv_colnorm(ekv_ctx_t ctx, const void* K_dev, int64_t rows, int d_c, doub
 int ekv_rank_channels(const double* q_colsq, const double* k_colsq, int d_c, int retained,
                       int* kept, double* cut_margin);
 
-/* Layer map (match_layers, layer_match.cpp:166-228) over probe outputs
- * [me][n][ce] / [nc][n][cc] (host fp64).  best[le] = matched cloud layer or
- * -1.  cka/rsa outputs [me][nc].  Computed on the host in fp64 (offline, once
- * per model pair; SURVEY.md section 8(f) row 3 moves it to the GPU). */
-int ekv_match_layers(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc,
-                     int cc, int n, double theta_cka, double theta_rsa, double* cka, double* rsa,
-                     int* best);
+/* Layer map (match_layers, layer_match.cpp:166-228) over probe outputs in HOST
+ * memory [me][n][ce] / [nc][n][cc] (fp64): uploaded and computed by K7 on the
+ * context's device (bit-identical to the reference).  best[le] = matched cloud
+ * layer or -1; cka/rsa outputs [me][nc].  Synchronises. */
+int ekv_match_layers(ekv_ctx_t ctx, const double* edge_outs, int me, int ce, const double* cloud_outs,
+                     int nc, int cc, int n, double theta_cka, double theta_rsa, double* cka,
+                     double* rsa, int* best);
 /* K7: the same layer map on the device.  edge_outs / cloud_outs are DEVICE
  * buffers (the probe-prefill outputs, fp64); cka / rsa / best are host arrays.
  * Bit-identical to match_layers (layer_match.cpp:166-228): fp64 in the
@@ -135,6 +135,118 @@ int ekv_match_layers(const double* edge_outs, int me, int ce, const double* clou
 int ekv_match_layers_dev(ekv_ctx_t c, const double* edge_outs, int me, int ce,
                          const double* cloud_outs, int nc, int cc, int n, double theta_cka,
                          double theta_rsa, double* cka, double* rsa, int* best);
+
+/* fp64 per-column sums of squares of an fp64 matrix (dev [rows][d] -> dev
+ * colsq[d], ACCUMULATED): the column-norm loop of select_channels
+ * (head_prune.cpp:92-97) for callers that hold Q / K in fp64 (the C++ mirror). */
+int ekv_colsq_f64(ekv_ctx_t ctx, const double* m_dev, int64_t rows, int d, double* colsq_dev);
+
+/* ------------------------------------------------------------------ */
+/* Device prefill, layer map and deep-KV construction (whole ops)      */
+/* ------------------------------------------------------------------ */
+
+/* prefill (transformer.cpp:244-251) = forward_rows with PositionKind::context over
+ * an empty KVCache (transformer.cpp:175-242), on the device: n rows at positions
+ * 0..n-1 through every layer of the model.  Outputs (device, each may be NULL):
+ *   layer_out fp32 [L][n][h]  the per-layer outputs (KVCache layer_outputs);
+ *   x0        fp32 [n][h]     gamma*(emb+pos)+b, the hidden state entering layer 0
+ *                             (build_deep_kv's input of cloud layer 0, sim.cpp:224-234);
+ *   k, v      bf16 [L][H][n][d] the rows' KV cache (KVCache keys / values).
+ * emb fp32 [n][h] on the device.  Synchronises. */
+int ekv_prefill(ekv_model_t m, const float* emb_dev, int n, float* layer_out_dev, float* x0_dev,
+                void* k_dev, void* v_dev);
+
+/* forward_rows (transformer.cpp:175-242) on the device: n new rows on top of the
+ * rows already cached in `cached` (an assembled context of this model's geometry;
+ * NULL = an empty cache, i.e. ekv_prefill), positions S..S+n-1.  Outputs as
+ * ekv_prefill (k / v receive the NEW rows' cache entries, [L][H][n][d]). */
+int ekv_forward_rows(ekv_model_t m, ekv_kvctx_t cached, const float* emb_dev, int n,
+                     float* layer_out_dev, float* x0_dev, void* k_dev, void* v_dev);
+
+/* The reference's fp64 arithmetic on the device, for callers that need its bits
+ * (the C++ mirror's project_qkv / segment_attention):
+ *   ekv_matmul_f64: out[n][m] = a[n][k] * b[k][m] (dev fp64, row-major), every
+ *     entry accumulated from 0.0 left to right with separate IEEE multiply and add
+ *     -- bit-identical to matmul (matrix.cpp:19-36) built without FMA;
+ *   ekv_segment_attention_f64: segment_attention (cache_merge.cpp:12-57) of one
+ *     query q[d] over k[n][d], v[n][vd] (dev fp64): o[vd] (dev), sigma and shift
+ *     (host) = the reference's (Sigma exp(l - max), max) pair; exp() is CUDA's
+ *     (<= 1 ulp from libm), everything else in the reference's order.  Synchronises. */
+int ekv_matmul_f64(ekv_ctx_t ctx, const double* a_dev, const double* b_dev, int n, int k, int m,
+                   double* out_dev);
+int ekv_segment_attention_f64(ekv_ctx_t ctx, const double* q_dev, const double* k_dev,
+                              const double* v_dev, int n, int d, int vd, double* o_dev,
+                              double* sigma, double* shift);
+
+/* Artifacts::deep_match (sim.cpp:100-122) on the device: probe prefill of the edge
+ * and the cloud model (n probe rows each, fp32 on the device: the reference's
+ * generate_embeddings(Rng::mix(seed, 0x9B0BE), n, h)), K7 match_layers over the
+ * per-layer outputs, then the map of the deep edge layers [M - deep_layers, M):
+ * deep_map[i] = matched cloud layer of edge layer M - deep_layers + i (host int).
+ * cka / rsa (host fp64 [M][N]) and best (host int [M], -1 = unmatched) may be NULL.
+ * Error: "ce_lslm: edge layer N has no matched cloud layer under the configured
+ * thresholds" (sim.cpp:113-115).  Both models on one context.  Synchronises. */
+int ekv_deep_match(ekv_model_t edge, ekv_model_t cloud, const float* edge_probe_dev,
+                   const float* cloud_probe_dev, int n, int deep_layers, double theta_cka,
+                   double theta_rsa, int* deep_map, double* cka, double* rsa, int* best);
+
+/* The cloud side of build_deep_kv: the m distinct matched cloud layers (sorted,
+ * as the reference's std::set, sim.cpp:219-221), their input hidden states, W_Q
+ * and cached K / V.  Layer i of X lives at x + x_index[i]*x_stride elements
+ * ([S][h_c] bf16; stride 0 = S*h_c, x_index NULL = 0..m-1); its W_Q^T at
+ * wq + wq_index[i]*wq_stride ([H*d_c][h_c] bf16, row hd*d_c+c = W_Q[lc][hd](:,c);
+ * stride 0 = h_c*h_c -- an ekv_model's weights give wqkvT(0), 4*h_c*h_c, lc);
+ * k[i] / v[i] dev bf16 [H][S][d_c] (the cloud KVCache of that layer). */
+typedef struct {
+    int m, S, H, d_c;
+    const void* x;
+    int64_t x_stride;
+    const int* x_index;
+    const void* wq;
+    int64_t wq_stride;
+    const int* wq_index;
+    const void* const* k;
+    const void* const* v;
+} ekv_cloud_kv;
+
+/* select_channels over the stacked Q / K rows of every matched cloud layer and
+ * head (sim.cpp:236-256, head_prune.cpp:83-108), on the device: K1 (tcgen05 Q
+ * projection, column sums folded over heads and layers) with the cached-K column
+ * sums fused, then the reference ranking on the device.  kept (host int
+ * [retained], ascending) and cut_margin may be NULL.  Synchronises. */
+int ekv_align_select(ekv_ctx_t ctx, const ekv_cloud_kv* cloud, double lambda, int* kept,
+                     double* cut_margin);
+
+/* Artifacts::build_deep_kv (sim.cpp:217-265) on the device, one stream, no host
+ * round trip: K1 (tcgen05: Q of every matched layer, column sums of squares
+ * folded over heads and layers; the cached-K column sums fused into the same
+ * launch) -> the reference ranking on the device (head_prune.cpp:94-107;
+ * ChannelMask::full when nothing is pruned, sim.cpp:255-256) -> one batched K3
+ * launch compressing K and V of every deep layer into the context:
+ * deep_kv[edge_layers[i]] = prune(cloud layer cloud_src[i]) (sim.cpp:258-264).
+ * The deep layers must be quantised layers of dst sharing one format.  kept
+ * (host int [retained], ascending) and cut_margin (host, see
+ * ekv_rank_channels) may be NULL.  Errors mirror assemble_context ("head count
+ * mismatch", "dim mismatch ... align with head pruning").  Synchronises. */
+int ekv_build_deep_kv(ekv_ctx_t ctx, const ekv_cloud_kv* cloud, double lambda, ekv_kvctx_t dst,
+                      int n_deep, const int* edge_layers, const int* cloud_src, int* kept,
+                      double* cut_margin);
+
+/* Artifacts::prompt + build_deep_kv + assembled_context (sim.cpp:124-138,
+ * 186-212, 217-265) on the device: the edge prefill of the context rows fills
+ * the local layers [0, M - n_deep) of dst (bf16); the cloud prefill of the same
+ * rows gives the hidden state entering each matched cloud layer and its KV cache;
+ * ekv_build_deep_kv fills the deep layers [M - n_deep, M) (int8 / int4).
+ *   emb_edge fp32 [S][h_e], emb_cloud fp32 [S][h_c] (device; the reference's
+ *   generate_embeddings(Rng::mix(seed, 0xC7E20000 + pid), S, h)), S = dst's rows;
+ *   deep_map[i] = cloud layer matched to edge layer M - n_deep + i (ekv_deep_match).
+ * kept / cut_margin as ekv_build_deep_kv.  Synchronises. */
+int ekv_prompt_context(ekv_model_t edge, ekv_model_t cloud, const float* emb_edge_dev,
+                       const float* emb_cloud_dev, int n_deep, const int* deep_map, double lambda,
+                       ekv_kvctx_t dst, int* kept, double* cut_margin);
+
+/* bf16_rn of an fp32 device array (e.g. prefill hidden states -> K1 operands). */
+int ekv_convert_f32_bf16(ekv_ctx_t ctx, const float* src_dev, void* dst_dev, int64_t n);
 
 /* ------------------------------------------------------------------ */
 /* Stage 2: representation compression (gather + quantise + pack)     */
@@ -170,6 +282,10 @@ int ekv_kv_compress_batched(ekv_ctx_t ctx, int n, const void* const* src_dev, in
 /* K6: dst = bf16_rn(code * scale) (fp32 product), dev bf16 [rows][d_e]. */
 int ekv_kv_dequant(ekv_ctx_t ctx, const void* codes_dev, const float* scales_dev, int64_t rows,
                    int d_e, int bits, int group, void* dst_dev);
+/* K6, exact: dst = code * (double)scale, dev fp64 [rows][d_e] (the historical-cache
+ * and C++-mirror paths that hand dequantised KV back as fp64). */
+int ekv_kv_dequant_f64(ekv_ctx_t ctx, const void* codes_dev, const float* scales_dev, int64_t rows,
+                       int d_e, int bits, int group, double* dst_dev);
 
 /* ------------------------------------------------------------------ */
 /* Stage 3: edge decode attention over the reused KV                   */
@@ -311,10 +427,11 @@ int ekv_collaborative_decode(ekv_session_t s, const float* user_emb_host, int U,
  * uploads[L]: per layer, host K/V in the layer's storage format (bf16 [H][S][d]
  * or codes) and fp32 scales for quantised layers; k_host == NULL = resident.
  * overlap = 0 runs the sequential schedule (all uploads, then compute) for
- * comparison.  Outputs: out_dev fp32 [n][h] (may be NULL), t_comm_ms[L]
- * (upload time of each layer on the copy stream), t_comp_ms[L] (compute of each
- * layer, measured by a kernel-by-kernel re-run with the context resident),
- * total_ms (first upload -> last output).  Synchronous. */
+ * comparison.  Outputs (each may be NULL): out_dev fp32 [n][h], t_comm_ms[L]
+ * (upload time of each layer on the copy stream), total_ms (first upload -> last
+ * output), t_comp_ms[L] (compute of each layer -- a diagnostic that re-runs the
+ * rows kernel by kernel with the context resident, so it doubles the work; pass
+ * NULL outside measurements).  Synchronous. */
 typedef struct {
     const void* k_host;
     const void* v_host;
@@ -324,6 +441,16 @@ typedef struct {
 int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
                                   const ekv_layer_upload* uploads, int overlap, float* t_comm_ms,
                                   float* t_comp_ms, float* total_ms);
+
+/* Eq. 20 with the context layers delivered by another agent on another stream --
+ * e.g. an NCCL receive from the cloud rank (the emulated cloud->edge link,
+ * Sim::fetch_deep_layer -> submit_transfer, sim.cpp:802-814, 417-449) landing in
+ * this context's storage (ekv_kvctx_layer pointers).  layer_ready[l] is a
+ * cudaEvent_t the producer records after layer l landed (NULL entry, or a NULL
+ * array = resident); layer l's attention waits on it, so the transfer of layer l
+ * overlaps the compute of layers < l.  Asynchronous on the context stream. */
+int ekv_session_forward_streamed(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
+                                 void* const* layer_ready);
 
 /* ------------------------------------------------------------------ */
 /* Batched sessions (BASELINE configs[2], concurrent edge sessions)     */

@@ -104,6 +104,7 @@ class Oracle:
         L.ekvo_collaborative_decode.argtypes = ([C.c_int] * 4 + [_dp] * 5 + [C.c_int, _dp, _dp,
                                                 _dp, C.c_int, C.c_int, _dp, C.c_int, _dp, _dp])
         L.ekvo_prefill.argtypes = [C.c_int] * 4 + [_dp] * 6 + [C.c_int, _dp, _dp, _dp]
+        L.ekvo_prefill_ex.argtypes = [C.c_int] * 4 + [_dp] * 6 + [C.c_int, C.c_int, _dp, _dp, _dp]
         L.ekvo_align_qnorm.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, _dp]
         L.ekvo_cka.restype = C.c_int
         L.ekvo_cka.argtypes = [_dp, C.c_int, _dp, C.c_int, C.c_int, _dp]
@@ -259,15 +260,18 @@ class Oracle:
             raise ValueError("collaborative_decode: steps must be >= 1")
         return pre[:U], st
 
-    def prefill(self, model, emb):
+    def prefill(self, model, emb, kv_bf16=False):
+        """prefill (forward_rows over an empty cache); kv_bf16 rounds the cached K/V rows
+        to bf16 as the B200 prefill stores them."""
         L, H, d, mp = model["L"], model["H"], model["d"], model["max_pos"]
         h = H * d
         emb = _f64(emb)
         n = emb.shape[0]
         lo = np.zeros((L, n, h)); ko = np.zeros((L, H, n, d)); vo = np.zeros((L, H, n, d))
-        self.lib.ekvo_prefill(L, H, d, mp, _d(_f64(model["wqkvT"])), _d(_f64(model["woT"])),
-                              _d(_f64(model["gamma"])), _d(_f64(model["bias"])),
-                              _d(_f64(model["pos"])), _d(emb), n, _d(lo), _d(ko), _d(vo))
+        self.lib.ekvo_prefill_ex(L, H, d, mp, _d(_f64(model["wqkvT"])), _d(_f64(model["woT"])),
+                                 _d(_f64(model["gamma"])), _d(_f64(model["bias"])),
+                                 _d(_f64(model["pos"])), _d(emb), n, int(kv_bf16), _d(lo), _d(ko),
+                                 _d(vo))
         return lo, ko, vo
 
     # --- layer matching ------------------------------------------------------

@@ -576,10 +576,12 @@ EKVO_EXPORT int ekvo_collaborative_decode(int L, int H, int d, int max_pos, cons
  * same B200 weight layout: returns per-layer outputs [L][n][h] and the K/V
  * cache [L][H][n][d].  Used to make the inputs of the alignment stage (the
  * cloud hidden states X_lc and the cloud K/V) in small end-to-end tests. */
-EKVO_EXPORT void ekvo_prefill(int L, int H, int d, int max_pos, const double* wqkvT,
-                              const double* woT, const double* gamma, const double* bias,
-                              const double* pos, const double* emb, int n, double* layer_out,
-                              double* k_out, double* v_out) {
+/* kv_bf16 = 1 rounds the cached K/V rows to bf16 before they are attended (and
+ * returned): the B200 prefill keeps its KV cache in bf16 (ekv_prefill). */
+EKVO_EXPORT void ekvo_prefill_ex(int L, int H, int d, int max_pos, const double* wqkvT,
+                                 const double* woT, const double* gamma, const double* bias,
+                                 const double* pos, const double* emb, int n, int kv_bf16,
+                                 double* layer_out, double* k_out, double* v_out) {
     (void)max_pos;
     const int h = H * d;
     double* x = (double*)malloc(sizeof(double) * (size_t)n * h);
@@ -602,8 +604,14 @@ EKVO_EXPORT void ekvo_prefill(int L, int H, int d, int max_pos, const double* wq
         for (int hd = 0; hd < H; ++hd) {
             for (int i = 0; i < n; ++i)
                 for (int c = 0; c < d; ++c) {
-                    kb[(size_t)i * d + c] = qkv[(size_t)i * 3 * h + h + hd * d + c];
-                    vb[(size_t)i * d + c] = qkv[(size_t)i * 3 * h + 2 * h + hd * d + c];
+                    double kv = qkv[(size_t)i * 3 * h + h + hd * d + c];
+                    double vv = qkv[(size_t)i * 3 * h + 2 * h + hd * d + c];
+                    if (kv_bf16) {
+                        kv = (double)bf16_to_f32(f32_to_bf16_rn((float)kv));
+                        vv = (double)bf16_to_f32(f32_to_bf16_rn((float)vv));
+                    }
+                    kb[(size_t)i * d + c] = kv;
+                    vb[(size_t)i * d + c] = vv;
                 }
             if (k_out) memcpy(k_out + (((size_t)l * H + hd) * n) * d, kb, sizeof(double) * (size_t)n * d);
             if (v_out) memcpy(v_out + (((size_t)l * H + hd) * n) * d, vb, sizeof(double) * (size_t)n * d);
@@ -628,6 +636,14 @@ EKVO_EXPORT void ekvo_prefill(int L, int H, int d, int max_pos, const double* wq
     free(o);
     free(kb);
     free(vb);
+}
+
+EKVO_EXPORT void ekvo_prefill(int L, int H, int d, int max_pos, const double* wqkvT,
+                              const double* woT, const double* gamma, const double* bias,
+                              const double* pos, const double* emb, int n, double* layer_out,
+                              double* k_out, double* v_out) {
+    ekvo_prefill_ex(L, H, d, max_pos, wqkvT, woT, gamma, bias, pos, emb, n, 0, layer_out, k_out,
+                    v_out);
 }
 
 /* Q = X * W_Q for one cloud layer in the B200 layout (wqT [H*d_c][h_c]) and

@@ -34,6 +34,13 @@ class ekv_kvpack_info(C.Structure):
                 ("bits", C.c_int), ("group", C.c_int), ("bytes", C.c_size_t)]
 
 
+class ekv_cloud_kv(C.Structure):
+    _fields_ = [("m", C.c_int), ("S", C.c_int), ("H", C.c_int), ("d_c", C.c_int),
+                ("x", C.c_void_p), ("x_stride", C.c_int64), ("x_index", C.POINTER(C.c_int)),
+                ("wq", C.c_void_p), ("wq_stride", C.c_int64), ("wq_index", C.POINTER(C.c_int)),
+                ("k", C.POINTER(C.c_void_p)), ("v", C.POINTER(C.c_void_p))]
+
+
 class ekv_model_config(C.Structure):
     _fields_ = [("num_layers", C.c_int), ("num_heads", C.c_int), ("head_dim", C.c_int),
                 ("max_positions", C.c_int)]
@@ -61,7 +68,18 @@ PROTOS = {
     "ekv_align_qnorm": [_vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "ekv_kv_colnorm": [_vp, _vp, _i64, _i, _vp],
     "ekv_rank_channels": [_dp, _dp, _i, _i, _ip, _dp],
-    "ekv_match_layers": [_dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
+    "ekv_match_layers": [_vp, _dp, _i, _i, _dp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
+    "ekv_colsq_f64": [_vp, _vp, _i64, _i, _vp],
+    "ekv_prefill": [_vp, _vp, _i, _vp, _vp, _vp, _vp],
+    "ekv_deep_match": [_vp, _vp, _vp, _vp, _i, _i, _d, _d, _ip, _dp, _dp, _ip],
+    "ekv_align_select": [_vp, C.POINTER(ekv_cloud_kv), _d, _ip, _dp],
+    "ekv_build_deep_kv": [_vp, C.POINTER(ekv_cloud_kv), _d, _vp, _i, _ip, _ip, _ip, _dp],
+    "ekv_kv_dequant_f64": [_vp, _vp, _vp, _i64, _i, _i, _i, _vp],
+    "ekv_prompt_context": [_vp, _vp, _vp, _vp, _i, _ip, _d, _vp, _ip, _dp],
+    "ekv_forward_rows": [_vp, _vp, _vp, _i, _vp, _vp, _vp, _vp],
+    "ekv_matmul_f64": [_vp, _vp, _vp, _i, _i, _i, _vp],
+    "ekv_segment_attention_f64": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _dp, _dp],
+    "ekv_convert_f32_bf16": [_vp, _vp, _vp, _i64],
     "ekv_match_layers_dev": [_vp, _vp, _i, _i, _vp, _i, _i, _i, _d, _d, _dp, _dp, _ip],
     "ekv_kv_gather": [_vp, _vp, _i64, _i, _vp, _i, _vp],
     "ekv_gather_columns": [_vp, _vp, _i64, _i, _vp, _i, _i, _vp],
@@ -94,6 +112,7 @@ PROTOS = {
     "ekv_session_profile_step": [_vp, _fp, _i, _ip],
     "ekv_session_user_kv": [_vp, _i, _pp, _pp, _ip],
     "ekv_session_forward_pipelined": [_vp, _vp, _i, _vp, _vp, _i, _fp, _fp, _fp],
+    "ekv_session_forward_streamed": [_vp, _vp, _i, _vp, _vp],
     "ekv_batch_create": [_vp, _vp, _i, _i, _pp],
     "ekv_fnv1a64": [_vp, C.c_size_t, _u64, C.POINTER(C.c_uint64)],
     "ekv_kvpack_size": [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_size_t)],

@@ -6,7 +6,10 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -14,11 +17,58 @@
 #include "ekv_kernels.h"
 #include "ekv_mega.h"
 #include "ekv_batch.h"
+#include "ekv_objects.h"
 
 namespace ekv {
 
 static std::atomic<int64_t> g_launches{0};
 void count_launches(int64_t n) { g_launches += n; }
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_smem_attr;          // (device, kernel) -> bytes set
+std::map<std::tuple<int, const void*, int, int>, int> g_occ;     // (device, kernel, thr, smem)
+std::map<int, int> g_sms;                                        // device -> SM count
+int current_device() {
+    int dev = 0;
+    EKV_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+}  // namespace
+
+void ensure_smem_attr(const void* fn, int bytes) {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& have = g_smem_attr[{dev, fn}];
+    if (have >= bytes) return;
+    EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+}
+
+int device_sm_count() {
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int sms = 0;
+    EKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    g_sms[dev] = sms;
+    return sms;
+}
+
+int blocks_per_sm(const void* fn, int threads, int smem) {
+    ensure_smem_attr(fn, smem);
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto key = std::make_tuple(dev, fn, threads, smem);
+    auto it = g_occ.find(key);
+    if (it != g_occ.end()) return it->second;
+    int occ = 0;
+    EKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+    if (occ < 1) occ = 1;
+    g_occ[key] = occ;
+    return occ;
+}
 
 void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
                                 int n_cols, double* colsq, int num_sms, cudaStream_t st);
@@ -27,104 +77,45 @@ void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, in
 
 using namespace ekv;
 
-namespace {
+namespace ekv {
 thread_local std::string g_err;
 
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return EKV_OK;
-    } catch (const Error& e) {
-        g_err = e.what();
-        return e.status;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return EKV_ENOMEM;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return EKV_EINVAL;
-    }
+void release_ctx(ekv_ctx_s* c) {
+    if (--c->refs > 0) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->capture);
+    if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->attn_ws) cudaFree(c->attn_ws);
+    if (c->attn_ctr) cudaFree(c->attn_ctr);
+    if (c->scratch) cudaFree(c->scratch);
+    delete c;
 }
 
-template <class T>
-T* dalloc(size_t count) {
-    void* p = nullptr;
-    if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
-    if (e != cudaSuccess) {
-        (void)cudaGetLastError();
-        throw Error(EKV_ENOMEM, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
-                                    " bytes failed: " + cudaGetErrorString(e));
-    }
-    return (T*)p;
+void release_model(ekv_model_s* m) {
+    if (--m->refs > 0) return;
+    ekv_ctx_s* c = m->ctx;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(m->weights);
+    cudaFree(m->gamma);
+    cudaFree(m->bias);
+    cudaFree(m->pos);
+    delete m;
+    release_ctx(c);
 }
 
-}  // namespace
-
-struct ekv_ctx_s {
-    int device = 0;
-    int num_sms = 148;
-    cudaStream_t stream = nullptr;
-    cudaStream_t capture = nullptr;  // graphs are captured here, launched on `stream`
-    cudaStream_t copy = nullptr;     // context uploads of the pipelined prefill (Eq. 20)
-    bool own_stream = false;
-};
-
-struct ekv_model_s {
-    ekv_ctx_s* ctx = nullptr;
-    ekv_model_config cfg{};
-    int h = 0;
-    uint16_t* weights = nullptr;  // per layer: [3h][h] wqkvT then [h][h] woT
-    float* gamma = nullptr;
-    float* bias = nullptr;
-    uint16_t* pos = nullptr;
-    size_t layer_elems() const { return (size_t)4 * h * h; }
-    uint16_t* wqkvT(int l) const { return weights + (size_t)l * layer_elems(); }
-    uint16_t* woT(int l) const { return wqkvT(l) + (size_t)3 * h * h; }
-};
-
-struct ekv_kvctx_s {
-    ekv_model_s* model = nullptr;
-    int S = 0, group = 0;
-    std::vector<int> fmt;
-    std::vector<ekv_segment> seg;
-    std::vector<void*> allocs;
-};
-
-struct ekv_session_s {
-    ekv_model_s* model = nullptr;
-    ekv_kvctx_s* kv = nullptr;
-    int cap = 0;                   // user/generated rows
-    uint16_t* uk = nullptr;        // [L][H][cap][d]
-    uint16_t* uv = nullptr;
-    float* xa = nullptr;           // [8][h]
-    float* xb = nullptr;           // [8][h]
-    float* q = nullptr;            // [8][h]
-    float* emb = nullptr;          // [cap][h] staged user embeddings
-    float* pre_out = nullptr;      // [cap][h] prefill outputs by user row
-    float* hist = nullptr;         // [cap][h] decode-step outputs by step
-    DevState* state = nullptr;
-    float* ws = nullptr;
-    unsigned* counters = nullptr;
-    int user_len = 0;              // host mirror of state->user_len
-    int steps = 0;                 // host mirror of state->step
-    cudaGraphExec_t step_graph = nullptr;
-    int64_t graph_kernels = 0;
-    // persistent decode-step kernel (k_decode_mega.cu)
-    int path = 0;                  // 0 = megakernel when supported, 1 = per-layer graph
-    bool mega_ok = false;
-    uint64_t* mega_ll = nullptr;     // tagged words of the dataflow (MegaArgs::ll_*)
-    unsigned* mega_sync = nullptr;   // [0] launch epoch
-    MegaArgs mega{};
-    // tensor-core prefill projections (R >= 2 rows; h % 128 == 0)
-    bool tc_prefill = false;
-    uint16_t* pxhl = nullptr;      // [2][8][h] bf16 hi / lo operand
-    float* ppart = nullptr;        // [max(KSq*3h, KSo*h)][8] split-K partials
-    int pKSq = 1, pKSo = 1;
-    CUtensorMap pmap_w{}, pmap_x{};
-    size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
-};
+void release_kvctx(ekv_kvctx_s* kc) {
+    if (--kc->refs > 0) return;
+    ekv_model_s* m = kc->model;
+    cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->stream);
+    for (void* p : kc->allocs) cudaFree(p);
+    delete kc;
+    release_model(m);
+}
+}  // namespace ekv
 
 namespace {
 
@@ -143,9 +134,6 @@ void check_device(int device, int* sms) {
     *sms = p.multiProcessorCount;
 }
 
-void set_dev(ekv_ctx_s* c) { EKV_CUDA(cudaSetDevice(c->device)); }
-
-int d_of(const ekv_model_s* m) { return m->cfg.head_dim; }
 
 // Tensor-core projections of R >= 2 rows of one session (K9 + split-K finish):
 // QKV of layer l from `in` (fp32 [R][h]; layer 0 gets the input transform at
@@ -327,8 +315,11 @@ void forward_chunk(ekv_session_s* s, const float* in, int R, float* out_hist,
 // the Eq. 20 pipelined prefill, where layer l may only start once its context
 // has arrived (ready[l]).  scratch: 2*n*h floats.  lev (optional): L+1 events
 // around the layers.  Results are identical to forward_chunk's.
+}  // namespace
+
+namespace ekv {
 void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, cudaStream_t st,
-                         const cudaEvent_t* ready, float* scratch, cudaEvent_t* lev) {
+                         const cudaEvent_t* ready, float* scratch, cudaEvent_t* lev, float* layer_out) {
     ekv_model_s* m = s->model;
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
     float* X = scratch;               // layer outputs [n][h]
@@ -401,9 +392,16 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             else
                 launch_gemv(o, st);
         }
+        if (layer_out)
+            EKV_CUDA(cudaMemcpyAsync(layer_out + (size_t)l * n * h, X, sizeof(float) * n * h,
+                                     cudaMemcpyDeviceToDevice, st));
     }
     if (lev) EKV_CUDA(cudaEventRecord(lev[L], st));
 }
+
+}  // namespace ekv
+
+namespace {
 
 size_t attn_ws_floats(int R, int H, int S, int d, int ucap) {
     int rpi = 0;
@@ -503,6 +501,9 @@ void session_alloc(ekv_session_s* s) {
     EKV_CUDA(cudaMemset(s->uv, 0, sizeof(uint16_t) * L * s->ukv_layer()));
 }
 
+}  // namespace
+
+namespace ekv {
 void session_reset(ekv_session_s* s, cudaStream_t st) {
     EKV_CUDA(cudaMemsetAsync(s->state, 0, sizeof(DevState), st));
     s->user_len = 0;
@@ -518,6 +519,10 @@ void check_overflow(ekv_session_s* s, int n) {
             "session full: " + std::to_string(s->user_len + n) + " user rows > capacity " +
                 std::to_string(s->cap));
 }
+
+}  // namespace ekv
+
+namespace {
 
 // rows [0, n) of emb_dev through merged_forward in chunks of <= 8 rows;
 // final-layer rows land in s->pre_out[user_row].
@@ -884,13 +889,7 @@ int ekv_ctx_create(int device, void* stream, ekv_ctx_t* out) {
 
 int ekv_ctx_destroy(ekv_ctx_t c) {
     return guard([&] {
-        if (!c) return;
-        cudaSetDevice(c->device);
-        cudaStreamSynchronize(c->stream);
-        if (c->own_stream) cudaStreamDestroy(c->stream);
-        cudaStreamDestroy(c->capture);
-        if (c->copy) cudaStreamDestroy(c->copy);
-        delete c;
+        if (c) release_ctx(c);
     });
 }
 
@@ -1018,83 +1017,6 @@ int ekv_rank_channels(const double* q_colsq, const double* k_colsq, int d_c, int
     });
 }
 
-// --- host layer map (match_layers, layer_match.cpp:166-228) ---------------
-namespace {
-void gram(const double* o, int n, int c, std::vector<double>& s) {
-    s.assign((size_t)n * n, 0.0);
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            double acc = 0.0;
-            for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)j * c + k];
-            s[(size_t)i * n + j] = acc;
-        }
-}
-double hsic_of(const std::vector<double>& se, const std::vector<double>& sc, int n) {
-    std::vector<double> rm(n, 0.0), cm(n, 0.0);
-    double tot = 0.0;
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j) {
-            rm[i] += se[(size_t)i * n + j];
-            cm[j] += se[(size_t)i * n + j];
-            tot += se[(size_t)i * n + j];
-        }
-    for (int i = 0; i < n; ++i) {
-        rm[i] /= n;
-        cm[i] /= n;
-    }
-    tot /= (double)n * n;
-    double tr = 0.0;
-    for (int i = 0; i < n; ++i)
-        for (int j = 0; j < n; ++j)
-            tr += (se[(size_t)i * n + j] - rm[i] - cm[j] + tot) * sc[(size_t)j * n + i];
-    return tr / ((double)(n - 1) * (n - 1));
-}
-std::vector<double> cos_lower(const double* o, int n, int c) {
-    std::vector<double> norms(n), flat;
-    for (int i = 0; i < n; ++i) {
-        double acc = 0.0;
-        for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)i * c + k];
-        norms[i] = std::sqrt(acc);
-        require(norms[i] != 0.0, "rsa: zero-norm row " + std::to_string(i));
-    }
-    for (int i = 1; i < n; ++i)
-        for (int j = 0; j < i; ++j) {
-            double acc = 0.0;
-            for (int k = 0; k < c; ++k) acc += o[(size_t)i * c + k] * o[(size_t)j * c + k];
-            flat.push_back(acc / (norms[i] * norms[j]));
-        }
-    return flat;
-}
-double pearson(const std::vector<double>& x, const std::vector<double>& y) {
-    const size_t n = x.size();
-    double mx = 0, my = 0;
-    for (size_t i = 0; i < n; ++i) {
-        mx += x[i];
-        my += y[i];
-    }
-    mx /= n;
-    my /= n;
-    double sxy = 0, sxx = 0, syy = 0;
-    for (size_t i = 0; i < n; ++i) {
-        sxy += (x[i] - mx) * (y[i] - my);
-        sxx += (x[i] - mx) * (x[i] - mx);
-        syy += (y[i] - my) * (y[i] - my);
-    }
-    require(sxx != 0.0 && syy != 0.0, "pearson_corr: zero variance");
-    return std::clamp(sxy / std::sqrt(sxx * syy), -1.0, 1.0);
-}
-std::vector<double> normalized(const double* o, int n, int c) {
-    std::vector<double> out(o, o + (size_t)n * c);
-    double f = 0.0;
-    for (double v : out) f += v * v;
-    f = std::sqrt(f);
-    if (f == 0.0) return out;
-    const double t = std::sqrt((double)n);
-    for (double& v : out) v *= t / f;
-    return out;
-}
-}  // namespace
-
 int ekv_match_layers_dev(ekv_ctx_t c, const double* edge_outs, int me, int ce, const double* cloud_outs,
                          int nc, int cc, int n, double theta_cka, double theta_rsa, double* cka_out,
                          double* rsa_out, int* best) {
@@ -1149,49 +1071,6 @@ int ekv_match_layers_dev(ekv_ctx_t c, const double* edge_outs, int me, int ce, c
                 cka_out[p] = ck;
                 rsa_out[p] = hc[p];
                 if (ck >= theta_cka && hc[p] >= theta_rsa && (bl < 0 || ck > bc)) {
-                    bl = lc;
-                    bc = ck;
-                }
-            }
-            best[le] = bl;
-        }
-    });
-}
-
-int ekv_match_layers(const double* edge_outs, int me, int ce, const double* cloud_outs, int nc,
-                     int cc, int n, double theta_cka, double theta_rsa, double* cka_out,
-                     double* rsa_out, int* best) {
-    return guard([&] {
-        require(edge_outs && cloud_outs && cka_out && rsa_out && best, "null argument");
-        require(me >= 1 && nc >= 1, "match_layers: empty layer output list");
-        require(theta_cka >= 0.0, "SimilarityConfig: theta_cka must be >= 0");
-        require(theta_rsa >= -1.0, "SimilarityConfig: theta_rsa must be >= -1");
-        require(n >= 3, "rsa: need N >= 3 samples");
-        std::vector<std::vector<double>> eg(me), cg(nc), ef(me), cf(nc);
-        std::vector<double> self_e(me), self_c(nc);
-        for (int l = 0; l < me; ++l) {
-            auto o = normalized(edge_outs + (size_t)l * n * ce, n, ce);
-            gram(o.data(), n, ce, eg[l]);
-            self_e[l] = hsic_of(eg[l], eg[l], n);
-            ef[l] = cos_lower(o.data(), n, ce);
-        }
-        for (int l = 0; l < nc; ++l) {
-            auto o = normalized(cloud_outs + (size_t)l * n * cc, n, cc);
-            gram(o.data(), n, cc, cg[l]);
-            self_c[l] = hsic_of(cg[l], cg[l], n);
-            cf[l] = cos_lower(o.data(), n, cc);
-        }
-        for (int le = 0; le < me; ++le) {
-            int bl = -1;
-            double bc = 0.0;
-            for (int lc = 0; lc < nc; ++lc) {
-                require(self_e[le] >= 1e-15 && self_c[lc] >= 1e-15,
-                        "cka: degenerate representation");
-                const double ck = hsic_of(eg[le], cg[lc], n) / std::sqrt(self_e[le] * self_c[lc]);
-                const double r = pearson(ef[le], cf[lc]);
-                cka_out[(size_t)le * nc + lc] = ck;
-                rsa_out[(size_t)le * nc + lc] = r;
-                if (ck >= theta_cka && r >= theta_rsa && (bl < 0 || ck > bc)) {
                     bl = lc;
                     bc = ck;
                 }
@@ -1303,22 +1182,25 @@ int ekv_decode_attention(ekv_ctx_t c, int R, int H, int d, const float* q,
                 "segment_attention: empty segment (user rows exceed the cache)");
         check_segment(*ctx_seg, d);
         set_dev(c);
-        static thread_local float* ws = nullptr;
-        static thread_local size_t ws_n = 0;
-        static thread_local unsigned* ctr = nullptr;
-        static thread_local size_t ctr_n = 0;
+        // the scratch belongs to this context (its device and stream): grown on demand
         const size_t need = attn_ws_floats(R, H, ctx_seg->S, d, user_cap);
-        if (need > ws_n) {
-            if (ws) cudaFree(ws);
-            ws = dalloc<float>(need);
-            ws_n = need;
+        if (need > c->attn_ws_n) {
+            EKV_CUDA(cudaStreamSynchronize(c->stream));
+            if (c->attn_ws) cudaFree(c->attn_ws);
+            c->attn_ws = nullptr;
+            c->attn_ws = dalloc<float>(need);
+            c->attn_ws_n = need;
         }
-        if ((size_t)R * H > ctr_n) {
-            if (ctr) cudaFree(ctr);
-            ctr = dalloc<unsigned>((size_t)R * H);
-            EKV_CUDA(cudaMemset(ctr, 0, sizeof(unsigned) * R * H));
-            ctr_n = (size_t)R * H;
+        if ((size_t)R * H > c->attn_ctr_n) {
+            EKV_CUDA(cudaStreamSynchronize(c->stream));
+            if (c->attn_ctr) cudaFree(c->attn_ctr);
+            c->attn_ctr = nullptr;
+            c->attn_ctr = dalloc<unsigned>((size_t)R * H);
+            EKV_CUDA(cudaMemset(c->attn_ctr, 0, sizeof(unsigned) * R * H));
+            c->attn_ctr_n = (size_t)R * H;
         }
+        float* ws = c->attn_ws;
+        unsigned* ctr = c->attn_ctr;
         AttnArgs a{};
         a.R = R;
         a.H = H;
@@ -1376,19 +1258,14 @@ int ekv_model_create(ekv_ctx_t c, const ekv_model_config* cfg, ekv_model_t* out)
             delete m;
             throw;
         }
+        c->refs++;
         *out = m;
     });
 }
 
 int ekv_model_destroy(ekv_model_t m) {
     return guard([&] {
-        if (!m) return;
-        cudaSetDevice(m->ctx->device);
-        cudaFree(m->weights);
-        cudaFree(m->gamma);
-        cudaFree(m->bias);
-        cudaFree(m->pos);
-        delete m;
+        if (m) release_model(m);
     });
 }
 
@@ -1493,16 +1370,14 @@ int ekv_kvctx_create(ekv_model_t m, int S, const int* layer_format, int group, e
             delete c;
             throw;
         }
+        m->refs++;
         *out = c;
     });
 }
 
 int ekv_kvctx_destroy(ekv_kvctx_t c) {
     return guard([&] {
-        if (!c) return;
-        cudaSetDevice(c->model->ctx->device);
-        for (void* p : c->allocs) cudaFree(p);
-        delete c;
+        if (c) release_kvctx(c);
     });
 }
 
@@ -1620,6 +1495,8 @@ int ekv_session_create(ekv_model_t m, ekv_kvctx_t c, int max_user_rows, ekv_sess
             delete s;
             throw;
         }
+        m->refs++;
+        c->refs++;
         *out = s;
     });
 }
@@ -1635,7 +1512,11 @@ int ekv_session_destroy(ekv_session_t s) {
                         (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync,
                         (void*)s->pxhl, (void*)s->ppart})
             cudaFree(p);
+        ekv_kvctx_s* kv = s->kv;
+        ekv_model_s* m = s->model;
         delete s;
+        release_kvctx(kv);
+        release_model(m);
     });
 }
 
@@ -1838,6 +1719,8 @@ int ekv_batch_create(ekv_model_t m, ekv_kvctx_t c, int sessions, int max_rows, e
             delete b;
             throw;
         }
+        m->refs++;
+        c->refs++;
         *out = b;
     });
 }
@@ -1849,7 +1732,11 @@ int ekv_batch_destroy(ekv_batch_t b) {
         cudaStreamSynchronize(b->model->ctx->stream);
         if (b->graph) cudaGraphExecDestroy(b->graph);
         batch_free(b);
+        ekv_kvctx_s* kv = b->kv;
+        ekv_model_s* m = b->model;
         delete b;
+        release_kvctx(kv);
+        release_model(m);
     });
 }
 
@@ -1962,12 +1849,64 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb, int U, 
 
 
 // ---------------------------------------------------------------- Eq. 20 pipelined prefill
+namespace {
+// Layer-major forward of n user rows where layer l's attention waits on ready[l] (null =
+// the layer is resident), then the decode state is advanced past the rows.  Shared by the
+// host-upload (Eq. 20 over pinned host memory) and the event-driven (NCCL receive) entry
+// points.  t_comp_ms (optional): per-layer compute re-measured by a kernel-by-kernel re-run
+// with the context resident (diagnostic: doubles the work, so only when asked for).
+void streamed_forward(ekv_session_s* s, const float* emb_dev, int n, float* out_dev,
+                      cudaEvent_t* ready, cudaEvent_t start_ev, cudaEvent_t end_ev,
+                      float* t_comp_ms) {
+    ekv_model_s* m = s->model;
+    ekv_ctx_s* c = m->ctx;
+    const int L = m->cfg.num_layers;
+    cudaStream_t st = c->stream;
+    const int prev_len = s->user_len;
+    float* scratch = nullptr;
+    std::vector<cudaEvent_t> lev;
+    auto cleanup = [&] {
+        if (scratch) cudaFreeAsync(scratch, st);
+        for (auto& e : lev)
+            if (e) cudaEventDestroy(e);
+    };
+    try {
+        EKV_CUDA(cudaMallocAsync((void**)&scratch, sizeof(float) * 2 * n * m->h, st));
+        if (start_ev) EKV_CUDA(cudaEventRecord(start_ev, st));
+        forward_layer_major(s, emb_dev, n, prev_len, st, ready, scratch, nullptr);
+        if (end_ev) EKV_CUDA(cudaEventRecord(end_ev, st));
+        if (out_dev)
+            EKV_CUDA(cudaMemcpyAsync(out_dev, s->pre_out + (size_t)prev_len * m->h,
+                                     sizeof(float) * n * m->h, cudaMemcpyDeviceToDevice, st));
+        if (t_comp_ms) {
+            // the same rows again, layer by layer with the context resident (rewrites the
+            // same user-cache rows and outputs with identical values)
+            lev.assign(L + 1, nullptr);
+            for (auto& e : lev) EKV_CUDA(cudaEventCreate(&e));
+            forward_layer_major(s, emb_dev, n, prev_len, st, nullptr, scratch, lev.data());
+            EKV_CUDA(cudaStreamSynchronize(st));
+            for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comp_ms[l], lev[l], lev[l + 1]));
+        }
+        // state: n more user rows; decode continues from the last row (xa[0]), step 0
+        launch_advance(s->state, n, st);
+        EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
+        EKV_CUDA(cudaMemcpyAsync(s->xa, scratch + (size_t)(n - 1) * m->h, sizeof(float) * m->h,
+                                 cudaMemcpyDeviceToDevice, st));
+        s->user_len += n;
+        s->steps = 0;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+}
+}  // namespace
+
 int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
                                   const ekv_layer_upload* uploads, int overlap, float* t_comm_ms,
                                   float* t_comp_ms, float* total_ms) {
     return guard([&] {
-        require(s && emb_dev && uploads && t_comm_ms && t_comp_ms && total_ms,
-                "ekv_session_forward_pipelined: null argument");
+        require(s && emb_dev && uploads, "ekv_session_forward_pipelined: null argument");
         require(n >= 1, "ekv_session_forward_pipelined: n must be >= 1");
         ekv_model_s* m = s->model;
         ekv_ctx_s* c = m->ctx;
@@ -1975,7 +1914,7 @@ int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, 
         check_overflow(s, n);
         set_dev(c);
         cudaStream_t st = c->stream, cp = c->copy;
-        std::vector<cudaEvent_t> up(L + 1, nullptr), ready(L, nullptr), cs(L + 1, nullptr);
+        std::vector<cudaEvent_t> up(L + 1, nullptr), ready(L, nullptr), cs(2, nullptr);
         auto cleanup = [&] {
             for (auto* v : {&up, &ready, &cs})
                 for (auto& e : *v)
@@ -2012,45 +1951,33 @@ int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, 
             if (!overlap) {  // sequential reference schedule: every upload before any compute
                 EKV_CUDA(cudaStreamWaitEvent(st, up[L], 0));
             }
-            const int prev_len = s->user_len;
-            float* scratch = nullptr;
-            EKV_CUDA(cudaMallocAsync((void**)&scratch, sizeof(float) * 2 * n * m->h, st));
-            EKV_CUDA(cudaEventRecord(cs[0], st));
-            forward_layer_major(s, emb_dev, n, prev_len, st, overlap ? ready.data() : nullptr, scratch, nullptr);
-            EKV_CUDA(cudaEventRecord(cs[L], st));
-            if (out_dev)
-                EKV_CUDA(cudaMemcpyAsync(out_dev, s->pre_out + (size_t)prev_len * m->h,
-                                         sizeof(float) * n * m->h, cudaMemcpyDeviceToDevice, st));
+            streamed_forward(s, emb_dev, n, out_dev, overlap ? ready.data() : nullptr, cs[0], cs[1],
+                             t_comp_ms);
             EKV_CUDA(cudaStreamSynchronize(cp));
             EKV_CUDA(cudaStreamSynchronize(st));
-            for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comm_ms[l], up[l], up[l + 1]));
-            float tot = 0.f;
-            EKV_CUDA(cudaEventElapsedTime(&tot, up[0], cs[L]));
-            *total_ms = tot;
-            // per-layer compute: the same rows again, layer by layer with the context resident
-            // (diagnostic; rewrites the same user-cache rows and outputs with identical values)
-            {
-                std::vector<cudaEvent_t> lev(L + 1);
-                for (auto& e : lev) EKV_CUDA(cudaEventCreate(&e));
-                forward_layer_major(s, emb_dev, n, prev_len, st, nullptr, scratch, lev.data());
-                EKV_CUDA(cudaStreamSynchronize(st));
-                for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comp_ms[l], lev[l], lev[l + 1]));
-                for (auto& e : lev) cudaEventDestroy(e);
-            }
-            // state: n more user rows; decode continues from the last row (xa[0]), step 0
-            launch_advance(s->state, n, st);
-            EKV_CUDA(cudaMemsetAsync(&s->state->step, 0, sizeof(int), st));
-            EKV_CUDA(cudaMemcpyAsync(s->xa, scratch + (size_t)(n - 1) * m->h, sizeof(float) * m->h,
-                                     cudaMemcpyDeviceToDevice, st));
-            EKV_CUDA(cudaFreeAsync(scratch, st));
-            s->user_len += n;
-            s->steps = 0;
+            if (t_comm_ms)
+                for (int l = 0; l < L; ++l) EKV_CUDA(cudaEventElapsedTime(&t_comm_ms[l], up[l], up[l + 1]));
+            if (total_ms) EKV_CUDA(cudaEventElapsedTime(total_ms, up[0], cs[1]));
         } catch (...) {
             cleanup();
             throw;
         }
         cleanup();
-        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int ekv_session_forward_streamed(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
+                                 void* const* layer_ready) {
+    return guard([&] {
+        require(s && emb_dev, "ekv_session_forward_streamed: null argument");
+        require(n >= 1, "ekv_session_forward_streamed: n must be >= 1");
+        ekv_model_s* m = s->model;
+        check_overflow(s, n);
+        set_dev(m->ctx);
+        std::vector<cudaEvent_t> ready(m->cfg.num_layers, nullptr);
+        if (layer_ready)
+            for (int l = 0; l < m->cfg.num_layers; ++l) ready[l] = (cudaEvent_t)layer_ready[l];
+        streamed_forward(s, emb_dev, n, out_dev, ready.data(), nullptr, nullptr, nullptr);
     });
 }
 

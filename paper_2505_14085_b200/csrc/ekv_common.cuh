@@ -31,6 +31,14 @@ inline void require(bool ok, const std::string& msg, int status = EKV_EINVAL) {
 // Kernel launch accounting (ekv_ctx_kernel_launches).
 void count_launches(int64_t n);
 
+// Per-device launch properties.  The dynamic shared-memory attribute and the
+// occupancy of a kernel belong to the device context, and one process may drive
+// several GPUs (one ekv_ctx per host thread), so both are cached per
+// (device ordinal, kernel) under a lock, never process-wide.
+void ensure_smem_attr(const void* fn, int bytes);   // on the current device
+int device_sm_count();                              // SMs of the current device
+int blocks_per_sm(const void* fn, int threads, int smem);  // occupancy, current device
+
 constexpr int kWarp = 32;
 
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }

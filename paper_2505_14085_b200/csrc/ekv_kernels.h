@@ -104,5 +104,62 @@ void launch_advance(DevState* s, int n, cudaStream_t st);
 // ---- K1 alignment GEMM (tcgen05 / TMEM / TMA) --------------------------------
 void launch_align_qnorm(const void* X, const void* WqT, int S, int h_c, int n_cols, double* colsq,
                         cudaStream_t st);
+constexpr int kMaxAlignLayers = 64;
+// Kernel parameters of K1 (by value, __grid_constant__).
+struct AlignArgs {
+    int m_layers, S, h_c, n_cols;
+    int fold;                        // 0: colsq [m][n_cols]; d_c: colsq [d_c] over heads and layers
+    double* colsq;
+    int x_index[kMaxAlignLayers];    // layer coordinate of group i in the X / W_Q tensor maps
+    int w_index[kMaxAlignLayers];
+    // fused K2 (warps 2-3): kcolsq[c] += sum over every row of every k[i] of K[row][c]^2
+    double* kcolsq;
+    int k_layers, d_c;
+    int64_t k_rows;                  // rows (H*S) per layer
+    const uint16_t* k[kMaxAlignLayers];
+};
+// Host description of one K1 launch.  X layers live at X + x_index[i]*x_stride
+// ([S][h_c] each, stride 0 = S*h_c), W_Q^T layers at WqT + w_index[i]*w_stride
+// ([n_cols][h_c], stride 0 = n_cols*h_c); null index tables mean 0..m-1.
+struct AlignLaunch {
+    const void* X = nullptr;
+    int64_t x_stride = 0;
+    const int* x_index = nullptr;
+    const void* WqT = nullptr;
+    int64_t w_stride = 0;
+    const int* w_index = nullptr;
+    int m = 0, S = 0, h_c = 0, n_cols = 0;
+    int fold = 0;
+    double* colsq = nullptr;
+    double* kcolsq = nullptr;   // null: no fused K norms
+    const void* const* k = nullptr;
+    int k_layers = 0, d_c = 0;
+    int64_t k_rows = 0;
+};
+void launch_align(const AlignLaunch& p, cudaStream_t st);
+
+// ---- small device utilities (k_util.cu) ------------------------------------------
+// Reference ranking (head_prune.cpp:98-107) on the device: score_c =
+// sqrt(q[c])*sqrt(k[c]) in fp64, stable descending order, keep the first
+// `retained`, listed ascending -> kept[retained]; margin = (s[r-1]-s[r])/s[r-1].
+void launch_rank_channels(const double* q, const double* k, int d_c, int retained, int* kept,
+                          double* margin, cudaStream_t st);
+void launch_f32_to_bf16(const float* src, uint16_t* dst, int64_t n, cudaStream_t st);
+void launch_f32_to_f64(const float* src, double* dst, int64_t n, cudaStream_t st);
+// x0[r] = gamma * (emb[r] + pos[p0 + r]) + bias (the layer-0 input transform, fp32)
+void launch_input_transform(const float* emb, const float* gamma, const float* bias,
+                            const uint16_t* pos, int p0, int n, int h, float* x0, cudaStream_t st);
+// fp64 column sums of squares of an fp64 matrix [rows][d] (accumulated)
+void launch_colsq_f64(const double* m, int64_t rows, int d, double* colsq, cudaStream_t st);
+// exact dequantisation to fp64: dst = code * (double)scale
+void launch_kv_dequant_f64(const void* codes, const float* scales, int64_t rows, int d_e, int bits,
+                           int group, double* dst, cudaStream_t st);
+// reference-order fp64 matmul (bit-identical to matrix.cpp:19-36): out[n][m] = a[n][k] b[k][m]
+void launch_matmul_f64(const double* a, const double* b, int n, int k, int m, double* out,
+                       cudaStream_t st);
+// segment_attention_prefix in fp64 (cache_merge.cpp:12-38); logits scratch [n];
+// stats = {sigma, shift}
+void launch_segment_attention_f64(const double* q, const double* k, const double* v, int n, int d,
+                                  int vd, double* logits, double* o, double* stats, cudaStream_t st);
 
 }  // namespace ekv

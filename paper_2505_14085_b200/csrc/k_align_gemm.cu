@@ -21,6 +21,8 @@
 // bug fails the launch instead of hanging the device.
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
 
@@ -152,10 +154,69 @@ __device__ __forceinline__ float butterfly_colsum(float* v, int lane) {
     return v[0];
 }
 
+// Fused K2 (warps 2-3, otherwise idle): per-column sums of squares of the cached
+// cloud K rows (d_c bf16 each) of every matched layer, the K half of the channel
+// score (head_prune.cpp:92-97).  Each CTA streams a contiguous slice of the rows
+// with 16-byte loads (8 in flight per thread) while the tensor pipe runs K1, so
+// the K read (m*H*S*d_c*2 B) hides under the GEMM.  fp32 partials over <= 32 rows
+// per thread are folded into fp64.
+__device__ __forceinline__ void fused_kcolsq(const AlignArgs& a, int t) {
+    const int lpr = a.d_c / 8;  // lanes per row
+    const int rpi = 64 / lpr;   // rows per pass of the 64 threads
+    const int cseg = t % lpr;
+    const int64_t T = (int64_t)a.k_layers * a.k_rows;
+    const int64_t r1 = T * (blockIdx.x + 1) / gridDim.x;
+    int64_t r = T * blockIdx.x / gridDim.x + t / lpr;
+    int layer = (int)(r / a.k_rows);
+    int64_t row = r - (int64_t)layer * a.k_rows;
+    double acc64[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    constexpr int U = 8;
+    while (r < r1) {
+        uint4 v[U];
+        int n = 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (r < r1) {
+                v[u] = ld_stream(a.k[layer] + row * a.d_c + cseg * 8);
+                ++n;
+                r += rpi;
+                row += rpi;
+                while (row >= a.k_rows && layer + 1 < a.k_layers) {
+                    row -= a.k_rows;
+                    ++layer;
+                }
+            }
+        }
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (u < n) {
+                const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float lo = bf16_lo(w[k]), hi = bf16_hi(w[k]);
+                    acc[2 * k] = fmaf(lo, lo, acc[2 * k]);
+                    acc[2 * k + 1] = fmaf(hi, hi, acc[2 * k + 1]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc64[k] += (double)acc[k];
+    }
+    const int lane = t & 31;
+    for (int o = lpr; o < 32; o <<= 1)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc64[k] += __shfl_xor_sync(0xffffffffu, acc64[k], o);
+    if (lane < lpr)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) atomicAdd(&a.kcolsq[cseg * 8 + k], acc64[k]);
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     align_qnorm_kernel(const __grid_constant__ CUtensorMap map_x,
-                       const __grid_constant__ CUtensorMap map_w, int m_layers, int S, int h_c,
-                       int n_cols, double* __restrict__ colsq) {
+                       const __grid_constant__ CUtensorMap map_w, const __grid_constant__ AlignArgs a) {
+    const int m_layers = a.m_layers, S = a.S, h_c = a.h_c, n_cols = a.n_cols;
+    double* __restrict__ colsq = a.colsq;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;
@@ -210,8 +271,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_3d(&map_x, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM, layer);
-                    tma_load_3d(&map_w, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN, layer);
+                    tma_load_3d(&map_x, &full[stage], sA + stage * A_BYTES, kb * BK, mb * BM,
+                                a.x_index[layer]);
+                    tma_load_3d(&map_w, &full[stage], sB + stage * B_BYTES, kb * BK, nb * BN,
+                                a.w_index[layer]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -272,12 +335,27 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (lane == 0) mbar_arrive(&tempty[acc]);
             asm volatile("bar.sync 1, 128;" ::: "memory");
             const int et = threadIdx.x - 128;
-            for (int col = et; col < BN; col += 128) {
-                const float s = red[col] + red[BN + col] + red[2 * BN + col] + red[3 * BN + col];
-                atomicAdd(&colsq[(size_t)layer * n_cols + nb * BN + col], (double)s);
+            if (a.fold == 0) {
+                for (int col = et; col < BN; col += 128) {
+                    const float s = red[col] + red[BN + col] + red[2 * BN + col] + red[3 * BN + col];
+                    atomicAdd(&colsq[(size_t)layer * n_cols + nb * BN + col], (double)s);
+                }
+            } else {
+                // fold heads (and, across tiles, layers) into [d_c]: the reference scores
+                // one mask over every stacked (layer, head) row (sim.cpp:236-256)
+                for (int col = et; col < BN; col += 128)
+                    red[col] = red[col] + red[BN + col] + red[2 * BN + col] + red[3 * BN + col];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                for (int c = et; c < a.fold; c += 128) {
+                    double s = 0.0;
+                    for (int j = c; j < BN; j += a.fold) s += (double)red[j];
+                    atomicAdd(&colsq[c], s);
+                }
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
         }
+    } else if (a.kcolsq != nullptr) {  // warps 2-3
+        fused_kcolsq(a, threadIdx.x - 64);
     }
     tc_fence_before();
     __syncthreads();
@@ -310,22 +388,6 @@ static PFN_encodeTiled get_encode() {
         fn = (PFN_encodeTiled)p;
     }
     return fn;
-}
-
-static CUtensorMap make_map_3d(const void* base, uint64_t inner, uint64_t rows, uint64_t layers,
-                               uint32_t box_rows) {
-    CUtensorMap m;
-    cuuint64_t dims[3] = {inner, rows, layers};
-    cuuint64_t strides[2] = {inner * 2, inner * rows * 2};
-    cuuint32_t box[3] = {(cuuint32_t)k1::BK, box_rows, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
-                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")",
-            EKV_ECUDA);
-    return m;
 }
 
 CUtensorMap make_map_2d(const void* base, CUtensorMapDataType dt, int elem_bytes, uint64_t inner,
@@ -390,33 +452,91 @@ CUtensorMap make_map_2d_bf16(const void* base, uint64_t inner, uint64_t rows, ui
     return m;
 }
 
-void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
-                                int n_cols, double* colsq, int num_sms, cudaStream_t st) {
+static CUtensorMap make_map_layers(const void* base, uint64_t inner, uint64_t rows, uint64_t layers,
+                                   uint64_t layer_stride_elems, uint32_t box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[3] = {inner, rows, layers};
+    cuuint64_t strides[2] = {inner * 2, layer_stride_elems * 2};
+    cuuint32_t box[3] = {(cuuint32_t)k1::BK, box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")",
+            EKV_ECUDA);
+    return m;
+}
+
+void launch_align(const AlignLaunch& p, cudaStream_t st) {
     using namespace k1;
-    require(S % BM == 0, "align_qnorm: S must be a multiple of 128", EKV_EUNSUPPORTED);
-    require(n_cols % BN == 0, "align_qnorm: H*d_c must be a multiple of 256", EKV_EUNSUPPORTED);
-    require(h_c % BK == 0, "align_qnorm: h_c must be a multiple of 64", EKV_EUNSUPPORTED);
-    const CUtensorMap mx = make_map_3d(X, h_c, S, m_layers, BM);
-    const CUtensorMap mw = make_map_3d(WqT, h_c, n_cols, m_layers, BN);
-    static bool attr = false;
-    if (!attr) {
-        EKV_CUDA(cudaFuncSetAttribute(align_qnorm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SMEM_BYTES));
-        attr = true;
+    require(p.m >= 1 && p.m <= kMaxAlignLayers,
+            "align_qnorm: 1.." + std::to_string(kMaxAlignLayers) + " matched layers per launch",
+            EKV_EUNSUPPORTED);
+    require(p.S % BM == 0, "align_qnorm: S must be a multiple of 128", EKV_EUNSUPPORTED);
+    require(p.n_cols % BN == 0, "align_qnorm: H*d_c must be a multiple of 256", EKV_EUNSUPPORTED);
+    require(p.h_c % BK == 0, "align_qnorm: h_c must be a multiple of 64", EKV_EUNSUPPORTED);
+    require(p.fold == 0 || (p.fold >= 1 && BN % p.fold == 0),
+            "align_qnorm: folded head_dim must divide 256", EKV_EUNSUPPORTED);
+    AlignArgs a{};
+    a.m_layers = p.m;
+    a.S = p.S;
+    a.h_c = p.h_c;
+    a.n_cols = p.n_cols;
+    a.fold = p.fold;
+    a.colsq = p.colsq;
+    int x_hi = 0, w_hi = 0;
+    for (int i = 0; i < p.m; ++i) {
+        a.x_index[i] = p.x_index ? p.x_index[i] : i;
+        a.w_index[i] = p.w_index ? p.w_index[i] : i;
+        require(a.x_index[i] >= 0 && a.w_index[i] >= 0, "align_qnorm: negative layer index");
+        x_hi = std::max(x_hi, a.x_index[i]);
+        w_hi = std::max(w_hi, a.w_index[i]);
     }
-    const int total = m_layers * (S / BM) * (n_cols / BN);
-    const int grid = total < num_sms ? total : num_sms;
-    align_qnorm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mx, mw, m_layers, S, h_c, n_cols, colsq);
+    if (p.kcolsq) {
+        require(p.d_c >= 8 && p.d_c <= 256 && (p.d_c & (p.d_c - 1)) == 0,
+                "kv_colnorm (fused): head_dim must be a power of two in [8, 256]", EKV_EUNSUPPORTED);
+        require(p.k_layers >= 1 && p.k_layers <= kMaxAlignLayers, "kv_colnorm (fused): bad layer count");
+        a.kcolsq = p.kcolsq;
+        a.k_layers = p.k_layers;
+        a.k_rows = p.k_rows;
+        a.d_c = p.d_c;
+        for (int i = 0; i < p.k_layers; ++i) {
+            require(((uintptr_t)p.k[i] & 15) == 0, "kv_colnorm (fused): K must be 16-byte aligned");
+            a.k[i] = (const uint16_t*)p.k[i];
+        }
+    }
+    const uint64_t xs = p.x_stride ? (uint64_t)p.x_stride : (uint64_t)p.S * p.h_c;
+    const uint64_t ws = p.w_stride ? (uint64_t)p.w_stride : (uint64_t)p.n_cols * p.h_c;
+    require(xs >= (uint64_t)p.S * p.h_c && ws >= (uint64_t)p.n_cols * p.h_c,
+            "align_qnorm: layer stride smaller than one layer");
+    const CUtensorMap mx = make_map_layers(p.X, p.h_c, p.S, x_hi + 1, xs, BM);
+    const CUtensorMap mw = make_map_layers(p.WqT, p.h_c, p.n_cols, w_hi + 1, ws, BN);
+    ensure_smem_attr((const void*)align_qnorm_kernel, SMEM_BYTES);
+    const int total = p.m * (p.S / BM) * (p.n_cols / BN);
+    const int sms = device_sm_count();
+    const int grid = total < sms ? total : sms;
+    align_qnorm_kernel<<<grid, THREADS, SMEM_BYTES, st>>>(mx, mw, a);
     EKV_CUDA(cudaGetLastError());
     count_launches(1);
 }
 
+void launch_align_qnorm_batched(const void* X, const void* WqT, int m_layers, int S, int h_c,
+                                int n_cols, double* colsq, int /*num_sms*/, cudaStream_t st) {
+    AlignLaunch p{};
+    p.X = X;
+    p.WqT = WqT;
+    p.m = m_layers;
+    p.S = S;
+    p.h_c = h_c;
+    p.n_cols = n_cols;
+    p.colsq = colsq;
+    launch_align(p, st);
+}
+
 void launch_align_qnorm(const void* X, const void* WqT, int S, int h_c, int n_cols, double* colsq,
                         cudaStream_t st) {
-    int dev = 0, sms = 148;
-    EKV_CUDA(cudaGetDevice(&dev));
-    EKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    launch_align_qnorm_batched(X, WqT, 1, S, h_c, n_cols, colsq, sms, st);
+    launch_align_qnorm_batched(X, WqT, 1, S, h_c, n_cols, colsq, 0, st);
 }
 
 }  // namespace ekv

@@ -1066,11 +1066,7 @@ void launch_batch_proj(const CUtensorMap& map_w, int w_row0, int N_out, int K, c
     int stages = (200 * 1024) / stage_bytes;
     if (stages > 6) stages = 6;
     const int smem = stages * stage_bytes + 1024 + 256;
-    static int attr = 0;
-    if (attr < smem) {
-        EKV_CUDA(cudaFuncSetAttribute(batch_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = 227 * 1024;
-    }
+    ensure_smem_attr((const void*)batch_proj_kernel, 227 * 1024);
     dim3 grid(N_out / BM, (B + BN - 1) / BN, KS);
     launch_pdl(batch_proj_kernel, grid, dim3(THREADS), smem, st, map_w, map_x, w_row0, N_out, K, B, BN, KS,
                stages, idesc_bf16(BM, BN), out);
@@ -1103,12 +1099,7 @@ template <int FMT>
 static void launch_ctx(const BatchCtxMaps& mp, const BatchCtxAttn& a, cudaStream_t st) {
     using namespace k10;
     using Cf = Cfg<64, FMT>;
-    static bool attr = false;
-    if (!attr) {
-        EKV_CUDA(cudaFuncSetAttribute(batch_ctx_attn_kernel<64, FMT>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
-        attr = true;
-    }
+    ensure_smem_attr((const void*)batch_ctx_attn_kernel<64, FMT>, Cf::SMEM);
     dim3 grid(a.H, a.nsplit, (a.B + BT - 1) / BT);
     launch_pdl(batch_ctx_attn_kernel<64, FMT>, grid, dim3(THREADS), Cf::SMEM, st, mp.k, mp.v, mp.ks, mp.vs, a);
 }

@@ -1257,11 +1257,7 @@ template <int D, int KC, bool TR>
 static void launch_dkt(const MegaArgs& a, int grid, cudaStream_t st) {
     auto fn = mk::decode_step_kernel<D, KC, TR>;
     const size_t smem = mega_smem_bytes(D);
-    static bool set = false;
-    if (!set) {
-        EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        set = true;
-    }
+    ensure_smem_attr((const void*)fn, (int)smem);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(mk::THREADS);

@@ -135,9 +135,7 @@ static void launch_r(const GemvArgs& a, cudaStream_t st) {
 #define EKV_GEMV_CASE(KC)                                                                        \
     case KC: {                                                                                   \
         auto fn = gemv_kernel<R, KC>;                                                            \
-        if (smem > 48 * 1024)                                                                    \
-            EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                          (int)smem));                                           \
+        if (smem > 48 * 1024) ensure_smem_attr((const void*)fn, (int)smem);                      \
         fn<<<blocks, kGemvThreads, smem, st>>>(a);                                               \
         break;                                                                                   \
     }

@@ -250,15 +250,8 @@ static bool try_fast(const CompressJobs& jobs, int n_jobs, int64_t rows, int d_c
     const int64_t total = (rows + TC::TILE - 1) / TC::TILE * n_jobs;
     auto fn = kv_compress_tile_kernel<DC, DE, BITS, TB, NS>;
     const int smem = NS * TC::BYTES + 64;
-    static int occ = 0, sms = 0;
-    if (!occ) {
-        EKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        EKV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, smem));
-        int dev = 0;
-        EKV_CUDA(cudaGetDevice(&dev));
-        EKV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (occ < 1) occ = 1;
-    }
+    const int occ = blocks_per_sm((const void*)fn, 128, smem);
+    const int sms = device_sm_count();
     int64_t grid = (int64_t)sms * occ;  // persistent: exactly the resident CTAs
     if (grid > total) grid = total;
     fn<<<(unsigned)grid, 128, smem, st>>>(jobs, n_jobs, rows, kept, group);

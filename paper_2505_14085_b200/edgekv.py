@@ -24,7 +24,7 @@ from .capi import EKV_KV_BF16, EKV_KV_INT4, EKV_KV_INT8, EkvError, call, ekv_mod
 __all__ = [
     "Context", "EkvError", "prune_retained", "align_qnorm", "kv_colnorm", "rank_channels",
     "select_channels", "prune_cache", "kv_compress", "kv_dequant", "decode_attention",
-    "match_layers", "match_layers_dev", "cache_source", "pipeline_schedule", "EdgeModel", "AssembledContext",
+    "match_layers", "match_layers_dev", "prefill", "deep_match", "prompt_context", "cache_source", "pipeline_schedule", "EdgeModel", "AssembledContext",
     "Session", "collaborative_decode", "build_deep_kv", "EKV_KV_BF16", "EKV_KV_INT8",
     "EKV_KV_INT4",
 ]
@@ -61,6 +61,11 @@ class Context:
         call("ekv_ctx_kernel_launches", self.h, C.byref(n))
         return n.value
 
+    def memset(self, t: torch.Tensor, value: int = 0):
+        """Byte fill of a device tensor on the context stream (no torch kernel)."""
+        call("ekv_memset", self.h, _ptr(t), value, t.numel() * t.element_size())
+        return t
+
     def fill_uniform_bf16(self, out: torch.Tensor, seed: int, stream_id: int, lo: float, hi: float):
         assert out.dtype == torch.bfloat16 and out.is_contiguous()
         call("ekv_fill_uniform_bf16", self.h, _ptr(out), out.numel(), seed, stream_id, lo, hi)
@@ -96,9 +101,10 @@ def align_qnorm(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, colsq: torch.T
     m, S, hc = X.shape
     n = WqT.shape[1]
     assert WqT.shape == (m, n, hc) and X.dtype == WqT.dtype == torch.bfloat16
-    if colsq is None:
-        colsq = torch.zeros((m, n), dtype=torch.float64, device=X.device)
     _sync_in()
+    if colsq is None:
+        colsq = torch.empty((m, n), dtype=torch.float64, device=X.device)
+        ctx.memset(colsq)
     call("ekv_align_qnorm", ctx.h, _ptr(X), _ptr(WqT), m, S, hc, n, _ptr(colsq))
     ctx.synchronize()
     return colsq
@@ -107,9 +113,10 @@ def align_qnorm(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, colsq: torch.T
 def kv_colnorm(ctx: Context, K: torch.Tensor, colsq: torch.Tensor | None = None):
     """K2: per-channel sum of squares over every row of K (bf16 [..., d_c]) -> fp64 [d_c]."""
     d = K.shape[-1]
-    if colsq is None:
-        colsq = torch.zeros(d, dtype=torch.float64, device=K.device)
     _sync_in()
+    if colsq is None:
+        colsq = torch.empty(d, dtype=torch.float64, device=K.device)
+        ctx.memset(colsq)
     call("ekv_kv_colnorm", ctx.h, _ptr(K), K.numel() // d, d, _ptr(colsq))
     ctx.synchronize()
     return colsq
@@ -131,8 +138,8 @@ def select_channels(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, K: torch.T
     """select_channels (head_prune.cpp:83-108) over the stacked rows of every matched
     layer and head, with Q recomputed on the tensor cores (K1) and K norms read
     from the cloud cache (K2).  Returns (kept, margin, q_colsq, k_colsq)."""
-    qs = align_qnorm(ctx, X, WqT)                             # [m][H*d_c]
-    q_c = qs.reshape(-1, d_c).sum(dim=0).cpu().numpy()        # fp64 over layers and heads
+    qs = align_qnorm(ctx, X, WqT).cpu().numpy()               # [m][H*d_c]
+    q_c = qs.reshape(-1, d_c).sum(axis=0)                     # fp64 over layers and heads
     k_c = kv_colnorm(ctx, K).cpu().numpy()
     retained = prune_retained(lam, d_c)
     kept, margin = rank_channels(q_c, k_c, retained)
@@ -213,15 +220,16 @@ def decode_attention(ctx: Context, q: torch.Tensor, seg: Segment, user_k: torch.
 
 
 # ------------------------------------------------------------------ host logic
-def match_layers(edge_outs: np.ndarray, cloud_outs: np.ndarray, theta_cka: float, theta_rsa: float):
-    """match_layers (layer_match.cpp:166-228): returns (cka, rsa, best) with best[le] = -1
-    for an unmatched edge layer."""
+def match_layers(ctx: "Context", edge_outs: np.ndarray, cloud_outs: np.ndarray, theta_cka: float,
+                 theta_rsa: float):
+    """match_layers (layer_match.cpp:166-228) from host fp64 probe outputs, computed by K7
+    on the device: returns (cka, rsa, best) with best[le] = -1 for an unmatched edge layer."""
     e = np.ascontiguousarray(edge_outs, dtype=np.float64)
     c = np.ascontiguousarray(cloud_outs, dtype=np.float64)
     me, n, ce = e.shape
     nc, _, cc = c.shape
     cka = np.zeros((me, nc)); rsa = np.zeros((me, nc)); best = np.zeros(me, dtype=np.int32)
-    call("ekv_match_layers", _dp(e), me, ce, _dp(c), nc, cc, n, theta_cka, theta_rsa, _dp(cka),
+    call("ekv_match_layers", ctx.h, _dp(e), me, ce, _dp(c), nc, cc, n, theta_cka, theta_rsa, _dp(cka),
          _dp(rsa), _ip(best))
     return cka, rsa, best
 
@@ -519,37 +527,106 @@ def collaborative_decode(session: Session, user_embeddings: np.ndarray, steps: i
     return pre[:U], st[:steps]
 
 
-def build_deep_kv(ctx: Context, context: AssembledContext, deep_match: dict, X: torch.Tensor,
-                  WqT: torch.Tensor, cloud_k: torch.Tensor, cloud_v: torch.Tensor, lam: float,
-                  cloud_layers: list):
-    """Artifacts::build_deep_kv (sim.cpp:217-265) on the GPU: K1+K2 channel scores
-    over every distinct matched cloud layer, host ranking, then K3 compression of
-    each matched layer's K/V straight into the context's deep-layer storage.
+def prefill(model: "EdgeModel", emb: torch.Tensor, want_x0: bool = False, want_kv: bool = False):
+    """prefill (transformer.cpp:244-251) on the device: emb fp32 [n][h] (device) at positions
+    0..n-1.  Returns (layer_outputs fp32 [L][n][h], x0 fp32 [n][h] | None,
+    k bf16 [L][H][n][d] | None, v | None)."""
+    emb = emb.contiguous().float()
+    n = emb.shape[0]
+    dev = emb.device
+    lo = torch.empty((model.L, n, model.h), dtype=torch.float32, device=dev)
+    x0 = torch.empty((n, model.h), dtype=torch.float32, device=dev) if want_x0 else None
+    k = v = None
+    if want_kv:
+        k = torch.empty((model.L, model.H, n, model.d), dtype=torch.bfloat16, device=dev)
+        v = torch.empty_like(k)
+    _sync_in()
+    call("ekv_prefill", model.hnd, _ptr(emb), n, _ptr(lo), _ptr(x0), _ptr(k), _ptr(v))
+    return lo, x0, k, v
 
-    deep_match: {edge_layer: cloud_layer}; cloud_layers: the distinct matched cloud
-    layers in the order X / WqT / cloud_k / cloud_v are stacked (m of them):
-      X [m][S][h_c], WqT [m][H*d_c][h_c], cloud_k/v [m][H][S][d_c] (bf16).
+
+def deep_match(edge: "EdgeModel", cloud: "EdgeModel", edge_probe: torch.Tensor,
+               cloud_probe: torch.Tensor, deep_layers: int, theta_cka: float, theta_rsa: float):
+    """Artifacts::deep_match (sim.cpp:100-122) on the device: probe prefill of both models,
+    K7 layer map, deep edge layer -> cloud layer.  Returns ({le: lc}, cka, rsa, best)."""
+    ep = edge_probe.contiguous().float()
+    cp = cloud_probe.contiguous().float()
+    n = ep.shape[0]
+    if cp.shape[0] != n:
+        raise ValueError("deep_match: probe row-count mismatch")
+    M, N = edge.L, cloud.L
+    dm = np.zeros(max(deep_layers, 1), np.int32)
+    cka = np.zeros((M, N)); rsa = np.zeros((M, N)); best = np.zeros(M, np.int32)
+    _sync_in()
+    call("ekv_deep_match", edge.hnd, cloud.hnd, _ptr(ep), _ptr(cp), n, deep_layers, theta_cka,
+         theta_rsa, _ip(dm), _dp(cka), _dp(rsa), _ip(best))
+    return {M - deep_layers + i: int(dm[i]) for i in range(deep_layers)}, cka, rsa, best
+
+
+def prompt_context(edge: "EdgeModel", cloud: "EdgeModel", emb_edge: torch.Tensor,
+                   emb_cloud: torch.Tensor | None, deep_map: dict, lam: float,
+                   context: "AssembledContext"):
+    """Artifacts::prompt + build_deep_kv + assembled_context (sim.cpp:124-138, 186-265) on
+    the device: edge prefill of the S context rows -> local layers of `context`; cloud
+    prefill -> hidden states + KV of the matched layers -> K1/K2 mask -> K3 codes into the
+    deep layers [M - n, M).  deep_map {edge_layer: cloud_layer} covers exactly those layers.
     Returns (kept, cut_margin)."""
-    m, H, S, d_c = cloud_k.shape
-    kept, margin, _, _ = select_channels(ctx, X, WqT, cloud_k, lam, d_c)
-    kept_t = torch.as_tensor(kept, device=cloud_k.device)
-    srcs, codes, scales = [], [], []
-    fmt = None
-    for le, lc in sorted(deep_match.items()):
-        i = cloud_layers.index(lc)
-        seg = context.segment(le)
-        assert seg.format in (EKV_KV_INT8, EKV_KV_INT4) and seg.S == S
-        assert fmt in (None, seg.format)
-        fmt, group = seg.format, seg.group
-        srcs += [cloud_k[i].data_ptr(), cloud_v[i].data_ptr()]
-        codes += [seg.k, seg.v]
-        scales += [seg.k_scales, seg.v_scales]
-    n = len(srcs)
-    arr = lambda xs: (C.c_void_p * n)(*xs)
-    compress_batched(ctx, n, arr(srcs), H * S, d_c, kept_t, len(kept), fmt, group, arr(codes),
-                     arr(scales))
-    ctx.synchronize()
-    return kept, margin
+    M = edge.L
+    les = sorted(deep_map)
+    n = len(les)
+    if les != list(range(M - n, M)):
+        raise ValueError("prompt_context: the deep layers must be the last n edge layers")
+    dm = np.asarray([deep_map[le] for le in les] or [0], np.int32)
+    ee = emb_edge.contiguous().float()
+    ec = emb_cloud.contiguous().float() if emb_cloud is not None else None
+    kept = np.zeros(max(prune_retained(lam, cloud.d), 1), np.int32)
+    margin = C.c_double(float("inf"))
+    _sync_in()
+    call("ekv_prompt_context", edge.hnd, cloud.hnd, _ptr(ee), _ptr(ec), n, _ip(dm), lam, context.hnd,
+         _ip(kept), C.byref(margin))
+    return kept[:prune_retained(lam, cloud.d)], margin.value
+
+
+def build_deep_kv(ctx: Context, context: AssembledContext, deep_match: dict, X: torch.Tensor,
+                  WqT: torch.Tensor, cloud_k, cloud_v, lam: float, cloud_layers: list,
+                  x_index=None, wq_index=None, wq_stride: int = 0):
+    """Artifacts::build_deep_kv (sim.cpp:217-265) through ekv_build_deep_kv: K1 channel
+    scores (K column norms fused) over every distinct matched cloud layer, the reference
+    ranking on the device and one batched K3 launch into the context's deep layers.
+
+    deep_match: {edge_layer: cloud_layer}; cloud_layers: the distinct matched cloud layers
+    (sorted) in the order of cloud_k / cloud_v (a [m][H][S][d_c] tensor or a list of m
+    [H][S][d_c] tensors, bf16).  X: bf16 [m][S][h_c] (or, with x_index, any [*][S][h_c]
+    stack), WqT: bf16 [m][H*d_c][h_c] (or with wq_index / wq_stride an ekv_model's weights).
+    Returns (kept, cut_margin)."""
+    m = len(cloud_layers)
+    ks = [cloud_k[i] for i in range(m)]
+    vs = [cloud_v[i] for i in range(m)]
+    H, S, d_c = ks[0].shape
+    for t in ks + vs:
+        if t.dtype != torch.bfloat16 or tuple(t.shape) != (H, S, d_c) or not t.is_contiguous():
+            raise ValueError("build_deep_kv: cloud K/V must be contiguous bf16 [H][S][d_c] per layer")
+    if H != context.model.H:
+        raise ValueError(f"assemble_context: head count mismatch (cloud {H}, edge {context.model.H})")
+    if prune_retained(lam, d_c) != context.model.d:
+        raise ValueError("assemble_context: dim mismatch; align with head pruning")
+    if S != context.S:
+        raise ValueError(f"assemble_context: dim mismatch (cloud context {S}, assembled {context.S})")
+    le_list = sorted(deep_match)
+    src = [cloud_layers.index(deep_match[le]) for le in le_list]
+    kp = (C.c_void_p * m)(*[t.data_ptr() for t in ks])
+    vp = (C.c_void_p * m)(*[t.data_ptr() for t in vs])
+    xi = (C.c_int * m)(*(x_index if x_index is not None else range(m)))
+    wi = (C.c_int * m)(*(wq_index if wq_index is not None else range(m)))
+    cl = capi.ekv_cloud_kv(m, S, H, d_c, X.data_ptr(), 0, xi, WqT.data_ptr(), wq_stride, wi,
+                           C.cast(kp, C.POINTER(C.c_void_p)), C.cast(vp, C.POINTER(C.c_void_p)))
+    kept = np.zeros(prune_retained(lam, d_c), np.int32)
+    margin = C.c_double()
+    le_a = np.asarray(le_list, np.int32); src_a = np.asarray(src, np.int32)
+    _sync_in()
+    call("ekv_build_deep_kv", ctx.h, C.byref(cl), lam, context.hnd, len(le_list), _ip(le_a), _ip(src_a),
+         _ip(kept), C.byref(margin))
+    return kept, margin.value
 
 
 def compress_batched(ctx: Context, n: int, src_ptrs, rows: int, d_c: int, kept_t: torch.Tensor,

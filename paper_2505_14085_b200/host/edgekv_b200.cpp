@@ -10,6 +10,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <set>
 #include <stdexcept>
 #include <string>
 
@@ -55,11 +56,14 @@ struct Runtime {
     std::mutex mu;
     int device = 0;
     ekv_ctx_t ctx = nullptr;
+    // device copies of Model objects, keyed by a hash of ALL their weight data
+    // (a reference caller may mutate weights in place), least recently used first
     struct ModelEntry {
-        ekv_model_t handle = nullptr;
         uint64_t signature = 0;
+        ekv_model_t handle = nullptr;
     };
-    std::map<const Model*, ModelEntry> models;
+    static constexpr size_t kMaxModels = 4;
+    std::vector<ModelEntry> models;
 
     ekv_ctx_t get() {
         if (!ctx) {
@@ -81,22 +85,34 @@ Runtime& rt() {
 
 ekv_ctx_t device_ctx() { return rt().get(); }
 
+// 64-bit hash of every weight word of the model (word-wise multiply-xorshift:
+// the same coverage as the reference's fnv1a checksum, transformer.cpp:118-131,
+// at ~1 ns per double).
 uint64_t signature(const Model& m) {
-    uint64_t h = 1469598103934665603ull;
-    auto mix = [&](double v) {
-        uint64_t u;
-        std::memcpy(&u, &v, 8);
-        h = (h ^ u) * 1099511628211ull;
+    uint64_t h = 0x9E3779B97F4A7C15ull;
+    auto mixw = [&](uint64_t u) {
+        h ^= u + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+        h *= 0xBF58476D1CE4E5B9ull;
+    };
+    auto mixv = [&](const std::vector<double>& v) {
+        mixw(v.size());
+        for (double x : v) {
+            uint64_t u;
+            std::memcpy(&u, &x, 8);
+            mixw(u);
+        }
     };
     const ModelConfig& c = m.config;
-    mix(c.num_layers), mix(c.num_heads), mix(c.head_dim), mix(c.max_positions);
+    mixw((uint64_t)c.num_layers), mixw((uint64_t)c.num_heads), mixw((uint64_t)c.head_dim),
+        mixw((uint64_t)c.max_positions);
     for (const LayerWeights& lw : m.layers) {
         for (const HeadWeights& w : lw.heads)
-            for (const Matrix* x : {&w.wq, &w.wk, &w.wv})
-                if (!x->data.empty()) mix(x->data.front()), mix(x->data.back());
-        if (!lw.out_proj.data.empty()) mix(lw.out_proj.data.front()), mix(lw.out_proj.data.back());
+            for (const Matrix* x : {&w.wq, &w.wk, &w.wv}) mixv(x->data);
+        mixv(lw.out_proj.data);
+        mixv(lw.gamma);
+        mixv(lw.bias);
     }
-    if (!m.pos_embedding.data.empty()) mix(m.pos_embedding.data.back());
+    mixv(m.pos_embedding.data);
     return h;
 }
 
@@ -133,6 +149,27 @@ ekv_model_t upload_model(ekv_ctx_t ctx, const Model& m) {
     for (size_t i = 0; i < pos.size(); ++i) pos[i] = to_bf16(m.pos_embedding.data[i]);
     check(ekv_model_set_io(mh, gamma.data(), bias.data(), pos.data()));
     return mh;
+}
+
+// The device copy of `m` (uploaded on first use, re-uploaded when any weight
+// changed; at most Runtime::kMaxModels kept).  Caller holds rt().mu.
+ekv_model_t device_model(const Model& m) {
+    Runtime& r = rt();
+    const uint64_t sig = signature(m);
+    for (size_t i = 0; i < r.models.size(); ++i)
+        if (r.models[i].signature == sig) {
+            Runtime::ModelEntry e = r.models[i];
+            r.models.erase(r.models.begin() + (long)i);
+            r.models.push_back(e);  // most recently used last
+            return e.handle;
+        }
+    if (r.models.size() >= Runtime::kMaxModels) {
+        ekv_model_destroy(r.models.front().handle);
+        r.models.erase(r.models.begin());
+    }
+    ekv_model_t h = upload_model(r.get(), m);
+    r.models.push_back(Runtime::ModelEntry{sig, h});
+    return h;
 }
 
 std::vector<uint16_t> head_major_bf16(const std::vector<Matrix>& per_head, int S, int d) {
@@ -222,27 +259,23 @@ ChannelMask select_channels(const Matrix& q, const Matrix& k, const PruneSpec& s
     std::lock_guard<std::mutex> g(rt().mu);
     ekv_ctx_t ctx = rt().get();
     const int d = spec.head_dim;
-    std::vector<double> qsq(d, 0.0), ksq(d, 0.0);
+    // column sums of squares in fp64 on the device (no rounding of Q / K)
     DevBuf sums(sizeof(double) * 2 * d);
     check(ekv_memset(ctx, sums.p, 0, sums.n));
     for (int which = 0; which < 2; ++which) {
         const Matrix& m = which ? k : q;
         if (m.rows == 0) continue;
-        std::vector<uint16_t> b(m.data.size());
-        for (size_t i = 0; i < b.size(); ++i) b[i] = to_bf16(m.data[i]);
-        DevBuf dev(b.size() * 2);
-        dev.put(b.data());
-        check(ekv_kv_colnorm(ctx, dev.p, (int64_t)m.rows, d, (double*)sums.p + which * d));
+        DevBuf dev(m.data.size() * 8);
+        dev.put(m.data.data());
+        check(ekv_colsq_f64(ctx, (const double*)dev.p, (int64_t)m.rows, d, (double*)sums.p + which * d));
         check(ekv_ctx_synchronize(ctx));
     }
     std::vector<double> both(2 * d);
     sums.get(both.data(), sizeof(double) * 2 * d);
-    std::copy(both.begin(), both.begin() + d, qsq.begin());
-    std::copy(both.begin() + d, both.end(), ksq.begin());
     ChannelMask mask;
     mask.head_dim = d;
     mask.kept.resize(spec.retained);
-    check(ekv_rank_channels(qsq.data(), ksq.data(), d, spec.retained, mask.kept.data(), nullptr));
+    check(ekv_rank_channels(both.data(), both.data() + d, d, spec.retained, mask.kept.data(), nullptr));
     return mask;
 }
 
@@ -275,6 +308,142 @@ KVCache prune_cache(const KVCache& cache, const ChannelMask& mask) {
     return out;
 }
 
+// ---------------------------------------------------------------- transformer
+QkvRows project_qkv(const Model& model, const Matrix& x, int layer, int head) {
+    const ModelConfig& cfg = model.config;
+    if (layer < 0 || layer >= cfg.num_layers)
+        throw std::invalid_argument("project_qkv: layer " + std::to_string(layer) + " out of range [0," +
+                                    std::to_string(cfg.num_layers - 1) + "]");
+    if (head < 0 || head >= cfg.num_heads)
+        throw std::invalid_argument("project_qkv: head " + std::to_string(head) + " out of range [0," +
+                                    std::to_string(cfg.num_heads - 1) + "]");
+    if (static_cast<int>(x.cols) != cfg.hidden_size)
+        throw std::invalid_argument("project_qkv: input has " + std::to_string(x.cols) +
+                                    " cols, expected hidden_size " + std::to_string(cfg.hidden_size));
+    const HeadWeights& w = model.layers[layer].heads[head];
+    const int n = (int)x.rows, h = cfg.hidden_size, d = cfg.head_dim;
+    QkvRows r{Matrix(n, d), Matrix(n, d), Matrix(n, d)};
+    if (n == 0) return r;
+    std::lock_guard<std::mutex> g(rt().mu);
+    ekv_ctx_t ctx = rt().get();
+    DevBuf dx(x.data.size() * 8), dw((size_t)h * d * 8), dout((size_t)n * d * 8);
+    dx.put(x.data.data());
+    const Matrix* ws[3] = {&w.wq, &w.wk, &w.wv};
+    Matrix* outs[3] = {&r.q, &r.k, &r.v};
+    for (int i = 0; i < 3; ++i) {
+        dw.put(ws[i]->data.data());
+        check(ekv_matmul_f64(ctx, (const double*)dx.p, (const double*)dw.p, n, h, d, (double*)dout.p));
+        check(ekv_ctx_synchronize(ctx));
+        dout.get(outs[i]->data.data(), dout.n);
+    }
+    return r;
+}
+
+std::vector<Matrix> forward_rows(const Model& model, KVCache& cache, const Matrix& embeddings,
+                                 PositionKind kind, FlopCounts* fc) {
+    const ModelConfig& cfg = model.config;
+    if (cache.num_layers != cfg.num_layers || cache.num_heads != cfg.num_heads ||
+        cache.head_dim != cfg.head_dim)
+        throw std::invalid_argument("forward_rows: cache shape does not match model");
+    if (static_cast<int>(embeddings.cols) != cfg.hidden_size)
+        throw std::invalid_argument("forward_rows: embeddings have " + std::to_string(embeddings.cols) +
+                                    " cols, expected hidden_size " + std::to_string(cfg.hidden_size));
+    const int n = static_cast<int>(embeddings.rows);
+    const int old = cache.size();
+    if (old + n > cfg.max_positions)
+        throw std::invalid_argument("position overflow: " + std::to_string(old + n) +
+                                    " > max_positions " + std::to_string(cfg.max_positions));
+    const int L = cfg.num_layers, H = cfg.num_heads, d = cfg.head_dim, h = cfg.hidden_size;
+    std::vector<Matrix> outs;
+    if (n == 0) {
+        for (int l = 0; l < L; ++l) outs.emplace_back(0, h);
+        return outs;
+    }
+    std::vector<float> lo((size_t)L * n * h);
+    std::vector<uint16_t> kb((size_t)L * H * n * d), vb(kb.size());
+    {
+        std::lock_guard<std::mutex> g(rt().mu);
+        ekv_ctx_t ctx = rt().get();
+        ekv_model_t mh = device_model(model);
+        ekv_kvctx_t kvc = nullptr;
+        std::unique_ptr<ekv_kvctx_s, int (*)(ekv_kvctx_t)> kguard(nullptr, ekv_kvctx_destroy);
+        if (old > 0) {  // the cached rows become the context the new rows attend to
+            std::vector<int> fmt(L, EKV_KV_BF16);
+            check(ekv_kvctx_create(mh, old, fmt.data(), d, &kvc));
+            kguard.reset(kvc);
+            for (int l = 0; l < L; ++l) {
+                auto k = head_major_bf16(cache.keys[l], old, d);
+                auto v = head_major_bf16(cache.values[l], old, d);
+                check(ekv_kvctx_upload_bf16(kvc, l, k.data(), v.data()));
+            }
+        }
+        std::vector<float> e(embeddings.data.begin(), embeddings.data.end());
+        DevBuf de(e.size() * 4), dlo(lo.size() * 4), dk(kb.size() * 2), dv(vb.size() * 2);
+        de.put(e.data());
+        check(ekv_forward_rows(mh, kvc, (const float*)de.p, n, (float*)dlo.p, nullptr, dk.p, dv.p));
+        dlo.get(lo.data(), dlo.n);
+        dk.get(kb.data(), dk.n);
+        dv.get(vb.data(), dv.n);
+    }
+    auto f = [](uint16_t b) {
+        const uint32_t u = (uint32_t)b << 16;
+        float x;
+        std::memcpy(&x, &u, 4);
+        return (double)x;
+    };
+    for (int l = 0; l < L; ++l) {
+        Matrix x(n, h);
+        for (size_t i = 0; i < x.data.size(); ++i) x.data[i] = lo[(size_t)l * n * h + i];
+        outs.push_back(std::move(x));
+        for (int hd = 0; hd < H; ++hd) {
+            Matrix& ck = cache.keys[l][hd];
+            Matrix& cv = cache.values[l][hd];
+            const size_t base = ((size_t)l * H + hd) * n * d;
+            ck.data.reserve(ck.data.size() + (size_t)n * d);
+            cv.data.reserve(cv.data.size() + (size_t)n * d);
+            for (size_t i = 0; i < (size_t)n * d; ++i) {
+                ck.data.push_back(f(kb[base + i]));
+                cv.data.push_back(f(vb[base + i]));
+            }
+            ck.rows += n;
+            cv.rows += n;
+            ck.cols = cv.cols = d;
+        }
+    }
+    for (int i = 0; i < n; ++i) cache.positions.push_back(PositionTag{kind, old + i});
+    if (fc) {  // the reference's closed-form counts (transformer.cpp:267-283)
+        const int64_t k = H;
+        fc->proj += 3ll * n * h + (int64_t)L * n * k * 3 * d * (2ll * h - 1);
+        for (int l = 0; l < L; ++l)
+            for (int i = 0; i < n; ++i) {
+                const int64_t vis = old + i + 1;
+                fc->score += k * vis * (2ll * d - 1);
+                fc->softmax += k * (3 * vis + 1);
+                fc->value += k * (vis * 2 * d + d);
+            }
+        fc->out_proj += (int64_t)L * n * h * (2ll * h - 1);
+    }
+    return outs;
+}
+
+PrefillResult prefill(const Model& model, const Matrix& embeddings, FlopCounts* fc, PositionKind kind) {
+    PrefillResult res;
+    res.cache = KVCache::empty_for(model.config.num_layers, model.config.num_heads, model.config.head_dim);
+    res.layer_outputs = forward_rows(model, res.cache, embeddings, kind, fc);
+    return res;
+}
+
+Vec decode_step(const Model& model, KVCache& cache, const Vec& embedding, FlopCounts* fc,
+                PositionKind kind) {
+    if (static_cast<int>(embedding.size()) != model.config.hidden_size)
+        throw std::invalid_argument("decode_step: embedding size " + std::to_string(embedding.size()) +
+                                    " != hidden_size " + std::to_string(model.config.hidden_size));
+    Matrix row(1, embedding.size());
+    row.data = embedding;
+    std::vector<Matrix> outs = forward_rows(model, cache, row, kind, fc);
+    return outs.back().row(0);
+}
+
 // ---------------------------------------------------------------- decode attention
 SegmentAttention segment_attention(const Vec& q, const Matrix& k, const Matrix& v) {
     if (k.rows == 0 || v.rows == 0) throw std::invalid_argument("segment_attention: empty segment");
@@ -284,36 +453,18 @@ SegmentAttention segment_attention(const Vec& q, const Matrix& k, const Matrix& 
     if (q.size() != k.cols)
         throw std::invalid_argument("segment_attention: q has " + std::to_string(q.size()) +
                                     " dims, K has " + std::to_string(k.cols));
-    const int d = static_cast<int>(k.cols), n = static_cast<int>(k.rows);
-    if (v.cols != k.cols || !(d == 32 || d == 64 || d == 128))
-        throw std::invalid_argument("segment_attention: head_dim " + std::to_string(d) +
-                                    " has no B200 kernel (32, 64 or 128)");
+    const int d = static_cast<int>(k.cols), n = static_cast<int>(k.rows), vd = static_cast<int>(v.cols);
     std::lock_guard<std::mutex> g(rt().mu);
     ekv_ctx_t ctx = rt().get();
-    // the whole segment is the "user" segment of a one-row attention with no context
-    std::vector<uint16_t> kb(k.data.size()), vb(v.data.size());
-    for (size_t i = 0; i < kb.size(); ++i) kb[i] = to_bf16(k.data[i]);
-    for (size_t i = 0; i < vb.size(); ++i) vb[i] = to_bf16(v.data[i]);
-    std::vector<float> qf(q.begin(), q.end());
-    DevBuf dk(kb.size() * 2), dv(vb.size() * 2), dq(qf.size() * 4), dout(qf.size() * 4), dlse(4);
-    dk.put(kb.data());
-    dv.put(vb.data());
-    dq.put(qf.data());
-    ekv_segment none{EKV_KV_BF16, 0, d, nullptr, nullptr, nullptr, nullptr};
-    check(ekv_decode_attention(ctx, 1, 1, d, (const float*)dq.p, &none, dk.p, dv.p, n, n - 1,
-                               (float*)dout.p, (float*)dlse.p));
-    check(ekv_ctx_synchronize(ctx));
-    std::vector<float> o(d);
-    float lse = 0.0f;
-    dout.get(o.data(), dout.n);
-    dlse.get(&lse, 4);
+    DevBuf dq(q.size() * 8), dk(k.data.size() * 8), dv(v.data.size() * 8), dout((size_t)vd * 8);
+    dq.put(q.data());
+    dk.put(k.data.data());
+    dv.put(v.data.data());
     SegmentAttention res;
-    res.o.assign(o.begin(), o.end());
-    // the normaliser as (mantissa, shift) = (1, log-sum-exp): the same
-    // sigma_raw = sigma * e^shift the reference carries, and merge_attention
-    // only ever uses sigma * e^(shift - m)
-    res.shift = lse;
-    res.sigma = 1.0;
+    check(ekv_segment_attention_f64(ctx, (const double*)dq.p, (const double*)dk.p, (const double*)dv.p, n,
+                                    d, vd, (double*)dout.p, &res.sigma, &res.shift));
+    res.o.resize(vd);
+    dout.get(res.o.data(), dout.n);
     return res;
 }
 
@@ -411,17 +562,11 @@ CollaborativeResult collaborative_decode(const Model& edge_model, const Assemble
                                     " > max_positions " + std::to_string(cfg.max_positions));
     std::lock_guard<std::mutex> g(rt().mu);
     ekv_ctx_t ctx = rt().get();
-    Runtime::ModelEntry& me = rt().models[&edge_model];
-    const uint64_t sig = signature(edge_model);
-    if (!me.handle || me.signature != sig) {
-        if (me.handle) ekv_model_destroy(me.handle);
-        me.handle = upload_model(ctx, edge_model);
-        me.signature = sig;
-    }
+    ekv_model_t mh = device_model(edge_model);
     const int L = cfg.num_layers, H = cfg.num_heads, d = cfg.head_dim, h = cfg.hidden_size;
     std::vector<int> fmt(L, EKV_KV_BF16);
     ekv_kvctx_t kvc = nullptr;
-    check(ekv_kvctx_create(me.handle, S, fmt.data(), d, &kvc));
+    check(ekv_kvctx_create(mh, S, fmt.data(), d, &kvc));
     std::unique_ptr<ekv_kvctx_s, int (*)(ekv_kvctx_t)> kguard(kvc, ekv_kvctx_destroy);
     for (int l = 0; l < L && S > 0; ++l) {
         auto kb = head_major_bf16(context.cache.keys[l], S, d);
@@ -429,7 +574,7 @@ CollaborativeResult collaborative_decode(const Model& edge_model, const Assemble
         check(ekv_kvctx_upload_bf16(kvc, l, kb.data(), vb.data()));
     }
     ekv_session_t sess = nullptr;
-    check(ekv_session_create(me.handle, kvc, U + steps, &sess));
+    check(ekv_session_create(mh, kvc, U + steps, &sess));
     std::unique_ptr<ekv_session_s, int (*)(ekv_session_t)> sguard(sess, ekv_session_destroy);
     std::vector<float> ue((size_t)U * h), pre((size_t)std::max(U, 1) * h), st((size_t)steps * h);
     for (size_t i = 0; i < ue.size(); ++i) ue[i] = static_cast<float>(user_embeddings.data[i]);
@@ -464,8 +609,11 @@ LayerMatchReport match_layers(const std::vector<Matrix>& edge_outputs,
     r.cka = Matrix(me, nc);
     r.rsa = Matrix(me, nc);
     std::vector<int> best(me);
-    check(ekv_match_layers(e.data(), me, ce, c.data(), nc, cc, (int)n, cfg.theta_cka, cfg.theta_rsa,
-                           r.cka.data.data(), r.rsa.data.data(), best.data()));
+    {
+        std::lock_guard<std::mutex> g(rt().mu);
+        check(ekv_match_layers(rt().get(), e.data(), me, ce, c.data(), nc, cc, (int)n, cfg.theta_cka,
+                               cfg.theta_rsa, r.cka.data.data(), r.rsa.data.data(), best.data()));
+    }
     r.best.assign(me, std::nullopt);
     for (int le = 0; le < me; ++le)
         if (best[le] >= 0) {
@@ -513,11 +661,14 @@ void set_device(int device) {
 
 void invalidate(const Model& model) {
     std::lock_guard<std::mutex> g(rt().mu);
-    auto it = rt().models.find(&model);
-    if (it != rt().models.end()) {
-        ekv_model_destroy(it->second.handle);
-        rt().models.erase(it);
-    }
+    const uint64_t sig = signature(model);
+    auto& ms = rt().models;
+    for (size_t i = 0; i < ms.size(); ++i)
+        if (ms[i].signature == sig) {
+            ekv_model_destroy(ms[i].handle);
+            ms.erase(ms.begin() + (long)i);
+            return;
+        }
 }
 
 std::vector<QuantizedLayer> compress_cache(const KVCache& cache, const ChannelMask& mask, int bits,
@@ -562,24 +713,115 @@ std::vector<QuantizedLayer> compress_cache(const KVCache& cache, const ChannelMa
 
 LayerKV dequantize(const QuantizedLayer& q, int num_heads) {
     LayerKV kv;
-    const int d = q.head_dim, S = q.positions, ng = d / q.group, rb = d * q.bits / 8;
-    auto code = [&](const std::vector<std::uint8_t>& c, size_t row, int col) {
-        if (q.bits == 8) return (int)(int8_t)c[row * rb + col];
-        const int nib = (c[row * rb + (col >> 1)] >> ((col & 1) * 4)) & 0xF;
-        return nib >= 8 ? nib - 16 : nib;
-    };
+    const int d = q.head_dim, S = q.positions;
+    const size_t rows = (size_t)num_heads * S;
+    if (q.k_codes.size() != rows * d * q.bits / 8 || q.k_scales.size() != rows * (d / q.group))
+        throw std::invalid_argument("dequantize: code / scale sizes do not match the layer shape");
+    std::vector<double> k(rows * d), v(rows * d);
+    if (rows > 0) {
+        std::lock_guard<std::mutex> g(rt().mu);
+        ekv_ctx_t ctx = rt().get();
+        DevBuf dc(q.k_codes.size()), ds(q.k_scales.size() * 4), out(rows * d * 8);
+        for (int which = 0; which < 2; ++which) {
+            dc.put(which ? q.v_codes.data() : q.k_codes.data());
+            ds.put(which ? q.v_scales.data() : q.k_scales.data());
+            check(ekv_kv_dequant_f64(ctx, dc.p, (const float*)ds.p, (int64_t)rows, d, q.bits, q.group,
+                                     (double*)out.p));
+            check(ekv_ctx_synchronize(ctx));
+            out.get(which ? v.data() : k.data(), out.n);
+        }
+    }
     for (int h = 0; h < num_heads; ++h) {
-        Matrix k(S, d), v(S, d);
-        for (int i = 0; i < S; ++i)
-            for (int c = 0; c < d; ++c) {
-                const size_t row = (size_t)h * S + i;
-                k(i, c) = (double)code(q.k_codes, row, c) * (double)q.k_scales[row * ng + c / q.group];
-                v(i, c) = (double)code(q.v_codes, row, c) * (double)q.v_scales[row * ng + c / q.group];
-            }
-        kv.keys.push_back(std::move(k));
-        kv.values.push_back(std::move(v));
+        Matrix km(S, d), vm(S, d);
+        std::copy(k.begin() + (size_t)h * S * d, k.begin() + (size_t)(h + 1) * S * d, km.data.begin());
+        std::copy(v.begin() + (size_t)h * S * d, v.begin() + (size_t)(h + 1) * S * d, vm.data.begin());
+        kv.keys.push_back(std::move(km));
+        kv.values.push_back(std::move(vm));
     }
     return kv;
+}
+
+DeepKV build_deep_kv(const Model& cloud_model, const PrefillResult& cloud_prefill,
+                     const Matrix& ctx_emb_cloud, const std::map<int, int>& match,
+                     const PruneSpec& spec) {
+    spec.validate();
+    const ModelConfig& cc = cloud_model.config;
+    if (spec.head_dim != cc.head_dim)
+        throw std::invalid_argument("select_channels: dim mismatch (spec dim " +
+                                    std::to_string(spec.head_dim) + ", cloud head_dim " +
+                                    std::to_string(cc.head_dim) + ")");
+    const int S = cloud_prefill.cache.size(), H = cc.num_heads, dc = cc.head_dim, hc = cc.hidden_size;
+    if ((int)ctx_emb_cloud.rows != S || (int)ctx_emb_cloud.cols != hc)
+        throw std::invalid_argument("build_deep_kv: context embeddings do not match the cloud prefill");
+    std::set<int> layers;
+    for (const auto& [le, lc] : match) {
+        if (lc < 0 || lc >= cc.num_layers)
+            throw std::invalid_argument("build_deep_kv: matched cloud layer " + std::to_string(lc) +
+                                        " out of range");
+        layers.insert(lc);
+    }
+    DeepKV out;
+    if (match.empty()) return out;
+    const std::vector<int> lcs(layers.begin(), layers.end());
+    const int m = (int)lcs.size();
+    if (spec.retained == dc) {
+        out.mask = ChannelMask::full(dc);
+        out.cut_margin = INFINITY;
+    } else {
+        // X_lc (bf16) = x0 for lc == 0 (sim.cpp:224-234), else the cloud prefill's layer lc-1 output
+        std::vector<uint16_t> xb((size_t)m * S * hc);
+        for (int i = 0; i < m; ++i) {
+            uint16_t* dst = xb.data() + (size_t)i * S * hc;
+            if (lcs[i] == 0) {
+                for (int r = 0; r < S; ++r)
+                    for (int c = 0; c < hc; ++c)
+                        dst[(size_t)r * hc + c] = to_bf16(cloud_model.layers[0].gamma[c] *
+                                                              (ctx_emb_cloud(r, c) + cloud_model.pos_embedding(r, c)) +
+                                                          cloud_model.layers[0].bias[c]);
+            } else {
+                const Matrix& x = cloud_prefill.layer_outputs[lcs[i] - 1];
+                for (size_t j = 0; j < x.data.size(); ++j) dst[j] = to_bf16(x.data[j]);
+            }
+        }
+        std::lock_guard<std::mutex> g(rt().mu);
+        ekv_ctx_t ctx = rt().get();
+        ekv_model_t mh = device_model(cloud_model);
+        void* w0 = nullptr;
+        void* wo = nullptr;
+        check(ekv_model_weights(mh, 0, &w0, &wo));
+        DevBuf dx(xb.size() * 2);
+        dx.put(xb.data());
+        std::vector<std::unique_ptr<DevBuf>> kbuf;
+        std::vector<const void*> kp;
+        for (int lc : lcs) {
+            auto kb = head_major_bf16(cloud_prefill.cache.keys[lc], S, dc);
+            kbuf.push_back(std::make_unique<DevBuf>(kb.size() * 2));
+            kbuf.back()->put(kb.data());
+            kp.push_back(kbuf.back()->p);
+        }
+        ekv_cloud_kv cl{};
+        cl.m = m;
+        cl.S = S;
+        cl.H = H;
+        cl.d_c = dc;
+        cl.x = dx.p;
+        cl.wq = w0;
+        cl.wq_stride = (int64_t)4 * hc * hc;
+        cl.wq_index = lcs.data();
+        cl.k = kp.data();
+        cl.v = kp.data();
+        out.mask.head_dim = dc;
+        out.mask.kept.resize(spec.retained);
+        check(ekv_align_select(ctx, &cl, spec.lambda, out.mask.kept.data(), &out.cut_margin));
+    }
+    const KVCache pruned = prune_cache(cloud_prefill.cache, out.mask);
+    for (const auto& [le, lc] : match) {
+        LayerKV kv;
+        kv.keys = pruned.keys[lc];
+        kv.values = pruned.values[lc];
+        out.deep_kv[le] = std::move(kv);
+    }
+    return out;
 }
 
 }  // namespace b200

@@ -30,6 +30,9 @@ int ekvo_collaborative_decode(int L, int H, int d, int max_pos, const double* wq
                               double* step_out);
 void ekvo_select_channels(const double* q, int64_t q_rows, const double* k, int64_t k_rows, int d,
                           int retained, int* kept, double* score_out);
+void ekvo_prefill_ex(int L, int H, int d, int max_pos, const double* wqkvT, const double* woT,
+                     const double* gamma, const double* bias, const double* pos, const double* emb,
+                     int n, int kv_bf16, double* layer_out, double* k_out, double* v_out);
 }
 
 using namespace edgekv;
@@ -230,6 +233,176 @@ static void test_segment_attention_and_merge() {
     CHECK_THROWS_WITH(merge_attention(a, b), "non-positive or non-finite sigma");
 }
 
+// matrix_test.cpp:21-27: the reference's own triple loop (no FMA at -O2 x86-64)
+static Matrix naive_matmul(const Matrix& a, const Matrix& b) {
+    Matrix out(a.rows, b.cols);
+    for (size_t i = 0; i < a.rows; ++i)
+        for (size_t j = 0; j < b.cols; ++j) {
+            double acc = 0.0;
+            for (size_t k = 0; k < a.cols; ++k) acc += a(i, k) * b(k, j);
+            out(i, j) = acc;
+        }
+    return out;
+}
+
+static void test_project_qkv_bit_exact() {
+    // transformer.cpp:133-152 on the device in fp64: identical bits, any input values
+    Model m = make_model(2, 4, 32, 16, 5);
+    Matrix x(37, 128);
+    ekvo_generate_embeddings(77, 37, 128, x.data.data());  // full fp64, not bf16-representable
+    QkvRows r = project_qkv(m, x, 1, 2);
+    const HeadWeights& w = m.layers[1].heads[2];
+    CHECK(r.q.data == naive_matmul(x, w.wq).data);
+    CHECK(r.k.data == naive_matmul(x, w.wk).data);
+    CHECK(r.v.data == naive_matmul(x, w.wv).data);
+    CHECK_THROWS_WITH(project_qkv(m, x, 2, 0), "layer 2 out of range");
+    CHECK_THROWS_WITH(project_qkv(m, x, 0, 4), "head 4 out of range");
+    CHECK_THROWS_WITH(project_qkv(m, Matrix(3, 5), 0, 0), "expected hidden_size 128");
+}
+
+static void test_segment_attention_fp64_pair() {
+    // the reference's (o, sigma, shift) triple in fp64 (cache_merge.cpp:12-38)
+    const int d = 48, n = 300;
+    Matrix k(n, d), v(n, d);
+    ekvo_generate_embeddings(91, n, d, k.data.data());
+    ekvo_generate_embeddings(92, n, d, v.data.data());
+    Vec q(d);
+    ekvo_generate_embeddings(93, 1, d, q.data());
+    for (double& x : q) x *= 3.0;  // hot logits: the max shift matters
+    SegmentAttention a = segment_attention(q, k, v);
+    std::vector<double> o(d);
+    double sg, sh;
+    ekvo_segment_attention(q.data(), k.data.data(), v.data.data(), n, d, d, o.data(), &sg, &sh);
+    CHECK(a.shift == sh);  // the max logit: bit-identical
+    CHECK(std::abs(a.sigma - sg) <= 1e-13 * sg);
+    CHECK(normwise(a.o, o) <= 1e-13);
+}
+
+static void test_select_channels_fp64_inputs() {
+    // full-precision Q/K (not bf16-representable) with a small but clear cut: the
+    // fp64 device norms give the reference's mask
+    const int d = 32, rows = 400;
+    Matrix q(rows, d), k(rows, d);
+    ekvo_generate_embeddings(101, rows, d, q.data.data());
+    ekvo_generate_embeddings(102, rows, d, k.data.data());
+    for (int i = 0; i < rows; ++i)
+        for (int c = 0; c < d; ++c) q(i, c) *= 1.0 + 1e-4 * c;  // ~1e-4 score steps
+    const PruneSpec spec = PruneSpec::from_lambda(0.5, d);
+    std::vector<int> want(spec.retained);
+    ekvo_select_channels(q.data.data(), rows, k.data.data(), rows, d, spec.retained, want.data(), nullptr);
+    CHECK(select_channels(q, k, spec).kept == want);
+}
+
+static void test_prefill_and_forward_rows() {
+    // forward_rows / prefill on the device vs the oracle (KV rows stored as bf16)
+    const int L = 3, H = 8, d = 32, h = H * d, n = 12, mp = 64;
+    Model m = make_model(L, H, d, mp, 31);
+    for (int c = 0; c < h; ++c) {
+        m.layers[0].gamma[c] = 1.0 + 0.01 * (c % 7);
+        m.layers[0].bias[c] = 0.02 * ((c % 5) - 2);
+    }
+    Matrix emb(n, h);
+    ekvo_generate_embeddings(33, n, h, emb.data.data());
+    for (double& x : emb.data) x = (double)(float)x;
+    FlopCounts fc;
+    PrefillResult pr = prefill(m, emb, &fc);
+    CHECK((int)pr.layer_outputs.size() == L && pr.cache.size() == n);
+    CHECK((int)pr.cache.keys[2][3].rows == n);
+    std::vector<double> w, wo, g, b, lo((size_t)L * n * h), ko((size_t)L * H * n * d), vo(ko.size());
+    b200_layout(m, w, wo, g, b);
+    ekvo_prefill_ex(L, H, d, mp, w.data(), wo.data(), g.data(), b.data(), m.pos_embedding.data.data(),
+                    emb.data.data(), n, 1, lo.data(), ko.data(), vo.data());
+    double worst = 0;
+    for (int l = 0; l < L; ++l)
+        for (int i = 0; i < n; ++i)
+            worst = std::max(worst, normwise(pr.layer_outputs[l].row(i), lo, ((size_t)l * n + i) * h));
+    std::printf("  prefill normwise error vs oracle: %.3e\n", worst);
+    CHECK(worst <= 1e-3);
+    // flop counts: the reference's closed form (transformer_test.cpp:251-281)
+    CHECK(fc.proj == 3ll * n * h + (int64_t)L * n * H * 3 * d * (2ll * h - 1));
+    CHECK(fc.out_proj == (int64_t)L * n * h * (2ll * h - 1));
+    // incremental == monolithic: 8 rows, then 4 more on top of the cache
+    Matrix a(8, h), c(4, h);
+    std::copy(emb.data.begin(), emb.data.begin() + 8 * h, a.data.begin());
+    std::copy(emb.data.begin() + 8 * h, emb.data.end(), c.data.begin());
+    PrefillResult inc = prefill(m, a);
+    std::vector<Matrix> more = forward_rows(m, inc.cache, c, PositionKind::user, nullptr);
+    CHECK(inc.cache.size() == n && inc.cache.positions.back().kind == PositionKind::user);
+    double dev = 0;
+    for (int l = 0; l < L; ++l)
+        for (int i = 0; i < 4; ++i)
+            dev = std::max(dev, normwise(more[l].row(i), pr.layer_outputs[l].data, (size_t)(8 + i) * h));
+    std::printf("  incremental vs monolithic prefill: %.3e\n", dev);
+    CHECK(dev <= 1e-4);
+    Vec last = decode_step(m, inc.cache, emb.row(0));
+    CHECK((int)last.size() == h && inc.cache.size() == n + 1);
+    CHECK_THROWS_WITH(decode_step(m, inc.cache, Vec(3)), "embedding size 3");
+    KVCache wrong = KVCache::empty_for(L, H, d + 1);
+    CHECK_THROWS_WITH(forward_rows(m, wrong, emb, PositionKind::context, nullptr), "cache shape");
+    Matrix big(mp + 1, h);
+    CHECK_THROWS_WITH(prefill(m, big), "position overflow");
+}
+
+static void test_build_deep_kv_on_tensor_cores() {
+    // Artifacts::build_deep_kv (sim.cpp:217-265) with K1: the mask equals the
+    // reference rule on the (bf16) inputs the tensor cores consumed; deep_kv is the
+    // exact pruned cloud KV
+    const int L = 4, H = 4, d = 64, h = H * d, S = 128, mp = 160;
+    Model cloud = make_model(L, H, d, mp, 41);
+    for (int l = 0; l < L; ++l)  // heterogeneous channel importance: a decidable cut
+        for (int hd = 0; hd < H; ++hd)
+            for (int r = 0; r < h; ++r)
+                for (int c = 0; c < d; ++c) cloud.layers[l].heads[hd].wq(r, c) *= std::exp(0.03 * ((c * 37) % d) - 1.0);
+    Matrix emb(S, h);
+    ekvo_generate_embeddings(43, S, h, emb.data.data());
+    PrefillResult pre = prefill(cloud, emb);
+    const std::map<int, int> match = {{2, 0}, {3, 3}};
+    const PruneSpec spec = PruneSpec::from_lambda(0.5, d);
+    b200::DeepKV dk = b200::build_deep_kv(cloud, pre, emb, match, spec);
+    CHECK((int)dk.mask.kept.size() == spec.retained && dk.cut_margin > 1e-6);
+    // the reference rule on the same bf16-rounded X, W_Q and K
+    auto r16 = [](double x) {
+        float f = (float)x;
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        u += 0x7FFFu + ((u >> 16) & 1u);
+        u &= 0xFFFF0000u;
+        std::memcpy(&f, &u, 4);
+        return (double)f;
+    };
+    std::vector<double> qs, ks;
+    for (int lc : {0, 3}) {
+        Matrix x(S, h);
+        for (int r = 0; r < S; ++r)
+            for (int c = 0; c < h; ++c)
+                x(r, c) = r16(lc == 0 ? cloud.layers[0].gamma[c] * (emb(r, c) + cloud.pos_embedding(r, c)) +
+                                            cloud.layers[0].bias[c]
+                                      : pre.layer_outputs[lc - 1](r, c));
+        for (int hd = 0; hd < H; ++hd) {
+            Matrix wq = cloud.layers[lc].heads[hd].wq;
+            for (double& v : wq.data) v = r16(v);
+            Matrix q = naive_matmul(x, wq);
+            qs.insert(qs.end(), q.data.begin(), q.data.end());
+            for (double v : pre.cache.keys[lc][hd].data) ks.push_back(r16(v));
+        }
+    }
+    std::vector<int> want(spec.retained);
+    ekvo_select_channels(qs.data(), (int64_t)qs.size() / d, ks.data(), (int64_t)ks.size() / d, d,
+                         spec.retained, want.data(), nullptr);
+    CHECK(dk.mask.kept == want);
+    bool exact = dk.deep_kv.size() == 2;
+    for (const auto& [le, lc] : match)
+        for (int hd = 0; hd < H; ++hd)
+            for (int r = 0; r < S; ++r)
+                for (int j = 0; j < spec.retained; ++j) {
+                    exact &= dk.deep_kv.at(le).keys[hd](r, j) == pre.cache.keys[lc][hd](r, want[j]);
+                    exact &= dk.deep_kv.at(le).values[hd](r, j) == pre.cache.values[lc][hd](r, want[j]);
+                }
+    CHECK(exact);
+    b200::DeepKV full = b200::build_deep_kv(cloud, pre, emb, match, PruneSpec::from_lambda(0.0, d));
+    CHECK((int)full.mask.kept.size() == d);
+}
+
 static void test_assemble_context_errors() {
     // cache_merge_test.cpp:224-271
     auto lkv = [](int S, int d) {
@@ -363,6 +536,11 @@ int main() {
         {"collaborative_decode vs oracle", test_collaborative_decode_matches_oracle},
         {"compress round trip", test_compress_round_trip},
         {"layer match + scheduler", test_layer_match_and_scheduler},
+        {"project_qkv bit-exact", test_project_qkv_bit_exact},
+        {"segment_attention fp64 (o, sigma, shift)", test_segment_attention_fp64_pair},
+        {"select_channels fp64 inputs", test_select_channels_fp64_inputs},
+        {"prefill / forward_rows / decode_step", test_prefill_and_forward_rows},
+        {"b200::build_deep_kv (K1)", test_build_deep_kv_on_tensor_cores},
     };
     for (auto& [name, fn] : tests) {
         const int before = g_fail;

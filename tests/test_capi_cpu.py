@@ -85,20 +85,6 @@ def test_abi_version_and_host_entry_points(lib, oracle):
         ek.pipeline_schedule([-1], [0])
 
 
-def test_host_match_layers_equals_oracle(lib, oracle):
-    from paper_2505_14085_b200 import edgekv as ek
-    from oracle import model_from_reference_layout
-    e = model_from_reference_layout(oracle.init_model(3, 2, 6, 64, 41), 3, 2, 6, 64)
-    c = model_from_reference_layout(oracle.init_model(5, 4, 6, 64, 43), 5, 4, 6, 64)
-    eo = oracle.prefill(e, oracle.generate_embeddings(9, 16, 12))[0]
-    co = oracle.prefill(c, oracle.generate_embeddings(9, 16, 24))[0]
-    a = ek.match_layers(eo, co, 0.5, 0.3)
-    b = oracle.match_layers(eo, co, 0.5, 0.3)
-    assert np.array_equal(a[2], b[2])
-    assert np.allclose(a[0], b[0], rtol=1e-12, atol=1e-14)
-    assert np.allclose(a[1], b[1], rtol=1e-12, atol=1e-14)
-
-
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
 def test_compute_entry_points_refuse_without_b200(lib):
     h = C.c_void_p()

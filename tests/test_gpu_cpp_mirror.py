@@ -30,7 +30,9 @@ def test_mirror_builds_and_links(tmp_path):
                          text=True, check=True).stdout
     for sym in ["edgekv::select_channels", "edgekv::prune_cache", "edgekv::segment_attention",
                 "edgekv::merge_attention", "edgekv::assemble_context", "edgekv::collaborative_decode",
-                "edgekv::match_layers", "edgekv::cache_source", "edgekv::pipeline_schedule"]:
+                "edgekv::match_layers", "edgekv::cache_source", "edgekv::pipeline_schedule",
+                "edgekv::project_qkv", "edgekv::forward_rows", "edgekv::prefill", "edgekv::decode_step",
+                "edgekv::b200::build_deep_kv"]:
         assert sym in out, sym
     assert os.path.exists(exe)
 

@@ -197,7 +197,7 @@ def run_full_ce_lslm_path(ek, ctx, oracle, Lc=8, Le=4, deep=2, bits=8):
     pseed = oracle.mix(42, 0x9B0BE)
     eo = oracle.prefill(ef, oracle.generate_embeddings(pseed, 64, he))[0]
     co = oracle.prefill(cf, oracle.generate_embeddings(pseed, 64, hc))[0]
-    cka, rsa, best = ek.match_layers(eo, co, 0.0, -1.0)
+    cka, rsa, best = ek.match_layers(ctx, eo, co, 0.0, -1.0)
     assert np.array_equal(best, oracle.match_layers(eo, co, 0.0, -1.0)[2])
     boundary = Le - deep
     deep_match = {le: int(best[le]) for le in range(boundary, Le)}
@@ -238,7 +238,8 @@ def run_full_ce_lslm_path(ek, ctx, oracle, Lc=8, Le=4, deep=2, bits=8):
         kb = f32_to_bf16_bits(e_k[l].astype(np.float32)); vb = f32_to_bf16_bits(e_v[l].astype(np.float32))
         kvc.upload_bf16(l, kb, vb)
         ck[l] = bf16_to_f64(kb); cv[l] = bf16_to_f64(vb)
-    ek.build_deep_kv(ctx, kvc, deep_match, Xd, Wd, Kd, Vd, 0.5, lcs)
+    got_kept, got_margin = ek.build_deep_kv(ctx, kvc, deep_match, Xd, Wd, Kd, Vd, 0.5, lcs)
+    assert got_kept.tolist() == want_kept.tolist() and got_margin > 1e-6
     for le, lc in deep_match.items():
         i = lcs.index(lc)
         for src, dst in ((Kd, ck), (Vd, cv)):
