@@ -91,6 +91,13 @@ int ekv_fill_uniform_bf16(ekv_ctx_t ctx, void* dst_dev, int64_t n, uint64_t seed
 /* Stage 1: layer-alignment map and projection into edge head geometry */
 /* ------------------------------------------------------------------ */
 
+/* generate_embeddings (transformer.cpp:308-317; Rng rng.hpp:13-45), host: row i
+ * is drawn from mt19937_64(Rng::mix(seed, i)), value = -1 + 2*((u >> 11) * 2^-53),
+ * so row i at width h is a prefix of row i at any larger width.  out host fp64
+ * [n][h].  The reference's probe / context / user inputs (sim.cpp:101-104,
+ * 130-132, 163). */
+int ekv_generate_embeddings(uint64_t seed, int n, int h, double* out);
+
 /* PruneSpec::from_lambda (head_prune.cpp:14-22): retained = floor((1-l)*d + 1e-9). */
 int ekv_prune_retained(double lambda, int head_dim, int* retained);
 
@@ -494,17 +501,22 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb_host, in
 /* The compressed cloud layers as one self-describing, checksummed byte
  * stream: what crosses the cloud -> edge link (the transfer the reference
  * simulates in Sim::submit_transfer, sim.cpp:417-449, sized by
- * deep_layer_bytes, sim.cpp:714) or is kept as the historical cache.
+ * deep_layer_bytes, sim.cpp:714) or is kept as the historical cache
+ * (sim.cpp:885-895).
  * Layout (little-endian):
- *   header 64 B: magic "EKVPACK1", u32 version (1), n_layers, H, S, d_e,
+ *   header 64 B: magic "EKVPACK1", u32 version (2), n_layers, H, S, d_e,
  *     d_c, bits, group, header_bytes, 3 x u32 reserved, u64 header_fnv
  *   i32 edge_layer[n], i32 cloud_layer[n] (the layer map), i32 kept[d_e]
  *   (the channel mask), u64 layer_fnv[n], zero padding to header_bytes
  *   (a multiple of 256)
  *   per layer: K codes [H][S][d_e*bits/8], V codes, K scales fp32
  *   [H][S][d_e/group], V scales
- * Checksums are FNV-1a 64 (the reference's fnv1a64, rng.cpp:7-15): the
- * header (with header_fnv = 0) and each layer's payload. */
+ * Checksums are FNV-1a 64 (the reference's fnv1a64, rng.cpp:7-15): the header
+ * (with header_fnv = 0) over its bytes; a layer (version 2) over the u64 FNV-1a
+ * 64s, little-endian, of its four arrays cut into 16 KiB chunks in payload order
+ * (the last chunk of an array may be shorter) -- independent chunks, so the
+ * device hashes a layer where its bytes are.  Version 1 (FNV-1a over the whole
+ * layer payload) is still read. */
 typedef struct {
     int n_layers, H, S, d_e, d_c, bits, group;
     size_t bytes;
@@ -522,8 +534,19 @@ int ekv_kvpack_export(ekv_kvctx_t c, const int* layers, const int* cloud_layers,
 int ekv_kvpack_parse(const void* host_src, size_t bytes, ekv_kvpack_info* info, int* layers,
                      int* cloud_layers, int* kept);
 /* Validate and copy the pack's layers into the context's storage (formats,
- * H, S and d_e must match: "kvpack: dim mismatch"). */
+ * H, S and d_e must match: "kvpack: dim mismatch").  Version 2: the payload is
+ * copied to an HBM staging buffer and hashed there; the context is written only
+ * after every layer checksum matched. */
 int ekv_kvpack_import(ekv_kvctx_t c, const void* host_src, size_t bytes);
+/* Eq. 20 over the wire format: the pack's layers are uploaded one by one (copy
+ * stream) into the session's context while the n rows are forwarded layer-major on
+ * the compute stream -- layer l's attention waits only for layer l's upload
+ * (cost_model.cpp:73-100, sim.cpp:802-814, 909-933).  Every layer is hashed on the
+ * device after its upload and checked at the end: on "checksum mismatch" the
+ * outputs and the context's imported layers are invalid.  Version-2 packs.
+ * Synchronises. */
+int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
+                             const void* host_src, size_t bytes);
 
 /* ------------------------------------------------------------------ */
 /* Scheduler interface (cost_model.hpp:53-84)                          */

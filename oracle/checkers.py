@@ -354,6 +354,9 @@ class Reference:
         L.ref_bench_setup.argtypes = [C.c_int] * 6 + [C.c_uint64]
         L.ref_bench_run.argtypes = [C.c_void_p] + [C.c_int] * 4 + [_dp, C.POINTER(C.c_int64)]
         L.ref_bench_free.argtypes = [C.c_void_p]
+        L.ref_full_path.argtypes = ([C.c_int] * 7 + [_dp] * 10 + [C.c_uint64, C.c_int, C.c_double,
+                                    C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                    _dp, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp])
 
     def _chk(self, rc):
         if rc < 0:
@@ -491,6 +494,25 @@ class Reference:
 
     def bench_free(self, handle):
         self.lib.ref_bench_free(handle)
+
+    def full_path(self, edge, cloud, seed, n_probe, theta_cka, theta_rsa, S, deep, lam, U, steps):
+        """The reference's whole value path for one request (Artifacts order, sim.cpp:100-265):
+        edge / cloud = dict(L,H,d,max_pos,wqkvT,woT,gamma,bias,pos) in the B200 layout (fp64).
+        Returns (stage seconds [8], kept, deep_map, step_outputs [steps][h_e])."""
+        assert edge["max_pos"] == cloud["max_pos"]
+        times = np.zeros(8)
+        kept = np.zeros(cloud["d"], np.int32)
+        dm = np.zeros(max(deep, 1), np.int32)
+        out = np.zeros((steps, edge["H"] * edge["d"]))
+        f = lambda m, k: _d(_f64(m[k]))
+        keep = [_f64(m[k]) for m in (edge, cloud) for k in ("wqkvT", "woT", "gamma", "bias", "pos")]
+        args = [edge["L"], edge["H"], edge["d"], cloud["L"], cloud["H"], cloud["d"], edge["max_pos"]]
+        args += [_d(a) for a in keep]
+        self._chk(self.lib.ref_full_path(*args, seed, n_probe, theta_cka, theta_rsa, S, deep, lam, U,
+                                         steps, _d(times), kept.ctypes.data_as(C.POINTER(C.c_int)),
+                                         dm.ctypes.data_as(C.POINTER(C.c_int)), _d(out)))
+        del f
+        return times, kept, dm[:deep], out
 
 
 def model_from_reference_layout(ref_model: dict, L: int, H: int, d: int, max_pos: int) -> dict:

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <exception>
 #include <map>
+#include <set>
 #include <string>
 #include <thread>
 #include <vector>
@@ -429,5 +430,120 @@ int ref_bench_run(void* handle, int U, int steps, int threads, int calls, double
 }
 
 void ref_bench_free(void* handle) { delete static_cast<RefBench*>(handle); }
+
+// The reference's whole CE-LSLM value path for one request, composed from its
+// public API in the order of Artifacts (sim.cpp:100-265): probe prefill of both
+// models -> match_layers -> deep map; context prefill of both models;
+// build_deep_kv (x0, project_qkv of every distinct matched cloud layer and head,
+// select_channels, prune_cache); assembled_context; collaborative_decode of the
+// user prompt.  Models in the B200 layout (populated directly).
+// times[8] (seconds): probe prefill, match, edge ctx prefill, cloud ctx prefill,
+// Q/K restack (project_qkv), select_channels, prune + assemble, decode.
+// kept_out[retained], deep_map_out[deep], step_out[steps][h_e] (may be null).
+int ref_full_path(int Le, int He, int de, int Lc, int Hc, int dc, int max_pos, const double* e_wqkvT,
+                  const double* e_woT, const double* e_gamma, const double* e_bias, const double* e_pos,
+                  const double* c_wqkvT, const double* c_woT, const double* c_gamma, const double* c_bias,
+                  const double* c_pos, uint64_t seed, int n_probe, double theta_cka, double theta_rsa,
+                  int S, int deep, double lambda, int U, int steps, double* times, int* kept_out,
+                  int* deep_map_out, double* step_out) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto sec = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double>(b - a).count();
+        };
+        const Model edge = make_model(Le, He, de, max_pos, e_wqkvT, e_woT, e_gamma, e_bias, e_pos);
+        const Model cloud = make_model(Lc, Hc, dc, max_pos, c_wqkvT, c_woT, c_gamma, c_bias, c_pos);
+        const int he = He * de, hc = Hc * dc;
+        auto t0 = clk::now();
+        Matrix pe = generate_embeddings(Rng::mix(seed, 0x9B0BE), n_probe, he);
+        Matrix pc = generate_embeddings(Rng::mix(seed, 0x9B0BE), n_probe, hc);
+        std::vector<Matrix> eo = prefill(edge, pe).layer_outputs;
+        std::vector<Matrix> co = prefill(cloud, pc).layer_outputs;
+        auto t1 = clk::now();
+        SimilarityConfig cfg;
+        cfg.theta_cka = theta_cka;
+        cfg.theta_rsa = theta_rsa;
+        cfg.num_probe_samples = n_probe;
+        LayerMatchReport rep = match_layers(eo, co, cfg);
+        const int boundary = Le - deep;
+        std::map<int, int> match;
+        for (int l = boundary; l < Le; ++l) {
+            if (!rep.best[l].has_value())
+                throw std::invalid_argument("ce_lslm: edge layer " + std::to_string(l) +
+                                            " has no matched cloud layer under the configured thresholds");
+            match[l] = rep.best[l].value();
+            if (deep_map_out) deep_map_out[l - boundary] = match[l];
+        }
+        auto t2 = clk::now();
+        const std::uint64_t eseed = Rng::mix(seed, 0xC7E20000ull);
+        Matrix emb_e = generate_embeddings(eseed, S, he);
+        Matrix emb_c = generate_embeddings(eseed, S, hc);
+        PrefillResult epf = prefill(edge, emb_e);
+        auto t3 = clk::now();
+        PrefillResult cpf = prefill(cloud, emb_c);
+        auto t4 = clk::now();
+        std::set<int> cls;
+        for (const auto& [le, lc] : match) cls.insert(lc);
+        Matrix x0((std::size_t)S, (std::size_t)hc);
+        for (int i = 0; i < S; ++i)
+            for (int c = 0; c < hc; ++c)
+                x0(i, c) = cloud.layers[0].gamma[c] * (emb_c(i, c) + cloud.pos_embedding(i, c)) +
+                           cloud.layers[0].bias[c];
+        const std::size_t blocks = cls.size() * (std::size_t)Hc;
+        Matrix q_stack(blocks * S, dc), k_stack(blocks * S, dc);
+        std::size_t block = 0;
+        for (int lc : cls) {
+            const Matrix& input = lc == 0 ? x0 : cpf.layer_outputs[lc - 1];
+            for (int h = 0; h < Hc; ++h) {
+                QkvRows qkv = project_qkv(cloud, input, lc, h);
+                for (int i = 0; i < S; ++i)
+                    for (int c = 0; c < dc; ++c) {
+                        q_stack(block * S + i, c) = qkv.q(i, c);
+                        k_stack(block * S + i, c) = qkv.k(i, c);
+                    }
+                ++block;
+            }
+        }
+        auto t5 = clk::now();
+        const PruneSpec spec = PruneSpec::from_lambda(lambda, dc);
+        const ChannelMask mask =
+            spec.retained == dc ? ChannelMask::full(dc) : select_channels(q_stack, k_stack, spec);
+        if (kept_out) std::copy(mask.kept.begin(), mask.kept.end(), kept_out);
+        auto t6 = clk::now();
+        const KVCache pruned = prune_cache(cpf.cache, mask);
+        std::map<int, LayerKV> local, shared;
+        std::map<int, CacheOrigin> origins;
+        for (int l = 0; l < boundary; ++l) {
+            LayerKV kv;
+            kv.keys = epf.cache.keys[l];
+            kv.values = epf.cache.values[l];
+            local[l] = std::move(kv);
+        }
+        for (const auto& [le, lc] : match) {
+            LayerKV kv;
+            kv.keys = pruned.keys[lc];
+            kv.values = pruned.values[lc];
+            shared[le] = std::move(kv);
+            origins[le] = CacheOrigin::cloud;
+        }
+        AssembledContext ctx = assemble_context(shared, local, origins, Le);
+        auto t7 = clk::now();
+        Matrix user = generate_embeddings(Rng::mix(seed, 0x55E20000ull), U, he);
+        CollaborativeResult r = collaborative_decode(edge, ctx, user, steps);
+        auto t8 = clk::now();
+        if (step_out)
+            for (int t = 0; t < steps; ++t) std::copy(r.step_outputs[t].begin(), r.step_outputs[t].end(),
+                                                      step_out + (std::size_t)t * he);
+        times[0] = sec(t0, t1);  // probe prefill
+        times[1] = sec(t1, t2);  // match_layers
+        times[2] = sec(t2, t3);  // edge context prefill
+        times[3] = sec(t3, t4);  // cloud context prefill
+        times[4] = sec(t4, t5);  // Q/K restack (project_qkv)
+        times[5] = sec(t5, t6);  // select_channels
+        times[6] = sec(t6, t7);  // prune + assemble
+        times[7] = sec(t7, t8);  // collaborative_decode
+        return 0;
+    });
+}
 
 }  // extern "C"

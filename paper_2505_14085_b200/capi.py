@@ -65,6 +65,7 @@ PROTOS = {
     "ekv_copy": [_vp, _vp, _vp, C.c_size_t, _i],
     "ekv_fill_uniform_bf16": [_vp, _vp, _i64, _u64, _u64, _d, _d],
     "ekv_prune_retained": [_d, _i, _ip],
+    "ekv_generate_embeddings": [_u64, _i, _i, _dp],
     "ekv_align_qnorm": [_vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "ekv_kv_colnorm": [_vp, _vp, _i64, _i, _vp],
     "ekv_rank_channels": [_dp, _dp, _i, _i, _ip, _dp],
@@ -119,6 +120,7 @@ PROTOS = {
     "ekv_kvpack_export": [_vp, _ip, _ip, _i, _ip, _i, _vp, C.c_size_t],
     "ekv_kvpack_parse": [_vp, C.c_size_t, C.POINTER(ekv_kvpack_info), _ip, _ip, _ip],
     "ekv_kvpack_import": [_vp, _vp, C.c_size_t],
+    "ekv_session_forward_pack": [_vp, _vp, _i, _vp, _vp, C.c_size_t],
     "ekv_batch_destroy": [_vp],
     "ekv_batch_reset": [_vp],
     "ekv_batch_info": [_vp, _ip, _ip, _ip],

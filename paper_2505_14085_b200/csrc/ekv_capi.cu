@@ -11,6 +11,7 @@
 #include <numeric>
 #include <tuple>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ekv_common.cuh"
@@ -1849,7 +1850,9 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb, int U, 
 
 
 // ---------------------------------------------------------------- Eq. 20 pipelined prefill
-namespace {
+}  // extern "C"
+
+namespace ekv {
 // Layer-major forward of n user rows where layer l's attention waits on ready[l] (null =
 // the layer is resident), then the decode state is advanced past the rows.  Shared by the
 // host-upload (Eq. 20 over pinned host memory) and the event-driven (NCCL receive) entry
@@ -1900,7 +1903,9 @@ void streamed_forward(ekv_session_s* s, const float* emb_dev, int n, float* out_
     }
     cleanup();
 }
-}  // namespace
+}  // namespace ekv
+
+extern "C" {
 
 int ekv_session_forward_pipelined(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
                                   const ekv_layer_upload* uploads, int overlap, float* t_comm_ms,
@@ -1978,210 +1983,6 @@ int ekv_session_forward_streamed(ekv_session_t s, const float* emb_dev, int n, f
         if (layer_ready)
             for (int l = 0; l < m->cfg.num_layers; ++l) ready[l] = (cudaEvent_t)layer_ready[l];
         streamed_forward(s, emb_dev, n, out_dev, ready.data(), nullptr, nullptr, nullptr);
-    });
-}
-
-// ---------------------------------------------------------------- packed-KV wire format
-namespace {
-constexpr char kPackMagic[8] = {'E', 'K', 'V', 'P', 'A', 'C', 'K', '1'};
-struct PackHeader {  // 64 bytes, little-endian
-    char magic[8];
-    uint32_t version, n_layers, H, S, d_e, d_c, bits, group, header_bytes, reserved[3];
-    uint64_t header_fnv;  // fnv1a64 of [0, header_bytes) with this field zero
-};
-static_assert(sizeof(PackHeader) == 64, "pack header layout");
-
-uint64_t fnv1a(const void* data, size_t len, uint64_t h = 14695981039346656037ull) {
-    const unsigned char* p = (const unsigned char*)data;
-    for (size_t i = 0; i < len; ++i) {
-        h ^= p[i];
-        h *= 1099511628211ull;
-    }
-    return h;
-}
-size_t pack_row_bytes(int d_e, int bits) { return (size_t)d_e * bits / 8; }
-size_t pack_layer_bytes(int H, int S, int d_e, int bits, int group) {
-    const size_t rows = (size_t)H * S;
-    return 2 * rows * pack_row_bytes(d_e, bits) + 2 * rows * (size_t)(d_e / group) * 4;
-}
-size_t pack_header_bytes(int n, int d_e) {
-    const size_t b = sizeof(PackHeader) + (size_t)n * 4 * 2 + (size_t)d_e * 4 + (size_t)n * 8;
-    return (b + 255) / 256 * 256;
-}
-void pack_check_shape(int n, int H, int S, int d_e, int bits, int group) {
-    require(n >= 1, "kvpack: no layers");
-    require(H >= 1 && S >= 1 && d_e >= 1, "kvpack: empty shape");
-    require(bits == 8 || bits == 4, "kvpack: bits must be 8 or 4");
-    require(group >= 1 && d_e % group == 0, "kvpack: group must divide d_e");
-    require(d_e * bits % 8 == 0, "kvpack: d_e * bits must be whole bytes");
-}
-// validated view of a pack in host memory
-struct PackView {
-    const PackHeader* hd;
-    const int32_t* edge;
-    const int32_t* cloud;
-    const int32_t* kept;
-    const uint64_t* lfnv;
-    const unsigned char* payload;
-    size_t layer_bytes;
-};
-PackView pack_view(const void* src, size_t bytes) {
-    require(src != nullptr, "kvpack: null buffer");
-    require(bytes >= sizeof(PackHeader), "kvpack: truncated header");
-    PackView v{};
-    v.hd = (const PackHeader*)src;
-    require(std::memcmp(v.hd->magic, kPackMagic, 8) == 0, "kvpack: bad magic");
-    require(v.hd->version == 1, "kvpack: unsupported version " + std::to_string(v.hd->version));
-    const int n = (int)v.hd->n_layers, H = (int)v.hd->H, S = (int)v.hd->S, de = (int)v.hd->d_e;
-    pack_check_shape(n, H, S, de, (int)v.hd->bits, (int)v.hd->group);
-    require(v.hd->header_bytes == pack_header_bytes(n, de), "kvpack: header size mismatch");
-    require(bytes >= v.hd->header_bytes, "kvpack: truncated header");
-    {
-        std::vector<unsigned char> tmp((const unsigned char*)src, (const unsigned char*)src + v.hd->header_bytes);
-        reinterpret_cast<PackHeader*>(tmp.data())->header_fnv = 0;
-        require(fnv1a(tmp.data(), tmp.size()) == v.hd->header_fnv, "kvpack: header checksum mismatch");
-    }
-    const unsigned char* b = (const unsigned char*)src + sizeof(PackHeader);
-    v.edge = (const int32_t*)b;
-    v.cloud = v.edge + n;
-    v.kept = v.cloud + n;
-    v.lfnv = (const uint64_t*)(v.kept + de);
-    v.payload = (const unsigned char*)src + v.hd->header_bytes;
-    v.layer_bytes = pack_layer_bytes(H, S, de, (int)v.hd->bits, (int)v.hd->group);
-    require(bytes >= v.hd->header_bytes + (size_t)n * v.layer_bytes, "kvpack: truncated payload");
-    for (int i = 0; i < n; ++i)
-        require(fnv1a(v.payload + (size_t)i * v.layer_bytes, v.layer_bytes) == v.lfnv[i],
-                "kvpack: checksum mismatch in layer " + std::to_string(v.edge[i]));
-    return v;
-}
-}  // namespace
-
-int ekv_fnv1a64(const void* data, size_t len, uint64_t seed, uint64_t* out) {
-    return guard([&] {
-        require(out && (data || len == 0), "ekv_fnv1a64: null argument");
-        *out = fnv1a(data, len, seed);
-    });
-}
-
-int ekv_kvpack_size(int n_layers, int H, int S, int d_e, int bits, int group, size_t* bytes) {
-    return guard([&] {
-        require(bytes != nullptr, "ekv_kvpack_size: null argument");
-        pack_check_shape(n_layers, H, S, d_e, bits, group);
-        *bytes = pack_header_bytes(n_layers, d_e) + (size_t)n_layers * pack_layer_bytes(H, S, d_e, bits, group);
-    });
-}
-
-int ekv_kvpack_export(ekv_kvctx_t c, const int* layers, const int* cloud_layers, int n, const int* kept, int d_c,
-                      void* dst, size_t capacity) {
-    return guard([&] {
-        require(c && layers && cloud_layers && kept && dst, "ekv_kvpack_export: null argument");
-        require(n >= 1, "kvpack: no layers");
-        const ekv_segment& s0 = c->seg.at(layers[0]);
-        const int H = c->model->cfg.num_heads, S = c->S, de = d_of(c->model);
-        const int bits = s0.format, group = s0.group;
-        require(bits == EKV_KV_INT8 || bits == EKV_KV_INT4, "kvpack: layer " + std::to_string(layers[0]) +
-                                                                " is not a compressed layer");
-        pack_check_shape(n, H, S, de, bits, group);
-        for (int i = 0; i < n; ++i) {
-            require(layers[i] >= 0 && layers[i] < (int)c->seg.size(), "missing layer " + std::to_string(layers[i]));
-            const ekv_segment& sg = c->seg[layers[i]];
-            require(sg.format == bits && sg.group == group,
-                    "kvpack: layer " + std::to_string(layers[i]) + " format differs from layer " +
-                        std::to_string(layers[0]));
-        }
-        const size_t hb = pack_header_bytes(n, de), lb = pack_layer_bytes(H, S, de, bits, group);
-        require(capacity >= hb + (size_t)n * lb, "kvpack: destination too small");
-        set_dev(c->model->ctx);
-        cudaStream_t st = c->model->ctx->stream;
-        unsigned char* out = (unsigned char*)dst;
-        std::memset(out, 0, hb);
-        PackHeader* hd = (PackHeader*)out;
-        std::memcpy(hd->magic, kPackMagic, 8);
-        hd->version = 1;
-        hd->n_layers = n;
-        hd->H = H;
-        hd->S = S;
-        hd->d_e = de;
-        hd->d_c = d_c;
-        hd->bits = bits;
-        hd->group = group;
-        hd->header_bytes = (uint32_t)hb;
-        int32_t* edge = (int32_t*)(out + sizeof(PackHeader));
-        int32_t* cloud = edge + n;
-        int32_t* kp = cloud + n;
-        uint64_t* lfnv = (uint64_t*)(kp + de);
-        const size_t rows = (size_t)H * S, cb = rows * pack_row_bytes(de, bits), sb = rows * (de / group) * 4;
-        for (int i = 0; i < n; ++i) {
-            edge[i] = layers[i];
-            cloud[i] = cloud_layers[i];
-            const ekv_segment& sg = c->seg[layers[i]];
-            unsigned char* p = out + hb + (size_t)i * lb;
-            EKV_CUDA(cudaMemcpyAsync(p, sg.k, cb, cudaMemcpyDeviceToHost, st));
-            EKV_CUDA(cudaMemcpyAsync(p + cb, sg.v, cb, cudaMemcpyDeviceToHost, st));
-            EKV_CUDA(cudaMemcpyAsync(p + 2 * cb, sg.k_scales, sb, cudaMemcpyDeviceToHost, st));
-            EKV_CUDA(cudaMemcpyAsync(p + 2 * cb + sb, sg.v_scales, sb, cudaMemcpyDeviceToHost, st));
-        }
-        for (int j = 0; j < de; ++j) kp[j] = kept[j];
-        EKV_CUDA(cudaStreamSynchronize(st));
-        for (int i = 0; i < n; ++i) lfnv[i] = fnv1a(out + hb + (size_t)i * lb, lb);
-        hd->header_fnv = 0;
-        hd->header_fnv = fnv1a(out, hb);
-    });
-}
-
-int ekv_kvpack_parse(const void* src, size_t bytes, ekv_kvpack_info* info, int* layers, int* cloud_layers,
-                     int* kept) {
-    return guard([&] {
-        const PackView v = pack_view(src, bytes);
-        if (info) {
-            info->n_layers = (int)v.hd->n_layers;
-            info->H = (int)v.hd->H;
-            info->S = (int)v.hd->S;
-            info->d_e = (int)v.hd->d_e;
-            info->d_c = (int)v.hd->d_c;
-            info->bits = (int)v.hd->bits;
-            info->group = (int)v.hd->group;
-            info->bytes = v.hd->header_bytes + (size_t)v.hd->n_layers * v.layer_bytes;
-        }
-        for (uint32_t i = 0; i < v.hd->n_layers; ++i) {
-            if (layers) layers[i] = v.edge[i];
-            if (cloud_layers) cloud_layers[i] = v.cloud[i];
-        }
-        if (kept)
-            for (uint32_t j = 0; j < v.hd->d_e; ++j) kept[j] = v.kept[j];
-    });
-}
-
-int ekv_kvpack_import(ekv_kvctx_t c, const void* src, size_t bytes) {
-    return guard([&] {
-        require(c != nullptr, "ekv_kvpack_import: null context");
-        const PackView v = pack_view(src, bytes);
-        const int H = c->model->cfg.num_heads, de = d_of(c->model);
-        require((int)v.hd->H == H && (int)v.hd->d_e == de && (int)v.hd->S == c->S,
-                "kvpack: dim mismatch (pack H=" + std::to_string(v.hd->H) + " S=" + std::to_string(v.hd->S) +
-                    " d=" + std::to_string(v.hd->d_e) + ", context H=" + std::to_string(H) +
-                    " S=" + std::to_string(c->S) + " d=" + std::to_string(de) + ")");
-        const int n = (int)v.hd->n_layers;
-        for (int i = 0; i < n; ++i) {
-            const int l = v.edge[i];
-            require(l >= 0 && l < (int)c->seg.size(), "missing layer " + std::to_string(l));
-            const ekv_segment& sg = c->seg[l];
-            require(sg.format == (int)v.hd->bits && sg.group == (int)v.hd->group,
-                    "kvpack: layer " + std::to_string(l) + " format differs from the context's");
-        }
-        set_dev(c->model->ctx);
-        cudaStream_t st = c->model->ctx->stream;
-        const size_t rows = (size_t)H * c->S, cb = rows * pack_row_bytes(de, (int)v.hd->bits),
-                     sb = rows * (de / v.hd->group) * 4;
-        for (int i = 0; i < n; ++i) {
-            const ekv_segment& sg = c->seg[v.edge[i]];
-            const unsigned char* p = v.payload + (size_t)i * v.layer_bytes;
-            EKV_CUDA(cudaMemcpyAsync((void*)sg.k, p, cb, cudaMemcpyHostToDevice, st));
-            EKV_CUDA(cudaMemcpyAsync((void*)sg.v, p + cb, cb, cudaMemcpyHostToDevice, st));
-            EKV_CUDA(cudaMemcpyAsync((void*)sg.k_scales, p + 2 * cb, sb, cudaMemcpyHostToDevice, st));
-            EKV_CUDA(cudaMemcpyAsync((void*)sg.v_scales, p + 2 * cb + sb, sb, cudaMemcpyHostToDevice, st));
-        }
-        EKV_CUDA(cudaStreamSynchronize(st));
     });
 }
 

@@ -150,6 +150,11 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
                          const cudaEvent_t* ready, float* scratch, cudaEvent_t* lev,
                          float* layer_out = nullptr);
 void session_reset(ekv_session_s* s, cudaStream_t st);
+// forward_layer_major + state advance of n user rows; ready[l] gates layer l
+// (null = resident); start/end events optional; t_comp_ms (optional) re-measures
+// each layer's compute kernel by kernel (diagnostic, doubles the work).
+void streamed_forward(ekv_session_s* s, const float* emb_dev, int n, float* out_dev, cudaEvent_t* ready,
+                      cudaEvent_t start_ev, cudaEvent_t end_ev, float* t_comp_ms);
 void release_ctx(ekv_ctx_s* c);
 void release_model(ekv_model_s* m);
 void release_kvctx(ekv_kvctx_s* c);

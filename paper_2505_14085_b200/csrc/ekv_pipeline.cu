@@ -14,6 +14,7 @@
 #include <cmath>
 #include <memory>
 #include <numeric>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -402,6 +403,20 @@ int ekv_prompt_context(ekv_model_t edge, ekv_model_t cloud, const float* emb_edg
         }
         rethrow(ekv_build_deep_kv(c, &cl, lambda, dst, n_deep, le.data(), src.data(), kept_host,
                                   cut_margin_host));
+    });
+}
+
+int ekv_generate_embeddings(uint64_t seed, int n, int h, double* out) {
+    return guard([&] {
+        require(out || n == 0 || h == 0, "ekv_generate_embeddings: null output");
+        require(n >= 0 && h >= 0, "ekv_generate_embeddings: negative shape");
+        for (int i = 0; i < n; ++i) {
+            // row i: its own mt19937_64 stream seeded with Rng::mix(seed, i) (rng.hpp:32-40)
+            std::mt19937_64 eng(mix64(seed, (uint64_t)i));
+            double* row = out + (size_t)i * h;
+            for (int c = 0; c < h; ++c)
+                row[c] = -1.0 + 2.0 * ((double)(eng() >> 11) * 0x1.0p-53);
+        }
     });
 }
 

@@ -7,7 +7,11 @@ over edge nodes, scenario.cpp:302).  The only data movement is the emulated
 cloud -> edge link: the cloud role (rank 0) aligns and compresses the deep
 layers once per prompt and broadcasts the packed KV (codes, scales, kept
 channel mask) to every edge rank -- the B200 counterpart of
-Sim::submit_transfer (sim.cpp:417-449).
+Sim::submit_transfer (sim.cpp:417-449).  The transfer is per layer
+(Sim::fetch_deep_layer, sim.cpp:802-814): layer l lands with its own CUDA
+event, so the edge's layer-major prefill (ekv_session_forward_streamed) starts
+layer l as soon as layer l arrived -- the Eq. 20 overlap of transfer and
+compute (cost_model.cpp:73-100) on real streams.
 """
 from __future__ import annotations
 
@@ -58,3 +62,95 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+class _DevPtr:
+    """__cuda_array_interface__ over raw device memory owned by the C ABI."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_bytes(ptr: int, nbytes: int, device) -> torch.Tensor:
+    """A uint8 tensor view of `nbytes` of device memory at `ptr` (no copy)."""
+    return torch.as_tensor(_DevPtr(int(ptr), int(nbytes)), device=device)
+
+
+def stream_layers(layer_bufs: list, src: int = 0, group=None, link_stream=None) -> dict:
+    """Broadcast every layer's buffers from `src`, one layer after the other, on
+    `link_stream` (CUDA) and record one event per layer when it has landed.  Returns
+    {bytes, seconds (max over ranks), events}.  Works with CPU tensors under gloo
+    (no events then)."""
+    nbytes = int(sum(t.numel() * t.element_size() for bufs in layer_bufs for t in bufs))
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return {"bytes": nbytes, "seconds": 0.0, "events": [None] * len(layer_bufs)}
+    cuda = bool(layer_bufs) and layer_bufs[0][0].is_cuda
+    dev = layer_bufs[0][0].device
+    warm = torch.zeros(1, device=dev)
+    dist.broadcast(warm, src=src, group=group)  # communicator set-up is not link time
+    dist.barrier(group)
+    if not cuda:
+        t0 = time.perf_counter()
+        for bufs in layer_bufs:
+            for t in bufs:
+                dist.broadcast(t, src=src, group=group)
+        return {"bytes": nbytes, "seconds": max_over_ranks(time.perf_counter() - t0, group=group),
+                "events": [None] * len(layer_bufs)}
+    torch.cuda.synchronize()
+    link = link_stream or torch.cuda.Stream(device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    events = []
+    with torch.cuda.stream(link):
+        e0.record(link)
+        for bufs in layer_bufs:
+            for t in bufs:
+                dist.broadcast(t, src=src, group=group)
+            ev = torch.cuda.Event()
+            ev.record(link)
+            events.append(ev)
+        e1.record(link)
+    return {"bytes": nbytes, "events": events, "timing": (e0, e1), "stream": link}
+
+
+def finish_stream(info: dict, group=None) -> dict:
+    """Wait for a stream_layers transfer and fill in its link time (max over ranks)."""
+    if "timing" in info:
+        e0, e1 = info.pop("timing")
+        info.pop("stream").synchronize()
+        info["seconds"] = max_over_ranks(e0.elapsed_time(e1) * 1e-3, device="cuda", group=group)
+    return info
+
+
+def context_layer_views(context, layers) -> list:
+    """The storage of each listed layer of an AssembledContext as uint8 device views
+    (codes K, codes V, scales K, scales V for quantised layers; K, V for bf16)."""
+    m = context.model
+    dev = torch.device("cuda", m.ctx.device)
+    out = []
+    for l in layers:
+        seg = context.segment(l)
+        rows = m.H * seg.S
+        if seg.format == 16:
+            cb, sb = rows * m.d * 2, 0
+        else:
+            cb, sb = rows * m.d * seg.format // 8, rows * (m.d // seg.group) * 4
+        bufs = [device_bytes(seg.k, cb, dev), device_bytes(seg.v, cb, dev)]
+        if sb:
+            bufs += [device_bytes(seg.k_scales, sb, dev), device_bytes(seg.v_scales, sb, dev)]
+        out.append(bufs)
+    return out
+
+
+def stream_deep_layers(context, layers, src: int = 0, group=None) -> dict:
+    """The emulated cloud -> edge link at N > 1: every listed layer of the cloud rank's
+    assembled context broadcast into every edge rank's, layer by layer (NCCL over
+    NVLink); waits for completion and reports {bytes, ms, gbs, layers, how}."""
+    info = finish_stream(stream_layers(context_layer_views(context, layers), src, group), group)
+    sec = info.get("seconds", 0.0)
+    return {"ms": 1e3 * sec, "bytes": info["bytes"], "gbs": info["bytes"] / max(sec, 1e-12) / 1e9,
+            "layers": len(layers),
+            "how": "per-layer NCCL broadcast (codes + scales of each deep layer) from rank 0 (cloud "
+                   "role) into every rank's context storage, one CUDA event per landed layer "
+                   "(Sim::fetch_deep_layer, sim.cpp:802-814); once per prompt, outside the decode "
+                   "timing"}

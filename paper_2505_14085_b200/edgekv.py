@@ -85,6 +85,22 @@ def _sync_in():
 
 
 # ------------------------------------------------------------------ stage 1
+def mix(a: int, b: int) -> int:
+    """Rng::mix (rng.hpp:35-40), the splitmix64 finaliser seeding every substream."""
+    m = (1 << 64) - 1
+    z = (a + 0x9E3779B97F4A7C15 * (b + 1)) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def generate_embeddings(seed: int, n: int, h: int) -> np.ndarray:
+    """generate_embeddings (transformer.cpp:308-317) through the C ABI: fp64 [n][h]."""
+    out = np.zeros((n, h), np.float64)
+    call("ekv_generate_embeddings", seed, n, h, _dp(out))
+    return out
+
+
 def prune_retained(lam: float, head_dim: int) -> int:
     """PruneSpec::from_lambda(lambda, head_dim).retained (head_prune.cpp:14-22)."""
     r = C.c_int()
@@ -148,7 +164,8 @@ def select_channels(ctx: Context, X: torch.Tensor, WqT: torch.Tensor, K: torch.T
 
 def prune_cache(ctx: Context, kv: torch.Tensor, kept) -> torch.Tensor:
     """prune_cache column slice (head_prune.cpp:170-197): bf16 [..., d_c] -> [..., d_e]."""
-    kept_t = torch.as_tensor(np.asarray(kept, dtype=np.int32), device=kv.device)
+    kept_t = kept.to(device=kv.device, dtype=torch.int32) if isinstance(kept, torch.Tensor) else \
+        torch.as_tensor(np.asarray(kept, dtype=np.int32), device=kv.device)
     d_c, d_e = kv.shape[-1], kept_t.numel()
     out = torch.empty(kv.shape[:-1] + (d_e,), dtype=kv.dtype, device=kv.device)
     _sync_in()
@@ -377,10 +394,12 @@ class Session:
         self.model.ctx.synchronize()
         return out
 
-    def forward_pipelined(self, emb: torch.Tensor, uploads: dict, overlap: bool = True):
+    def forward_pipelined(self, emb: torch.Tensor, uploads: dict, overlap: bool = True,
+                          measure_compute: bool = True):
         """Eq. 20 pipelined prefill: `uploads` = {layer: (k, v, k_scales, v_scales)} pinned host
         tensors (scales None for bf16 layers) copied into the context while the rows are
-        forwarded.  Returns (out [n][h], t_comm_ms [L], t_comp_ms [L], total_ms)."""
+        forwarded.  Returns (out [n][h], t_comm_ms [L], t_comp_ms [L] | None, total_ms);
+        measure_compute re-runs the rows kernel by kernel for t_comp_ms (diagnostic)."""
         emb = emb.contiguous().float()
         out = torch.empty_like(emb)
         L = self.model.L
@@ -395,8 +414,36 @@ class Session:
         _sync_in()
         call("ekv_session_forward_pipelined", self.hnd, _ptr(emb), emb.shape[0], _ptr(out),
              C.cast(arr, C.c_void_p), 1 if overlap else 0, tc.ctypes.data_as(C.POINTER(C.c_float)),
-             tp.ctypes.data_as(C.POINTER(C.c_float)), C.byref(tot))
-        return out, tc, tp, tot.value
+             tp.ctypes.data_as(C.POINTER(C.c_float)) if measure_compute else None, C.byref(tot))
+        return out, tc, (tp if measure_compute else None), tot.value
+
+    def forward_pack(self, emb: torch.Tensor, pack: torch.Tensor) -> torch.Tensor:
+        """Eq. 20 over an EKVPACK1 stream in (pinned) host memory: its layers are uploaded
+        and hashed layer by layer while the rows are forwarded layer-major."""
+        emb = emb.contiguous().float()
+        out = torch.empty_like(emb)
+        _sync_in()
+        call("ekv_session_forward_pack", self.hnd, _ptr(emb), emb.shape[0], _ptr(out),
+             C.c_void_p(pack.data_ptr()), pack.numel())
+        return out
+
+    def forward_streamed(self, emb: torch.Tensor, layer_events: dict, sync: bool = True) -> torch.Tensor:
+        """Layer-major forward of n rows where layer l's attention waits on layer_events[l]
+        (a torch.cuda.Event recorded by whoever delivers that context layer, e.g. the NCCL
+        receive of dist.stream_layers); layers without an event are resident."""
+        emb = emb.contiguous().float()
+        out = torch.empty_like(emb)
+        L = self.model.L
+        evs = (C.c_void_p * L)()
+        for l, ev in layer_events.items():
+            if ev is not None:
+                evs[l] = ev.cuda_event
+        _sync_in()
+        call("ekv_session_forward_streamed", self.hnd, _ptr(emb), emb.shape[0], _ptr(out),
+             C.cast(evs, C.c_void_p))
+        if sync:
+            self.model.ctx.synchronize()
+        return out
 
     def decode(self, steps: int, out: torch.Tensor | None = None, sync: bool = True) -> torch.Tensor:
         if out is None:
@@ -653,17 +700,38 @@ def kvpack_size(n_layers: int, H: int, S: int, d_e: int, bits: int, group: int) 
     return out.value
 
 
-def kvpack_export(context: "AssembledContext", layers, cloud_layers, kept, d_c: int) -> torch.Tensor:
-    """The compressed `layers` of the context as one EKVPACK1 byte stream (pinned host uint8)."""
+def kvpack_export(context: "AssembledContext", layers, cloud_layers, kept, d_c: int,
+                  out: torch.Tensor | None = None) -> torch.Tensor:
+    """The compressed `layers` of the context as one EKVPACK1 byte stream (pinned host uint8;
+    `out` reuses a buffer of at least kvpack_size bytes)."""
     seg = context.segment(int(layers[0]))
     m = context.model
     n = len(layers)
     size = kvpack_size(n, m.H, seg.S, m.d, seg.format, seg.group)
-    buf = torch.empty(size, dtype=torch.uint8).pin_memory()
+    buf = out if out is not None else torch.empty(size, dtype=torch.uint8).pin_memory()
+    if buf.numel() < size:
+        raise ValueError("kvpack_export: buffer too small")
     ly = np.ascontiguousarray(layers, np.int32); cl = np.ascontiguousarray(cloud_layers, np.int32)
     kp = np.ascontiguousarray(kept, np.int32)
     call("ekv_kvpack_export", context.hnd, _ip(ly), _ip(cl), n, _ip(kp), d_c, C.c_void_p(buf.data_ptr()), size)
-    return buf
+    return buf[:size]
+
+
+def kvpack_layer_uploads(buf: torch.Tensor, L: int) -> dict:
+    """Per-layer host sources of a validated pack for Session.forward_pipelined: {edge layer:
+    (k codes, v codes, k scales, v scales)} as views into the pack's payload."""
+    info = kvpack_parse(buf)
+    H, S, de, bits, g = info["H"], info["S"], info["d_e"], info["bits"], info["group"]
+    rows = H * S
+    cb, sb = rows * de * bits // 8, rows * (de // g) * 4
+    lb = 2 * cb + 2 * sb
+    hb = info["bytes"] - info["n_layers"] * lb
+    ups = {}
+    for i, l in enumerate(info["layers"]):
+        p = hb + i * lb
+        ups[l] = (buf[p:p + cb], buf[p + cb:p + 2 * cb], buf[p + 2 * cb:p + 2 * cb + sb].view(torch.float32),
+                  buf[p + 2 * cb + sb:p + lb].view(torch.float32))
+    return ups
 
 
 def kvpack_parse(buf) -> dict:

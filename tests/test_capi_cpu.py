@@ -91,3 +91,14 @@ def test_compute_entry_points_refuse_without_b200(lib):
     rc = lib.ekv_ctx_create(0, None, C.byref(h))
     assert rc == -4  # EKV_ENODEV
     assert "no CPU fallback" in lib.ekv_last_error().decode()
+
+
+def test_generate_embeddings_bit_exact(lib, oracle):
+    """a1: the product's host input generator == the reference's generate_embeddings
+    (via the pinned oracle restatement), including the width-prefix property."""
+    from paper_2505_14085_b200 import edgekv as ek
+    for seed in (42, ek.mix(42, 0x9B0BE), ek.mix(42, 0xC7E20000)):
+        assert ek.mix(seed, 7) == oracle.mix(seed, 7)
+        a = ek.generate_embeddings(seed, 9, 96)
+        assert np.array_equal(a, oracle.generate_embeddings(seed, 9, 96))
+        assert np.array_equal(ek.generate_embeddings(seed, 9, 40), a[:, :40])

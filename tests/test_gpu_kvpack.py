@@ -68,3 +68,32 @@ def test_kvpack_round_trip(ek, ctx, oracle, fmt):
     other = ek.AssembledContext(model, S + 16, formats, group=kvc.segment(1).group)
     with pytest.raises(ek.EkvError, match="dim mismatch"):
         ek.kvpack_import(other, pack)
+
+
+def test_forward_pack_eq20_over_the_wire_format(ek, ctx, oracle):
+    """ekv_session_forward_pack: the pack's layers uploaded + hashed layer by layer while
+    the user rows run layer-major == the resident-context forward, bit for bit; decode
+    continues from it; a corrupted layer is reported."""
+    L, H, d, S, U, T = 3, 4, 64, 256, 9, 3
+    formats = [16, 8, 8]
+    bits, _ = host_bf16_model(oracle, L, H, d, S + U + T + 1, seed=71)
+    model = upload_model(ek, ctx, bits, L, H, d, S + U + T + 1)
+    kvc, _, _ = make_context(ek, ctx, oracle, model, S, formats, seed=73)
+    ue = torch.from_numpy(oracle.generate_embeddings(79, U, H * d).astype(np.float32)).cuda()
+    ref = ek.Session(model, kvc, U + T)
+    want = ref.forward(ue).cpu().numpy()
+    want_steps = ref.decode(T).cpu().numpy()
+    pack = ek.kvpack_export(kvc, [1, 2], [4, 6], list(range(0, 2 * d, 2)), 2 * d)
+    kv2 = ek.AssembledContext(model, S, formats, group=kvc.segment(1).group)
+    s0 = kvc.segment(0)
+    kv2.upload_bf16(0, dev_bytes(ctx, s0.k, H * S * d * 2).view(np.uint16),
+                    dev_bytes(ctx, s0.v, H * S * d * 2).view(np.uint16))
+    sess = ek.Session(model, kv2, U + T)
+    got = sess.forward_pack(ue, pack).cpu().numpy()
+    assert np.array_equal(got, want)
+    assert np.array_equal(sess.decode(T).cpu().numpy(), want_steps)
+    bad = pack.clone()
+    bad[-5] ^= 0x40
+    s3 = ek.Session(model, kv2, U + T)
+    with pytest.raises(ek.EkvError, match="checksum mismatch in layer 2"):
+        s3.forward_pack(ue, bad)

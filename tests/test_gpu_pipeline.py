@@ -12,8 +12,8 @@
                      device at BASELINE configs[0]'s shape, then collaborative
                      decode over the result vs the oracle.
 Bars: normwise max|gpu-ref|/max|ref| <= 1e-3 per row for fp32 outputs; bf16-stored
-KV rows within one bf16 ulp of the oracle's bf16-rounded rows; masks, maps and codes
-exact.
+KV rows within that bar plus one bf16 ulp of the oracle's bf16-rounded rows; masks, maps
+and codes exact.
 """
 import numpy as np
 import pytest
@@ -39,9 +39,10 @@ def ctx(ek):
 
 
 def within_bf16_ulp(got, want):
-    """bf16-stored rows vs the oracle's bf16-rounded rows: the fp32 inputs differ by
-    ~1e-6 relative, so a rounding may land one bf16 ulp (<= 2^-7 relative) apart."""
-    tol = 2.0 ** -7 * np.abs(want) + 1e-5 * np.max(np.abs(want))
+    """bf16-stored rows vs the oracle's bf16-rounded rows: the rows are projections of
+    hidden states that carry the fp32 path's error (normwise <= 1e-3, the output bar), then
+    round to bf16, where the two roundings may land one bf16 ulp (<= 2^-7 relative) apart."""
+    tol = 2.0 ** -7 * np.abs(want) + TOL * np.max(np.abs(want))
     return bool(np.all(np.abs(got - want) <= tol))
 
 

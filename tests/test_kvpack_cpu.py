@@ -1,7 +1,8 @@
 """Packed-KV wire format (EKVPACK1, include/ekv_capi.h) -- host side, no GPU:
 the FNV-1a 64 checksum is the reference's fnv1a64 (rng.cpp:7-15, pinned through
-the oracle), and a pack written here independently from the documented layout
-is accepted by ekv_kvpack_parse, while corruption anywhere is rejected."""
+the oracle), and packs written here independently from the documented layout
+(version 1: FNV over each layer payload; version 2: FNV over 16 KiB chunk FNVs)
+are accepted by ekv_kvpack_parse, while corruption anywhere is rejected."""
 import struct
 
 import numpy as np
@@ -39,6 +40,46 @@ def write_pack(n, H, S, d_e, d_c, bits, group, seed=0):
     hdr = bytearray(head + struct.pack("<Q", 0) + body + bytes(hb - 64 - len(body)))
     struct.pack_into("<Q", hdr, 56, fnv(bytes(hdr)))
     return bytes(hdr) + b"".join(layer), edge, cloud, kept
+
+
+def chunked_fnv(arrays: list) -> int:
+    """Version-2 layer checksum: FNV-1a 64 over the little-endian u64 FNV-1a 64s of
+    16 KiB chunks of each array, in payload order."""
+    hs = []
+    for a in arrays:
+        for off in range(0, len(a), 16384):
+            hs.append(fnv(a[off:off + 16384]))
+    return fnv(struct.pack(f"<{len(hs)}Q", *hs))
+
+
+def write_pack_v2(n, H, S, d_e, d_c, bits, group, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = H * S
+    cb, sb = rows * d_e * bits // 8, rows * (d_e // group) * 4
+    layers = []
+    for _ in range(n):
+        arrs = [rng.integers(0, 256, cb, dtype=np.uint8).tobytes() for _ in range(2)] + \
+               [rng.standard_normal(sb // 4).astype(np.float32).tobytes() for _ in range(2)]
+        layers.append(arrs)
+    edge = list(range(3, 3 + n)); cloud = [e + 1 for e in edge]; kept = list(range(d_e))
+    body = struct.pack(f"<{n}i{n}i{d_e}i", *edge, *cloud, *kept) + \
+        struct.pack(f"<{n}Q", *[chunked_fnv(a) for a in layers])
+    hb = (64 + len(body) + 255) // 256 * 256
+    head = b"EKVPACK1" + struct.pack("<12I", 2, n, H, S, d_e, d_c, bits, group, hb, 0, 0, 0)
+    hdr = bytearray(head + struct.pack("<Q", 0) + body + bytes(hb - 64 - len(body)))
+    struct.pack_into("<Q", hdr, 56, fnv(bytes(hdr)))
+    return bytes(hdr) + b"".join(b"".join(a) for a in layers), edge
+
+
+def test_parse_version2_chunked_checksums():
+    # arrays longer than one 16 KiB chunk, with a short last chunk
+    buf, edge = write_pack_v2(2, 3, 100, 64, 128, 8, 64, seed=3)
+    info = ek.kvpack_parse(np.frombuffer(buf, np.uint8))
+    assert info["layers"] == edge and info["bytes"] == len(buf)
+    a = np.frombuffer(buf, np.uint8).copy()
+    a[-7] ^= 0x10  # the last layer's V scales
+    with pytest.raises(ek.EkvError, match="checksum mismatch in layer 4"):
+        ek.kvpack_parse(a)
 
 
 @pytest.mark.parametrize("bits,group", [(8, 64), (4, 32)])
