@@ -374,6 +374,14 @@ int ekv_kvctx_upload_bf16(ekv_kvctx_t c, int layer, const uint16_t* k_host,
  * sim.cpp:186-212). */
 int ekv_kvctx_set_layer(ekv_kvctx_t c, int layer, const void* k_dev, const void* v_dev,
                         const float* k_scales_dev, const float* v_scales_dev);
+/* Peer sharing of context layers (the simulator's peer source, Eq. 19
+ * cache_source -> peer, sim.cpp:705-719, 757-786): copy `layers` of `src` (a
+ * context of the same geometry, possibly on another GPU of this process) into
+ * `dst`, device to device over NVLink (cudaMemcpyPeerAsync, peer access enabled
+ * when the pair supports it), ordered after src's queued work, on dst's stream.
+ * Across processes the same transfer runs over NCCL (paper_2505_14085_b200.dist).
+ * Synchronises dst's stream. */
+int ekv_kvctx_copy_layers(ekv_kvctx_t dst, ekv_kvctx_t src, const int* layers, int n);
 /* Fill every layer with counter-hash random data (synthetic context). */
 int ekv_kvctx_synthesize(ekv_kvctx_t c, uint64_t seed);
 

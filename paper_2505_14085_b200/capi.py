@@ -102,6 +102,7 @@ PROTOS = {
     "ekv_kvctx_upload_bf16": [_vp, _i, _vp, _vp],
     "ekv_kvctx_set_layer": [_vp, _i, _vp, _vp, _vp, _vp],
     "ekv_kvctx_synthesize": [_vp, _u64],
+    "ekv_kvctx_copy_layers": [_vp, _vp, _ip, _i],
     "ekv_session_create": [_vp, _vp, _i, _pp],
     "ekv_session_destroy": [_vp],
     "ekv_session_reset": [_vp],

@@ -1433,6 +1433,59 @@ int ekv_kvctx_set_layer(ekv_kvctx_t c, int layer, const void* k, const void* v, 
     });
 }
 
+int ekv_kvctx_copy_layers(ekv_kvctx_t dst, ekv_kvctx_t src, const int* layers, int n) {
+    return guard([&] {
+        require(dst && src && (layers || n == 0), "ekv_kvctx_copy_layers: null argument");
+        ekv_model_s* dm = dst->model;
+        ekv_model_s* sm = src->model;
+        require(dm->cfg.num_heads == sm->cfg.num_heads && dm->cfg.head_dim == sm->cfg.head_dim &&
+                    dst->S == src->S,
+                "assemble_context: dim mismatch (peer context H=" + std::to_string(sm->cfg.num_heads) +
+                    " S=" + std::to_string(src->S) + ", this context H=" + std::to_string(dm->cfg.num_heads) +
+                    " S=" + std::to_string(dst->S) + ")");
+        const int dd = dm->ctx->device, sd = sm->ctx->device;
+        if (dd != sd) {  // NVLink peer access when the pair supports it (else staged by the driver)
+            int ok = 0;
+            EKV_CUDA(cudaDeviceCanAccessPeer(&ok, dd, sd));
+            if (ok) {
+                set_dev(dm->ctx);
+                cudaError_t e = cudaDeviceEnablePeerAccess(sd, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) EKV_CUDA(e);
+                (void)cudaGetLastError();
+            }
+        }
+        // the copy runs on the destination's stream after the source's queued work
+        cudaEvent_t src_done = nullptr;
+        set_dev(sm->ctx);
+        EKV_CUDA(cudaEventCreateWithFlags(&src_done, cudaEventDisableTiming));
+        EKV_CUDA(cudaEventRecord(src_done, sm->ctx->stream));
+        set_dev(dm->ctx);
+        cudaStream_t st = dm->ctx->stream;
+        cudaError_t werr = cudaStreamWaitEvent(st, src_done, 0);
+        cudaEventDestroy(src_done);
+        EKV_CUDA(werr);
+        const size_t rows = (size_t)dm->cfg.num_heads * dst->S, d = dm->cfg.head_dim;
+        for (int i = 0; i < n; ++i) {
+            const int l = layers[i];
+            require(l >= 0 && l < (int)dst->seg.size() && l < (int)src->seg.size(),
+                    "assemble_context: missing layer " + std::to_string(l));
+            const ekv_segment& a = src->seg[l];
+            const ekv_segment& b = dst->seg[l];
+            require(a.format == b.format && a.group == b.group,
+                    "assemble_context: layer " + std::to_string(l) + " format differs between the contexts");
+            if (dst->S == 0) continue;
+            const size_t cb = rows * d * b.format / 8, sb = rows * (d / std::max(b.group, 1)) * 4;
+            EKV_CUDA(cudaMemcpyPeerAsync((void*)b.k, dd, a.k, sd, cb, st));
+            EKV_CUDA(cudaMemcpyPeerAsync((void*)b.v, dd, a.v, sd, cb, st));
+            if (b.format != EKV_KV_BF16) {
+                EKV_CUDA(cudaMemcpyPeerAsync((void*)b.k_scales, dd, a.k_scales, sd, sb, st));
+                EKV_CUDA(cudaMemcpyPeerAsync((void*)b.v_scales, dd, a.v_scales, sd, sb, st));
+            }
+        }
+        EKV_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 int ekv_kvctx_synthesize(ekv_kvctx_t c, uint64_t seed) {
     return guard([&] {
         require(c != nullptr, "null context");

@@ -362,6 +362,12 @@ class AssembledContext:
     def synthesize(self, seed: int):
         call("ekv_kvctx_synthesize", self.hnd, seed)
 
+    def copy_layers_from(self, peer: "AssembledContext", layers):
+        """Peer sharing (sim.cpp:757-786): the listed layers of a peer's context (same
+        geometry, any GPU of this process) copied device to device over NVLink."""
+        ly = np.ascontiguousarray(layers, np.int32)
+        call("ekv_kvctx_copy_layers", self.hnd, peer.hnd, _ip(ly), len(ly))
+
     def __del__(self):
         try:
             capi.load().ekv_kvctx_destroy(self.hnd)

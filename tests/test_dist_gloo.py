@@ -29,6 +29,14 @@ def _worker(rank, world, port, q):
     if rank != 0:  # edge ranks start with garbage
         codes.zero_(); scales.fill_(-1.0); kept.fill_(-1)
     info = ekd.broadcast_packed_kv([codes, scales, kept])
+    # the per-layer link (Sim::fetch_deep_layer): layer by layer from the cloud rank
+    layers = [[torch.full((5,), float(rank * 100 + l)), torch.full((3,), -float(l))] for l in range(4)]
+    if rank == 0:
+        for l in range(4):
+            layers[l][0].fill_(float(l)); layers[l][1].fill_(float(10 + l))
+    st = ekd.stream_layers(layers, src=0)
+    assert st["bytes"] == 4 * (5 + 3) * 4 and len(st["events"]) == 4
+    assert all(float(layers[l][0][0]) == l and float(layers[l][1][2]) == 10 + l for l in range(4))
     digest = (int(codes.long().sum()), float(scales.sum()), kept.tolist()[:4])
     t = ekd.max_over_ranks(1.0 + rank)
     q.put((rank, digest, info["bytes"], t, ekd.session_shard(10, world, rank)))
