@@ -257,6 +257,7 @@ def bench_align_compress(ek, ctx, st, kvc, deep_match, lcs, cl, hbm, bf16_burst,
     the whole ekv_build_deep_kv call (pipeline_ms), which also leaves the deep layers of
     `kvc` filled."""
     import ctypes as C
+    import numpy as np
     import torch
     from paper_2505_14085_b200.capi import call
     S_ = S_ or S
@@ -280,7 +281,10 @@ def bench_align_compress(ek, ctx, st, kvc, deep_match, lcs, cl, hbm, bf16_burst,
         scs += [seg.k_scales, seg.v_scales]
     arr = lambda xs: (C.c_void_p * len(xs))(*xs)
     js, jc, jsc = arr(srcs), arr(cds), arr(scs)
-    kept_t = torch.arange(0, dc, 2, dtype=torch.int32, device="cuda")
+    # the channel mask this stage actually selects (the gather pattern sets the shared-
+    # memory bank behaviour of K3, so a synthetic mask would time another workload)
+    kept0, _ = ek.build_deep_kv(ctx, kvc, deep_match, cl["X"], cl["Wq"], cl["K"], cl["V"], LAMBDA, lcs)
+    kept_t = torch.from_numpy(kept0.astype(np.int32)).cuda()
     k3_ms, _ = _event_ms(st, lambda: ek.compress_batched(ctx, len(srcs), js, H_ * S_, dc, kept_t, d_e,
                                                         BITS, d_e, jc, jsc), 5)
     # the whole stage: build_deep_kv (K1 with fused K norms -> device rank -> batched K3)
@@ -799,7 +803,9 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                 srcs = [torch.empty((Hc, S, dc), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
                 for j, t in enumerate(srcs):
                     ctx.fill_uniform_bf16(t, 79, j, -1.0, 1.0)
-                kept5 = torch.arange(0, dc, 2, dtype=torch.int32, device="cuda")
+                # a mask of the kind select_channels returns (64 of 128, ascending, seeded)
+                kept5 = torch.sort(torch.randperm(dc, generator=torch.Generator().manual_seed(5))[:d]).values
+                kept5 = kept5.to(dtype=torch.int32, device="cuda")
                 sp, cp, scp = [], [], []
                 for le in range(Le - deep, Le):
                     seg = kv5.segment(le)

@@ -111,8 +111,9 @@ void release_kvctx(ekv_kvctx_s* kc) {
     if (--kc->refs > 0) return;
     ekv_model_s* m = kc->model;
     cudaSetDevice(m->ctx->device);
+    cudaStreamSynchronize(m->ctx->copy);
     cudaStreamSynchronize(m->ctx->stream);
-    for (void* p : kc->allocs) cudaFree(p);
+    for (void* p : kc->allocs) cudaFreeAsync(p, m->ctx->stream);
     delete kc;
     release_model(m);
 }
@@ -165,12 +166,13 @@ void tc_qkv_rows(ekv_session_s* s, int l, const float* in, int R, int row0, cons
         xp.part = in;
     }
     launch_batch_xprep(xp, st);
-    launch_batch_proj(s->pmap_w, l * 4 * h, 3 * h, h, pmap_x, R, s->pKSq, s->ppart, st);
+    const int ks = R <= 8 ? s->pKSq : batch_proj_splits(3 * h, h, R, m->ctx->num_sms);
+    launch_batch_proj(s->pmap_w, l * 4 * h, 3 * h, h, pmap_x, R, ks, s->ppart, st);
     PrefillFinish f{};
     f.mode = 0;
     f.R = R;
     f.N = 3 * h;
-    f.KS = s->pKSq;
+    f.KS = ks;
     f.H = m->cfg.num_heads;
     f.d = m->cfg.head_dim;
     f.cap = s->cap;
@@ -195,12 +197,13 @@ void tc_out_rows(ekv_session_s* s, int l, const float* x, float* y, float* y_his
     xp.state = s->state;
     xp.xhl = s->pxhl;
     launch_batch_xprep(xp, st);
-    launch_batch_proj(s->pmap_w, l * 4 * h + 3 * h, h, h, pmap_x, R, s->pKSo, s->ppart, st);
+    const int ks = R <= 8 ? s->pKSo : batch_proj_splits(h, h, R, s->model->ctx->num_sms);
+    launch_batch_proj(s->pmap_w, l * 4 * h + 3 * h, h, h, pmap_x, R, ks, s->ppart, st);
     PrefillFinish f{};
     f.mode = 1;
     f.R = R;
     f.N = h;
-    f.KS = s->pKSo;
+    f.KS = ks;
     f.row0 = row0;
     f.part = s->ppart;
     f.y = y;
@@ -325,10 +328,11 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m), h = m->h;
     float* X = scratch;               // layer outputs [n][h]
     float* Y = scratch + (size_t)n * h;  // attention outputs [n][h]
+    const int step = s->tc_prefill ? s->pchunk : 8;
     for (int l = 0; l < L; ++l) {
         if (lev) EKV_CUDA(cudaEventRecord(lev[l], st));
-        for (int r0 = 0; r0 < n; r0 += 8) {
-            const int R = std::min(8, n - r0);
+        for (int r0 = 0; r0 < n; r0 += step) {
+            const int R = std::min(step, n - r0);
             const bool tc = s->tc_prefill && R >= 2;
             CUtensorMap pmap_x{};
             if (tc) pmap_x = tc_operand_map(s, R);
@@ -412,28 +416,37 @@ size_t attn_ws_floats(int R, int H, int S, int d, int ucap) {
 
 void session_alloc(ekv_session_s* s) {
     ekv_model_s* m = s->model;
+    cudaStream_t ast = m->ctx->stream;
     const int L = m->cfg.num_layers, h = m->h;
-    s->uk = dalloc<uint16_t>((size_t)L * s->ukv_layer());
-    s->uv = dalloc<uint16_t>((size_t)L * s->ukv_layer());
-    s->xa = dalloc<float>((size_t)8 * h);
-    s->xb = dalloc<float>((size_t)8 * h);
-    s->q = dalloc<float>((size_t)8 * h);
-    s->emb = dalloc<float>((size_t)s->cap * h);
-    s->pre_out = dalloc<float>((size_t)s->cap * h);
-    s->hist = dalloc<float>((size_t)s->cap * h);
-    s->state = dalloc<DevState>(1);
+    s->uk = dalloc_on<uint16_t>((size_t)L * s->ukv_layer(), ast);
+    s->uv = dalloc_on<uint16_t>((size_t)L * s->ukv_layer(), ast);
+    // the layer-major forward (prefill over many rows) runs the tensor-core projections
+    // on chunks of up to 256 rows: the weights are read once per chunk, not per 8 rows
+    const bool tc = m->h % 128 == 0 && !getenv("EKV_NO_TC_PREFILL");
+    s->pchunk = tc ? std::max(8, std::min(s->cap, 256)) : 8;
+    s->xa = dalloc_on<float>((size_t)8 * h, ast);
+    s->xb = dalloc_on<float>((size_t)8 * h, ast);
+    s->q = dalloc_on<float>((size_t)s->pchunk * h, ast);
+    s->emb = dalloc_on<float>((size_t)s->cap * h, ast);
+    s->pre_out = dalloc_on<float>((size_t)s->cap * h, ast);
+    s->hist = dalloc_on<float>((size_t)s->cap * h, ast);
+    s->state = dalloc_on<DevState>(1, ast);
     size_t ws = 0;
-    for (int R = 1; R <= 8; ++R)
+    for (int R : {1, 2, 3, 4, 5, 6, 7, 8, s->pchunk})
         ws = std::max(ws, attn_ws_floats(R, m->cfg.num_heads, s->kv->S, m->cfg.head_dim, s->cap));
-    s->ws = dalloc<float>(ws);
-    s->counters = dalloc<unsigned>((size_t)8 * m->cfg.num_heads);
-    if (m->h % 128 == 0 && !getenv("EKV_NO_TC_PREFILL")) {
+    s->ws = dalloc_on<float>(ws, ast);
+    s->counters = dalloc_on<unsigned>((size_t)s->pchunk * m->cfg.num_heads, ast);
+    if (tc) {
         const int G = m->ctx->num_sms, h = m->h;
         s->tc_prefill = true;
         s->pKSq = batch_proj_splits(3 * h, h, 8, G);
         s->pKSo = batch_proj_splits(h, h, 8, G);
-        s->pxhl = dalloc<uint16_t>((size_t)2 * 8 * h);
-        s->ppart = dalloc<float>(std::max((size_t)s->pKSq * 3 * h, (size_t)s->pKSo * h) * 8);
+        s->pxhl = dalloc_on<uint16_t>((size_t)2 * s->pchunk * h, ast);
+        size_t part = 0;
+        for (int R : {8, s->pchunk})
+            part = std::max(part, std::max((size_t)batch_proj_splits(3 * h, h, R, G) * 3 * h,
+                                           (size_t)batch_proj_splits(h, h, R, G) * h) * R);
+        s->ppart = dalloc_on<float>(part, ast);
         s->pmap_w = make_map_2d(m->weights, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)h,
                                 (uint64_t)m->cfg.num_layers * 4 * h, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         // the operand map is re-encoded per chunk size R (rows >= R read as zeros)
@@ -451,10 +464,10 @@ void session_alloc(ekv_session_s* s) {
             const int G = m->ctx->num_sms;
             const int h = m->h;
             const size_t words = (size_t)h + (size_t)H * h + 3 * (size_t)h + (size_t)G * 2 * (D + 2);
-            s->mega_ll = dalloc<uint64_t>(words);
-            EKV_CUDA(cudaMemset(s->mega_ll, 0, sizeof(uint64_t) * words));
-            s->mega_sync = dalloc<unsigned>(8);
-            EKV_CUDA(cudaMemset(s->mega_sync, 0, sizeof(unsigned) * 8));
+            s->mega_ll = dalloc_on<uint64_t>(words, ast);
+            EKV_CUDA(cudaMemsetAsync(s->mega_ll, 0, sizeof(uint64_t) * words, ast));
+            s->mega_sync = dalloc_on<unsigned>(8, ast);
+            EKV_CUDA(cudaMemsetAsync(s->mega_sync, 0, sizeof(unsigned) * 8, ast));
             MegaArgs& a = s->mega;
             a.L = L;
             a.H = H;
@@ -496,10 +509,11 @@ void session_alloc(ekv_session_s* s) {
             }
         }
     }
-    EKV_CUDA(cudaMemset(s->counters, 0, sizeof(unsigned) * 8 * m->cfg.num_heads));
-    EKV_CUDA(cudaMemset(s->state, 0, sizeof(DevState)));
-    EKV_CUDA(cudaMemset(s->uk, 0, sizeof(uint16_t) * L * s->ukv_layer()));
-    EKV_CUDA(cudaMemset(s->uv, 0, sizeof(uint16_t) * L * s->ukv_layer()));
+    EKV_CUDA(cudaMemsetAsync(s->counters, 0, sizeof(unsigned) * s->pchunk * m->cfg.num_heads, ast));
+    EKV_CUDA(cudaMemsetAsync(s->state, 0, sizeof(DevState), ast));
+    EKV_CUDA(cudaMemsetAsync(s->uk, 0, sizeof(uint16_t) * L * s->ukv_layer(), ast));
+    EKV_CUDA(cudaMemsetAsync(s->uv, 0, sizeof(uint16_t) * L * s->ukv_layer(), ast));
+    EKV_CUDA(cudaStreamSynchronize(ast));
 }
 
 }  // namespace
@@ -587,6 +601,7 @@ void session_decode(ekv_session_s* s, int steps, cudaStream_t st) {
 
 void ctx_storage(ekv_kvctx_s* c) {
     ekv_model_s* m = c->model;
+    cudaStream_t ast = m->ctx->stream;
     const int L = m->cfg.num_layers, H = m->cfg.num_heads, d = d_of(m);
     c->seg.assign(L, ekv_segment{});
     for (int l = 0; l < L; ++l) {
@@ -597,18 +612,18 @@ void ctx_storage(ekv_kvctx_s* c) {
         if (c->S == 0) continue;
         const size_t rows = (size_t)H * c->S;
         if (s.format == EKV_KV_BF16) {
-            void* k = dalloc<uint16_t>(rows * d);
-            void* v = dalloc<uint16_t>(rows * d);
+            void* k = dalloc_on<uint16_t>(rows * d, ast);
+            void* v = dalloc_on<uint16_t>(rows * d, ast);
             c->allocs.push_back(k);
             c->allocs.push_back(v);
             s.k = k;
             s.v = v;
         } else {
             const size_t bytes = rows * d * s.format / 8;
-            void* k = dalloc<uint8_t>(bytes);
-            void* v = dalloc<uint8_t>(bytes);
-            float* ks = dalloc<float>(rows * (d / s.group));
-            float* vs = dalloc<float>(rows * (d / s.group));
+            void* k = dalloc_on<uint8_t>(bytes, ast);
+            void* v = dalloc_on<uint8_t>(bytes, ast);
+            float* ks = dalloc_on<float>(rows * (d / s.group), ast);
+            float* vs = dalloc_on<float>(rows * (d / s.group), ast);
             for (void* p : {k, v, (void*)ks, (void*)vs}) c->allocs.push_back(p);
             s.k = k;
             s.v = v;
@@ -884,6 +899,11 @@ int ekv_ctx_create(int device, void* stream, ekv_ctx_t* out) {
         }
         EKV_CUDA(cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking));
         EKV_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        // keep freed stream-ordered allocations in the pool (per-request objects)
+        cudaMemPool_t pool;
+        EKV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        EKV_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         *out = c;
     });
 }
@@ -1367,10 +1387,12 @@ int ekv_kvctx_create(ekv_model_t m, int S, const int* layer_format, int group, e
             set_dev(m->ctx);
             ctx_storage(c);
         } catch (...) {
-            for (void* p : c->allocs) cudaFree(p);
+            for (void* p : c->allocs) cudaFreeAsync(p, m->ctx->stream);
+            cudaStreamSynchronize(m->ctx->stream);
             delete c;
             throw;
         }
+        EKV_CUDA(cudaStreamSynchronize(m->ctx->stream));  // storage usable from any stream
         m->refs++;
         *out = c;
     });
@@ -1544,8 +1566,10 @@ int ekv_session_create(ekv_model_t m, ekv_kvctx_t c, int max_user_rows, ekv_sess
         } catch (...) {
             for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                             (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
-                            (void*)s->ws, (void*)s->counters, (void*)s->pxhl, (void*)s->ppart})
-                cudaFree(p);
+                            (void*)s->ws, (void*)s->counters, (void*)s->pxhl, (void*)s->ppart,
+                            (void*)s->mega_ll, (void*)s->mega_sync})
+                if (p) cudaFreeAsync(p, m->ctx->stream);
+            cudaStreamSynchronize(m->ctx->stream);
             delete s;
             throw;
         }
@@ -1559,13 +1583,15 @@ int ekv_session_destroy(ekv_session_t s) {
     return guard([&] {
         if (!s) return;
         cudaSetDevice(s->model->ctx->device);
-        cudaStreamSynchronize(s->model->ctx->stream);
+        cudaStream_t fst = s->model->ctx->stream;
+        cudaStreamSynchronize(s->model->ctx->copy);
+        cudaStreamSynchronize(fst);
         if (s->step_graph) cudaGraphExecDestroy(s->step_graph);
         for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                         (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
                         (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync,
                         (void*)s->pxhl, (void*)s->ppart})
-            cudaFree(p);
+            if (p) cudaFreeAsync(p, fst);
         ekv_kvctx_s* kv = s->kv;
         ekv_model_s* m = s->model;
         delete s;

@@ -52,6 +52,23 @@ T* dalloc(size_t count) {
 }
 
 
+// Stream-ordered allocation from the device's default memory pool (kept cached:
+// ekv_ctx_create raises the pool's release threshold), for the objects created
+// per request -- sessions, assembled contexts, prefill scratch -- so creating and
+// destroying them costs no device-wide synchronisation.
+template <class T>
+T* dalloc_on(size_t count, cudaStream_t st) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMallocAsync(&p, count * sizeof(T), st);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        throw Error(EKV_ENOMEM, "cudaMallocAsync of " + std::to_string(count * sizeof(T)) +
+                                    " bytes failed: " + cudaGetErrorString(e));
+    }
+    return (T*)p;
+}
+
 }  // namespace ekv
 
 using ekv::DevState;
@@ -132,6 +149,7 @@ struct ekv_session_s {
     uint16_t* pxhl = nullptr;      // [2][8][h] bf16 hi / lo operand
     float* ppart = nullptr;        // [max(KSq*3h, KSo*h)][8] split-K partials
     int pKSq = 1, pKSo = 1;
+    int pchunk = 8;                // rows per tensor-core chunk of the layer-major forward
     CUtensorMap pmap_w{}, pmap_x{};
     size_t ukv_layer() const { return (size_t)model->cfg.num_heads * cap * model->cfg.head_dim; }
 };

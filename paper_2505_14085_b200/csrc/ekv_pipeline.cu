@@ -41,11 +41,12 @@ void rethrow(int rc) {
     if (rc != EKV_OK) throw Error(rc, g_err);
 }
 
-// device buffer freed on scope exit (cold paths only: prefill / layer map)
+// device buffer of one call, stream-ordered on the context stream (pooled)
 struct DevMem {
     void* p = nullptr;
-    explicit DevMem(size_t bytes) { p = dalloc<uint8_t>(bytes); }
-    ~DevMem() { cudaFree(p); }
+    cudaStream_t st;
+    DevMem(size_t bytes, cudaStream_t s) : st(s) { p = dalloc_on<uint8_t>(bytes, s); }
+    ~DevMem() { cudaFreeAsync(p, st); }
     template <class T>
     T* as() const { return (T*)p; }
 };
@@ -70,7 +71,7 @@ void device_prefill(ekv_model_s* m, const float* emb, int n, float* layer_out, f
     rethrow(ekv_session_create(m, kv, n, &s));
     std::unique_ptr<ekv_session_s, int (*)(ekv_session_t)> sg(s, ekv_session_destroy);
     check_overflow(s, n);
-    DevMem scratch(sizeof(float) * 2 * (size_t)n * h);
+    DevMem scratch(sizeof(float) * 2 * (size_t)n * h, st);
     if (x0) launch_input_transform(emb, m->gamma, m->bias, m->pos, kv->S, n, h, x0, st);
     forward_layer_major(s, emb, n, 0, st, nullptr, scratch.as<float>(), nullptr, layer_out);
     const size_t kv_bytes = sizeof(uint16_t) * (size_t)L * s->ukv_layer();  // cap == n
@@ -197,7 +198,7 @@ int ekv_match_layers(ekv_ctx_t c, const double* edge_outs, int me, int ce, const
         require(n >= 1 && ce >= 1 && cc >= 1, "match_layers: bad layer width");
         set_dev(c);
         const size_t ne = (size_t)me * n * ce, ncl = (size_t)nc * n * cc;
-        DevMem d(sizeof(double) * (ne + ncl));
+        DevMem d(sizeof(double) * (ne + ncl), c->stream);
         EKV_CUDA(cudaMemcpyAsync(d.as<double>(), edge_outs, sizeof(double) * ne, cudaMemcpyHostToDevice,
                                  c->stream));
         EKV_CUDA(cudaMemcpyAsync(d.as<double>() + ne, cloud_outs, sizeof(double) * ncl,
@@ -223,8 +224,8 @@ int ekv_deep_match(ekv_model_t edge, ekv_model_t cloud, const float* edge_probe,
         const int he = edge->h, hc = cloud->h;
         const size_t ne = (size_t)M * n * he, ncl = (size_t)N * n * hc;
         // probe prefill of both models; per-layer outputs fp32 -> fp64 for K7
-        DevMem f32(sizeof(float) * std::max(ne, ncl));
-        DevMem f64(sizeof(double) * (ne + ncl));
+        DevMem f32(sizeof(float) * std::max(ne, ncl), c->stream);
+        DevMem f64(sizeof(double) * (ne + ncl), c->stream);
         device_prefill(edge, edge_probe, n, f32.as<float>(), nullptr, nullptr, nullptr);
         launch_f32_to_f64(f32.as<float>(), f64.as<double>(), (int64_t)ne, c->stream);
         device_prefill(cloud, cloud_probe, n, f32.as<float>(), nullptr, nullptr, nullptr);
@@ -345,7 +346,7 @@ int ekv_prompt_context(ekv_model_t edge, ekv_model_t cloud, const float* emb_edg
         // edge prefill of the context rows -> local layers [0, boundary) (sim.cpp:133, 192-205)
         if (boundary > 0) {
             const size_t lkv = (size_t)He * S * de;
-            DevMem ek(sizeof(uint16_t) * M * lkv), ev(sizeof(uint16_t) * M * lkv);
+            DevMem ek(sizeof(uint16_t) * M * lkv, st), ev(sizeof(uint16_t) * M * lkv, st);
             device_prefill(edge, emb_edge, S, nullptr, nullptr, ek.p, ev.p);
             for (int l = 0; l < boundary; ++l) {
                 const ekv_segment& sg = dst->seg[l];
@@ -371,10 +372,10 @@ int ekv_prompt_context(ekv_model_t edge, ekv_model_t cloud, const float* emb_edg
         lcs.erase(std::unique(lcs.begin(), lcs.end()), lcs.end());  // std::set order (sim.cpp:219-221)
         const int m = (int)lcs.size();
         const size_t ckv = (size_t)Hc * S * dc;
-        DevMem lo(sizeof(float) * (size_t)Lc * S * hc), x0(sizeof(float) * (size_t)S * hc);
-        DevMem ck(sizeof(uint16_t) * Lc * ckv), cv(sizeof(uint16_t) * Lc * ckv);
+        DevMem lo(sizeof(float) * (size_t)Lc * S * hc, st), x0(sizeof(float) * (size_t)S * hc, st);
+        DevMem ck(sizeof(uint16_t) * Lc * ckv, st), cv(sizeof(uint16_t) * Lc * ckv, st);
         device_prefill(cloud, emb_cloud, S, lo.as<float>(), x0.as<float>(), ck.p, cv.p);
-        DevMem xb(sizeof(uint16_t) * (size_t)m * S * hc);
+        DevMem xb(sizeof(uint16_t) * (size_t)m * S * hc, st);
         std::vector<const void*> kp(m), vp(m);
         std::vector<int> wq_index(m);
         for (int i = 0; i < m; ++i) {

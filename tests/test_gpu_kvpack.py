@@ -81,7 +81,7 @@ def test_forward_pack_eq20_over_the_wire_format(ek, ctx, oracle):
     kvc, _, _ = make_context(ek, ctx, oracle, model, S, formats, seed=73)
     ue = torch.from_numpy(oracle.generate_embeddings(79, U, H * d).astype(np.float32)).cuda()
     ref = ek.Session(model, kvc, U + T)
-    want = ref.forward(ue).cpu().numpy()
+    want = ref.forward_streamed(ue, {}).cpu().numpy()   # the same layer-major forward, resident
     want_steps = ref.decode(T).cpu().numpy()
     pack = ek.kvpack_export(kvc, [1, 2], [4, 6], list(range(0, 2 * d, 2)), 2 * d)
     kv2 = ek.AssembledContext(model, S, formats, group=kvc.segment(1).group)
