@@ -521,7 +521,7 @@ int ekv_collaborative_decode_batch(ekv_batch_t b, const float* user_emb_host, in
  *   [H][S][d_e/group], V scales
  * Checksums are FNV-1a 64 (the reference's fnv1a64, rng.cpp:7-15): the header
  * (with header_fnv = 0) over its bytes; a layer (version 2) over the u64 FNV-1a
- * 64s, little-endian, of its four arrays cut into 16 KiB chunks in payload order
+ * 64s, little-endian, of its four arrays cut into 4 KiB chunks in payload order
  * (the last chunk of an array may be shorter) -- independent chunks, so the
  * device hashes a layer where its bytes are.  Version 1 (FNV-1a over the whole
  * layer payload) is still read. */

@@ -88,6 +88,7 @@ void release_ctx(ekv_ctx_s* c) {
     if (c->own_stream) cudaStreamDestroy(c->stream);
     cudaStreamDestroy(c->capture);
     if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->aux) cudaStreamDestroy(c->aux);
     if (c->attn_ws) cudaFree(c->attn_ws);
     if (c->attn_ctr) cudaFree(c->attn_ctr);
     if (c->scratch) cudaFree(c->scratch);
@@ -544,6 +545,12 @@ namespace {
 void session_forward(ekv_session_s* s, const float* emb_dev, int n, cudaStream_t st,
                      const cudaEvent_t* ready = nullptr) {
     check_overflow(s, n);
+    if (s->tc_prefill && n >= 2 && !ready) {
+        // many rows: layer-major, every layer's weights read once per chunk of <= 256
+        // rows by the tensor-core projections (the user prefill of collaborative_decode)
+        streamed_forward(s, emb_dev, n, nullptr, nullptr, nullptr, nullptr, nullptr);
+        return;
+    }
     for (int r0 = 0; r0 < n; r0 += 8) {
         const int R = std::min(8, n - r0);
         forward_chunk(s, emb_dev + (size_t)r0 * s->model->h, R, s->pre_out,
@@ -899,6 +906,7 @@ int ekv_ctx_create(int device, void* stream, ekv_ctx_t* out) {
         }
         EKV_CUDA(cudaStreamCreateWithFlags(&c->capture, cudaStreamNonBlocking));
         EKV_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        EKV_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
         // keep freed stream-ordered allocations in the pool (per-request objects)
         cudaMemPool_t pool;
         EKV_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));

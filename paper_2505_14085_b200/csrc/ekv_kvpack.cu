@@ -6,7 +6,7 @@
 // (sim.cpp:885-895).  Checksums are the reference's fnv1a64 (rng.cpp:7-15).
 //
 // Version 2 (written here): each of a layer's four arrays (K codes, V codes,
-// K scales, V scales) is cut into 16 KiB chunks; the layer checksum is
+// K scales, V scales) is cut into 4 KiB chunks; the layer checksum is
 // FNV-1a 64 over the little-endian u64 FNV-1a 64 of every chunk, in payload
 // order.  The chunk hashes are independent, so the device hashes a layer in
 // microseconds (one thread per chunk) right where the bytes are: export hashes
@@ -26,7 +26,7 @@ using namespace ekv;
 namespace {
 constexpr char kPackMagic[8] = {'E', 'K', 'V', 'P', 'A', 'C', 'K', '1'};
 constexpr uint32_t kPackVersion = 2;
-constexpr size_t kChunk = 16384;
+constexpr size_t kChunk = 4096;
 constexpr uint64_t kFnvOffset = 14695981039346656037ull, kFnvPrime = 1099511628211ull;
 
 struct PackHeader {  // 64 bytes, little-endian
@@ -407,7 +407,7 @@ int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float
         ekv_ctx_s* ctx = m->ctx;
         check_overflow(s, n);
         set_dev(ctx);
-        cudaStream_t st = ctx->stream, cp = ctx->copy;
+        cudaStream_t st = ctx->stream, cp = ctx->copy, hs = ctx->aux;
         const int L = m->cfg.num_layers, nl = (int)v.hd->n_layers;
         std::vector<cudaEvent_t> ready(L, nullptr);
         cudaEvent_t start = nullptr;
@@ -421,10 +421,13 @@ int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float
             EKV_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
             EKV_CUDA(cudaEventRecord(start, st));
             EKV_CUDA(cudaStreamWaitEvent(cp, start, 0));
-            // per layer on the copy stream: upload into the context, hash it there, then
-            // release the layer to the compute stream (Eq. 20: upload l overlaps compute < l)
+            // per layer on the copy stream: upload into the context and release the layer to
+            // the compute stream (Eq. 20: upload l overlaps compute < l); the checksum of
+            // layer l runs on a third stream behind its upload, off both critical paths
             const size_t per = v.la.chunks();
             EKV_CUDA(cudaMallocAsync((void**)&dch, sizeof(uint64_t) * per * nl, cp));
+            EKV_CUDA(cudaEventRecord(start, cp));
+            EKV_CUDA(cudaStreamWaitEvent(hs, start, 0));
             for (int i = 0; i < nl; ++i) {
                 const int l = v.edge[i];
                 HashTable t{};
@@ -439,15 +442,17 @@ int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float
                 }
                 EKV_CUDA(cudaEventCreateWithFlags(&ready[l], cudaEventDisableTiming));
                 EKV_CUDA(cudaEventRecord(ready[l], cp));
-                chunk_fnv_kernel<<<(t.first[4] + 127) / 128, 128, 0, cp>>>(t, dch + (size_t)i * per);
+                EKV_CUDA(cudaStreamWaitEvent(hs, ready[l], 0));
+                chunk_fnv_kernel<<<(t.first[4] + 127) / 128, 128, 0, hs>>>(t, dch + (size_t)i * per);
                 EKV_CUDA(cudaGetLastError());
                 count_launches(1);
             }
             streamed_forward(s, emb_dev, n, out_dev, ready.data(), nullptr, nullptr, nullptr);
             std::vector<uint64_t> ch(per * nl);
-            EKV_CUDA(cudaMemcpyAsync(ch.data(), dch, sizeof(uint64_t) * ch.size(), cudaMemcpyDeviceToHost, cp));
-            EKV_CUDA(cudaFreeAsync(dch, cp));
+            EKV_CUDA(cudaMemcpyAsync(ch.data(), dch, sizeof(uint64_t) * ch.size(), cudaMemcpyDeviceToHost, hs));
+            EKV_CUDA(cudaFreeAsync(dch, hs));
             dch = nullptr;
+            EKV_CUDA(cudaStreamSynchronize(hs));
             EKV_CUDA(cudaStreamSynchronize(cp));
             EKV_CUDA(cudaStreamSynchronize(st));
             for (int i = 0; i < nl; ++i)
@@ -455,6 +460,7 @@ int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float
                         "kvpack: checksum mismatch in layer " + std::to_string(v.edge[i]) +
                             " (the forward's outputs and the context's layers are invalid)");
         } catch (...) {
+            cudaStreamSynchronize(hs);
             if (dch) cudaFreeAsync(dch, cp);
             cudaStreamSynchronize(cp);
             cudaStreamSynchronize(st);

@@ -85,6 +85,7 @@ struct ekv_ctx_s {
     cudaStream_t stream = nullptr;
     cudaStream_t capture = nullptr;  // graphs are captured here, launched on `stream`
     cudaStream_t copy = nullptr;     // context uploads of the pipelined prefill (Eq. 20)
+    cudaStream_t aux = nullptr;      // side work off the critical path (pack checksums)
     bool own_stream = false;
     // scratch of ekv_decode_attention (split-KV partials + merge counters), grown on demand
     float* attn_ws = nullptr;

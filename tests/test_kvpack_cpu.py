@@ -1,7 +1,7 @@
 """Packed-KV wire format (EKVPACK1, include/ekv_capi.h) -- host side, no GPU:
 the FNV-1a 64 checksum is the reference's fnv1a64 (rng.cpp:7-15, pinned through
 the oracle), and packs written here independently from the documented layout
-(version 1: FNV over each layer payload; version 2: FNV over 16 KiB chunk FNVs)
+(version 1: FNV over each layer payload; version 2: FNV over 4 KiB chunk FNVs)
 are accepted by ekv_kvpack_parse, while corruption anywhere is rejected."""
 import struct
 
@@ -44,11 +44,11 @@ def write_pack(n, H, S, d_e, d_c, bits, group, seed=0):
 
 def chunked_fnv(arrays: list) -> int:
     """Version-2 layer checksum: FNV-1a 64 over the little-endian u64 FNV-1a 64s of
-    16 KiB chunks of each array, in payload order."""
+    4 KiB chunks of each array, in payload order."""
     hs = []
     for a in arrays:
-        for off in range(0, len(a), 16384):
-            hs.append(fnv(a[off:off + 16384]))
+        for off in range(0, len(a), 4096):
+            hs.append(fnv(a[off:off + 4096]))
     return fnv(struct.pack(f"<{len(hs)}Q", *hs))
 
 
@@ -72,7 +72,7 @@ def write_pack_v2(n, H, S, d_e, d_c, bits, group, seed=0):
 
 
 def test_parse_version2_chunked_checksums():
-    # arrays longer than one 16 KiB chunk, with a short last chunk
+    # arrays longer than one 4 KiB chunk, with a short last chunk
     buf, edge = write_pack_v2(2, 3, 100, 64, 128, 8, 64, seed=3)
     info = ek.kvpack_parse(np.frombuffer(buf, np.uint8))
     assert info["layers"] == edge and info["bytes"] == len(buf)
