@@ -106,6 +106,29 @@ def cpu_reference(seconds_budget: float, threads: int, calls: int | None = None)
     raise RuntimeError("oracle/_ref not built; port baseline not wired for C2 (see DESIGN.md)")
 
 
+def cpu_reference_c4(threads: int):
+    """configs[3] CPU baseline, bounded: the reference's collaborative_decode on a 2-layer
+    slice of the C4 edge (1 local + 1 cloud layer, 32 heads x 64, S = 32768 context rows),
+    `threads` concurrent sessions of (1 user row + 1 decode step); the per-layer cost is
+    extrapolated linearly to the 22 layers of the edge model."""
+    from oracle import REF_SO, Reference  # CPU-baseline leg only
+    if not os.path.exists(REF_SO):
+        return None
+    ref = Reference()
+    S4, Ls = 32768, 2
+    hnd = ref.bench_setup(Ls, EDGE["H"], EDGE["d"], S4, 1, S4 + 8, 43)
+    try:
+        sec, rows = ref.bench_run(hnd, 1, 1, threads, 1)
+    finally:
+        ref.bench_free(hnd)
+    per_row_layer = sec / (rows / threads) / Ls  # seconds per row per layer, per session
+    tok_s = threads / (per_row_layer * EDGE["L"])
+    return {"value": tok_s, "unit": "tok/s", "cores": threads, "kind": "reference",
+            "sample": f"reference collaborative_decode (fp64) on a {Ls}-layer slice of the C4 edge "
+                      f"(S={S4}), {threads} concurrent sessions x (1 user row + 1 step) in {sec:.1f} s; "
+                      f"extrapolated x{EDGE['L']}/{Ls} layers (cost is linear in layers)"}
+
+
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
@@ -888,6 +911,18 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             cpu = {"value": None, "unit": "tok/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)[:200]}
 
+    if cpu and conc and "error" not in conc:
+        conc["cpu_baseline"] = dict(cpu, sample="the same measurement as cpu_baseline: "
+                                    f"{cpu.get('cores')} concurrent sessions of the reference's "
+                                    "collaborative_decode, one per host thread (aggregate tok/s; "
+                                    "the reference itself is single-threaded)")
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and c4 and "error" not in c4:
+        try:
+            c4["cpu_baseline"] = cpu_reference_c4(ref_threads())
+            if c4["cpu_baseline"] and c4.get("decode"):
+                c4["decode"]["speedup_vs_cpu"] = c4["decode"]["tok_s"] / c4["cpu_baseline"]["value"]
+        except Exception as e:  # noqa: BLE001
+            c4["cpu_baseline"] = {"value": None, "kind": "unavailable", "sample": str(e)[:200]}
     if rank == 0:
         tok_s = world * K / (ms * 1e-3)
         line = {
