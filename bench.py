@@ -560,8 +560,15 @@ def run_b200(args, rank: int, world: int, local_rank: int):
     align = bench_align_compress(ek, ctx, st, kvc, deep_match, lcs, cl, hbm, bf16_burst)
     kv_transfer = None
     if world > 1:
-        from paper_2505_14085_b200.dist import stream_deep_layers
+        from paper_2505_14085_b200.dist import capi_link, link_deep_layers, stream_deep_layers
         kv_transfer = stream_deep_layers(kvc, list(range(L - DEEP, L)), src=0)
+        try:
+            link = capi_link(ctx)
+            rx = ek.Session(model, kvc, 4)
+            kv_transfer["capi_link"] = link_deep_layers(link, kvc, rx, list(range(L - DEEP, L)))
+            del rx, link
+        except Exception as e:  # noqa: BLE001
+            kv_transfer["capi_link"] = {"error": str(e)[:300]}
 
     # --- decode session: prefill U rows, warm up, then K timed graph replays ---
     sess = ek.Session(model, kvc, cap)

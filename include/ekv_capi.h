@@ -74,8 +74,11 @@ int ekv_ctx_synchronize(ekv_ctx_t ctx);
 int ekv_ctx_kernel_launches(ekv_ctx_t ctx, int64_t* count);
 
 /* Device memory helpers for hosts that do not link the CUDA runtime (the C++
- * mirror): allocation on the context's device, and synchronous copies on the
- * context stream.  kind: 0 host->device, 1 device->host, 2 device->device. */
+ * mirror): allocation on the context's device from the device's pooled
+ * stream-ordered allocator (no device-wide synchronisation per allocation;
+ * ekv_device_free releases after the context stream's queued work), and
+ * synchronous copies on the context stream.  kind: 0 host->device,
+ * 1 device->host, 2 device->device. */
 int ekv_device_alloc(ekv_ctx_t ctx, size_t bytes, void** out);
 int ekv_device_free(ekv_ctx_t ctx, void* p);
 int ekv_memset(ekv_ctx_t ctx, void* dst_dev, int value, size_t bytes);
@@ -555,6 +558,31 @@ int ekv_kvpack_import(ekv_kvctx_t c, const void* host_src, size_t bytes);
  * Synchronises. */
 int ekv_session_forward_pack(ekv_session_t s, const float* emb_dev, int n, float* out_dev,
                              const void* host_src, size_t bytes);
+
+/* ------------------------------------------------------------------ */
+/* The emulated cloud -> edge link over NCCL (one process per GPU)      */
+/* ------------------------------------------------------------------ */
+/* The B200 counterpart of Sim::fetch_deep_layer -> submit_transfer
+ * (sim.cpp:802-814, 417-449): the cloud rank sends the compressed deep layers of
+ * its assembled context layer by layer (ncclSend, one NCCL group per layer, on the
+ * context's copy stream); the edge rank receives them straight into its context's
+ * storage while the user rows are forwarded layer-major on the compute stream,
+ * layer l's attention waiting only for layer l's receive (Eq. 20,
+ * cost_model.cpp:73-100).  NCCL (libnccl.so.2) is resolved at run time.
+ * id: the 128-byte ncclUniqueId, made on one rank and shared out of band. */
+typedef struct ekv_link_s* ekv_link_t;
+int ekv_link_unique_id(void* id128);
+int ekv_link_create(ekv_ctx_t ctx, const void* id128, int nranks, int rank, ekv_link_t* out);
+int ekv_link_destroy(ekv_link_t link);
+/* Sender: `layers` of src (after the context stream's queued work) to rank peer.
+ * seconds (optional): link time of the whole transfer.  Synchronises. */
+int ekv_link_send_layers(ekv_link_t link, ekv_kvctx_t src, const int* layers, int n, int peer,
+                         float* seconds);
+/* Receiver: `layers` of the session's context from rank peer; with rows > 0 the
+ * session forwards emb_dev (fp32 [rows][h]) layer-major meanwhile (out_dev fp32
+ * [rows][h], may be NULL).  seconds (optional): link time.  Synchronises. */
+int ekv_link_recv_forward(ekv_link_t link, ekv_session_t s, const int* layers, int n, int peer,
+                          const float* emb_dev, int rows, float* out_dev, float* seconds);
 
 /* ------------------------------------------------------------------ */
 /* Scheduler interface (cost_model.hpp:53-84)                          */

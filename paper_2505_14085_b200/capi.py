@@ -130,6 +130,11 @@ PROTOS = {
     "ekv_batch_profile_row": [_vp, _fp, _i, _ip],
     "ekv_collaborative_decode_batch": [_vp, _vp, _i, _i, _vp, _vp],
     "ekv_collaborative_decode": [_vp, _vp, _i, _i, _vp, _vp],
+    "ekv_link_unique_id": [_vp],
+    "ekv_link_create": [_vp, _vp, _i, _i, _pp],
+    "ekv_link_destroy": [_vp],
+    "ekv_link_send_layers": [_vp, _vp, _ip, _i, _i, _fp],
+    "ekv_link_recv_forward": [_vp, _vp, _ip, _i, _i, _vp, _i, _vp, _fp],
     "ekv_cache_source": [_i, _d, _d, _i, _i, _ip],
     "ekv_pipeline_schedule": [_dp, _dp, _i, _dp, _dp, _dp],
 }

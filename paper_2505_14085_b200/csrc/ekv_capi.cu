@@ -948,7 +948,10 @@ int ekv_device_alloc(ekv_ctx_t c, size_t bytes, void** out) {
     return guard([&] {
         require(c && out, "ekv_device_alloc: null argument");
         set_dev(c);
-        *out = dalloc<uint8_t>(bytes);
+        // from the device's pooled stream-ordered allocator: the C++ mirror allocates per
+        // call, and the pool makes that free of cudaMalloc / cudaFree device syncs
+        *out = dalloc_on<uint8_t>(bytes, c->stream);
+        EKV_CUDA(cudaStreamSynchronize(c->stream));  // usable from any stream on return
     });
 }
 
@@ -956,7 +959,7 @@ int ekv_device_free(ekv_ctx_t c, void* p) {
     return guard([&] {
         require(c != nullptr, "null context");
         set_dev(c);
-        EKV_CUDA(cudaFree(p));
+        if (p) EKV_CUDA(cudaFreeAsync(p, c->stream));  // after the stream's queued work
     });
 }
 

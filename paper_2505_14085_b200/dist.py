@@ -154,3 +154,32 @@ def stream_deep_layers(context, layers, src: int = 0, group=None) -> dict:
                    "role) into every rank's context storage, one CUDA event per landed layer "
                    "(Sim::fetch_deep_layer, sim.cpp:802-814); once per prompt, outside the decode "
                    "timing"}
+
+
+def capi_link(ctx, group=None):
+    """An ekv_link (the C ABI's NCCL link) over the ranks of `group`: rank 0 makes the
+    NCCL unique id, every rank receives it through torch.distributed (plumbing only)."""
+    from . import edgekv as ek
+    uid = [ek.Link.unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    return ek.Link(ctx, uid[0], dist.get_world_size(group), dist.get_rank(group))
+
+
+def link_deep_layers(link, context, session, layers) -> dict:
+    """The cloud rank (0) sends `layers` of its context to every other rank through the C
+    ABI's link (ncclSend / ncclRecv per layer); returns the per-destination link time."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    secs = []
+    for dst in range(1, world):
+        if rank == 0:
+            secs.append(link.send_layers(context, layers, dst))
+        elif rank == dst:
+            secs.append(link.recv_forward(session, layers, 0)[1])
+        dist.barrier()
+    sec = max_over_ranks(max(secs) if secs else 0.0, device="cuda")
+    nbytes = int(sum(t.numel() for bufs in context_layer_views(context, layers) for t in bufs))
+    return {"ms_per_destination": 1e3 * sec, "bytes": nbytes, "gbs": nbytes / max(sec, 1e-12) / 1e9,
+            "destinations": world - 1, "layers": len(layers),
+            "how": "C-ABI link (ekv_link_send_layers / ekv_link_recv_forward): ncclSend/ncclRecv of "
+                   "each deep layer's codes + scales, one NCCL group per layer, from rank 0 (cloud "
+                   "role) to each edge rank in turn; once per prompt, outside the decode timing"}

@@ -499,6 +499,52 @@ class Session:
             pass
 
 
+class Link:
+    """ekv_link: the emulated cloud -> edge link over NCCL from the C ABI (one process per
+    GPU): per-layer sends of the cloud context's deep layers, received into the edge's
+    context while its user rows run layer-major (Eq. 20)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        call("ekv_link_unique_id", C.cast(buf, C.c_void_p))
+        return buf.raw
+
+    def __init__(self, ctx: Context, uid: bytes, nranks: int, rank: int):
+        self.ctx = ctx
+        hnd = C.c_void_p()
+        call("ekv_link_create", ctx.h, C.c_char_p(uid), nranks, rank, C.byref(hnd))
+        self.hnd = hnd
+
+    def send_layers(self, context: "AssembledContext", layers, peer: int) -> float:
+        ly = np.ascontiguousarray(layers, np.int32)
+        sec = C.c_float()
+        call("ekv_link_send_layers", self.hnd, context.hnd, _ip(ly), len(ly), peer, C.byref(sec))
+        return sec.value
+
+    def recv_forward(self, session: "Session", layers, peer: int, emb: torch.Tensor | None = None):
+        """Receive `layers` into the session's context; with emb (fp32 [n][h], device) the rows
+        are forwarded meanwhile.  Returns (out [n][h] | None, link seconds)."""
+        ly = np.ascontiguousarray(layers, np.int32)
+        sec = C.c_float()
+        out = None
+        n = 0
+        if emb is not None:
+            emb = emb.contiguous().float()
+            out = torch.empty_like(emb)
+            n = emb.shape[0]
+            _sync_in()
+        call("ekv_link_recv_forward", self.hnd, session.hnd, _ip(ly), len(ly), peer, _ptr(emb), n,
+             _ptr(out), C.byref(sec))
+        return out, sec.value
+
+    def __del__(self):
+        try:
+            capi.load().ekv_link_destroy(self.hnd)
+        except Exception:
+            pass
+
+
 class SessionBatch:
     """ekv_batch: B concurrent sessions over one shared AssembledContext, advanced in
     lock-step (BASELINE configs[2]).  Per session the result is collaborative_decode
