@@ -97,9 +97,16 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
     const int sub = lane % LPR, rsub = lane / LPR;
     const int glanes = group / 8;  // lanes per group (power of two, <= LPR)
     const int ng = DE / group;
-    int ch2[8];  // byte offsets of my kept channels inside a row
+    // Byte offsets of my kept channels inside a row.  Rows sit 2*DC bytes apart (a
+    // multiple of 128 B), so a channel falls in the same shared-memory bank in every
+    // row: the RPW row groups of a warp would all hit the same banks when they gather
+    // the same channel index.  Each row group walks its 8 channels rotated by 2*rsub
+    // instead (different channels -> different banks at every step), and the codes
+    // are rotated back into channel order when packed.
+    const int rot = 2 * (rsub & 3);
+    int ch2[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ch2[e] = 2 * kept[sub * 8 + e];
+    for (int e = 0; e < 8; ++e) ch2[e] = 2 * kept[sub * 8 + ((e + rot) & 7)];
     const int64_t ntiles = (rows + TC::TILE - 1) / TC::TILE;
     const int64_t total = ntiles * n_jobs;
     if (threadIdx.x == 0) {
@@ -171,15 +178,21 @@ __global__ void __launch_bounds__(128) kv_compress_tile_kernel(CompressJobs jobs
             if (row < rows) {
                 if ((sub % glanes) == 0) job.scales[row * ng + sub / glanes] = scale;
                 if constexpr (BITS == 8) {
-                    const uint32_t lo = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
-                                                    __byte_perm(q[2], q[3], 0x0040), 0x5410);
-                    const uint32_t hi = __byte_perm(__byte_perm(q[4], q[5], 0x0040),
-                                                    __byte_perm(q[6], q[7], 0x0040), 0x5410);
-                    reinterpret_cast<uint2*>((uint8_t*)job.codes + row * DE)[sub] = make_uint2(lo, hi);
+                    uint32_t lo = __byte_perm(__byte_perm(q[0], q[1], 0x0040),
+                                              __byte_perm(q[2], q[3], 0x0040), 0x5410);
+                    uint32_t hi = __byte_perm(__byte_perm(q[4], q[5], 0x0040),
+                                              __byte_perm(q[6], q[7], 0x0040), 0x5410);
+                    // byte e holds channel (e + rot) & 7: rotate left by rot bytes
+                    const uint64_t w = ((uint64_t)hi << 32) | lo;
+                    const uint64_t r = rot ? (w << (8 * rot)) | (w >> (64 - 8 * rot)) : w;
+                    reinterpret_cast<uint2*>((uint8_t*)job.codes + row * DE)[sub] =
+                        make_uint2((uint32_t)r, (uint32_t)(r >> 32));
                 } else {
                     uint32_t w = 0;
 #pragma unroll
                     for (int e = 0; e < 8; ++e) w |= (q[e] & 0xFu) << (4 * e);
+                    // nibble e holds channel (e + rot) & 7: rotate left by rot nibbles
+                    w = rot ? (w << (4 * rot)) | (w >> (32 - 4 * rot)) : w;
                     reinterpret_cast<uint32_t*>((uint8_t*)job.codes + row * (DE / 2))[sub] = w;
                 }
             }
