@@ -71,11 +71,12 @@ struct TileCfgB {                                       // TB-byte stages
     static constexpr int BYTES = TILE * DC * 2;
 };
 constexpr int kCompressStages = 2;
-// 8 KB stages: more CTAs per SM beat deeper rings (C2, 11 layers x K/V, measured:
-// 8 KB x 2 = 4.75-4.80 TB/s; 16 KB x 2 4.61; 8 KB x 3 4.70; 4 KB x 2 4.22; 16 KB x 4 3.33).
-// Per-warp stage release through an "empty" mbarrier instead of the CTA barrier measured
-// slower (8 KB x 2 4.52, 8 KB x 3 4.43, 4 KB x 4 3.83 TB/s; profiles/r01s6_k3_release_ab.txt).
-constexpr int kCompressTileBytes = 8192;
+// 16 KB x 2 stages.  Round 1 (before the bank-conflict-free gather order) measured 8 KB x 2
+// best (4.75-4.80 TB/s; 16 KB x 2 4.61); with the rotated gather (round 2, C2 22 jobs / C4
+// 32k 22 jobs, fraction of the 6551 GB/s peak): 8 KB x 2 0.73 / 0.82, 8 KB x 3 0.73 / 0.80,
+// 16 KB x 2 0.77-0.79 / 0.87-0.88, 16 KB x 3 0.73 / 0.80, 16 KB x 4 0.64 / 0.69, 32 KB x 2
+// 0.69 / 0.75 (profiles/r02_megakernel_experiments.txt has the log).
+constexpr int kCompressTileBytes = 16384;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
