@@ -1615,7 +1615,7 @@ int ekv_session_trace_step(ekv_session_t s, uint64_t* out, int capacity, int* n_
     return guard([&] {
         require(s && out && n_out, "null argument");
         require(use_mega(s), "trace: the persistent decode kernel is not active");
-        const int G = mega_grid(s->model->cfg.num_heads, s->model->ctx->num_sms);
+        const int G = mega_grid(s->mega, s->model->ctx->num_sms);
         const int L = s->model->cfg.num_layers;
         const int n = 16 * (L + 1) * G;
         require(capacity >= n, "trace: need " + std::to_string(n) + " entries");

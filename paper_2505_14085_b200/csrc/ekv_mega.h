@@ -49,7 +49,7 @@ struct MegaArgs {
 bool mega_supported(int L, int H, int D, int S, int h);
 size_t mega_smem_bytes(int D);
 int mega_wo_box_rows(int D);
-int mega_grid(int H, int num_sms);  // CTAs of the persistent kernel (a multiple of H)
+int mega_grid(const MegaArgs& a, int num_sms);  // CTAs of the persistent kernel (a multiple of H)
 void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st);
 CUtensorMap make_map_2d_bf16(const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
                              uint32_t box_rows);

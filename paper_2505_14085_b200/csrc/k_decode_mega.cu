@@ -36,6 +36,7 @@
 // data are neighbours, and each CTA touches at most two heads per phase.
 #include <math_constants.h>
 
+#include <cmath>
 #include <cstdlib>
 
 #include "ekv_common.cuh"
@@ -1291,11 +1292,23 @@ static void launch_d(const MegaArgs& a, int grid, int kc, cudaStream_t st) {
     }
 }
 
-// Grid = the largest multiple of the head count that fits the SMs: every head then
-// gets the same number of attention CTAs, so no head's merge waits for a CTA that
-// carries a larger share (C2, 32 heads: 128 CTAs = 3149 tok/s vs 148 CTAs = 2840).
-int mega_grid(int H, int num_sms) {
+// Grid = a multiple of the head count (every head gets the same number of attention
+// CTAs, so no head's merge waits for a CTA that carries a larger share; C2, 32 heads:
+// 128 CTAs = 3149 tok/s vs 148 CTAs = 2840), at most the SMs, and no more CTAs than the
+// token's bytes need: below ~64 KB per CTA the dataflow's per-CTA synchronisation costs
+// more than the extra bandwidth brings (configs[0], 4 layers h = 256, ~4 MB per token:
+// 64 CTAs 30.3 k tok/s vs 144 CTAs 23.2 k).
+int mega_grid(const MegaArgs& a, int num_sms) {
+    const int H = a.H;
     int g = H <= num_sms ? num_sms / H * H : num_sms;
+    double bytes = 0.0;
+    const double h = (double)a.H * a.D;
+    for (int l = 0; l < a.L; ++l) {
+        const int f = a.layer[l].fmt;
+        bytes += 8.0 * h * h + 2.0 * a.H * a.S * (f == 16 ? 2.0 * a.D : a.D * f / 8.0 + 4.0);
+    }
+    const int want = (int)std::ceil(bytes / (64.0 * 1024.0) / H) * H;
+    if (H <= num_sms && want >= H && want < g) g = want;
     if (const char* e = getenv("EKV_MEGA_GRID")) {  // experiments
         const int v = atoi(e);
         if (v >= 1 && v < g) g = v;
@@ -1304,7 +1317,7 @@ int mega_grid(int H, int num_sms) {
 }
 
 void launch_decode_mega(const MegaArgs& a, int num_sms, cudaStream_t st) {
-    num_sms = mega_grid(a.H, num_sms);
+    num_sms = mega_grid(a, num_sms);
     require(num_sms <= 160, "decode megakernel: at most 160 SMs", EKV_EUNSUPPORTED);
     require(a.H * a.D >= num_sms, "decode megakernel: hidden size below the SM count", EKV_EUNSUPPORTED);
     const int kc = a.H * a.D / 256;
