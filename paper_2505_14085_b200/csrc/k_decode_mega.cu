@@ -38,6 +38,9 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "ekv_common.cuh"
 #include "ekv_kernels.h"
@@ -191,6 +194,60 @@ __device__ __forceinline__ float ll_spin(const uint64_t* p, unsigned long long w
         } while ((uint32_t)(w >> 32) != tag);
     }
     return __uint_as_float((uint32_t)w);
+}
+
+// ---------------------------------------------------------------------------
+// Head clusters (CL kernels).  When every head has the same number of CTAs
+// (G = cs * H, cs <= 8), the CTAs of one head form a thread-block cluster and
+// the two intra-head exchanges -- A's q/k/v rows to B, B's partials to the
+// merge -- go through distributed shared memory: st.async into every cluster
+// CTA's buffer, each store counting its bytes on that CTA's mbarrier, which
+// the CTA armed with the layer's byte count (arrive.expect_tx, one arrival).
+// No global round trip, no polling, no fence.  The buffers are single: a CTA
+// rewrites a peer's buffer for layer l+1 only after that layer's input
+// exists, i.e. after every CTA (the peer included) finished reading layer l's
+// and re-armed its barrier.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// the same shared-memory offset in cluster CTA `rank`
+__device__ __forceinline__ uint32_t cl_map(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+// an asynchronous 4-byte store into a cluster CTA's shared memory that counts
+// its bytes on that CTA's mbarrier (complete_tx): no fence, no arrive
+__device__ __forceinline__ void cl_st_async(uint32_t addr, float v, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(addr), "f"(v),
+                 "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void cl_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(saddr(b)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > 4000000000ll) __trap();
+    }
+}
+__device__ __forceinline__ void cl_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -416,6 +473,9 @@ struct Smem {
     OPlan op;                     // a per-thread copy would live in local memory)
     int hfirst[160], hlast[160];  // contributing CTA range of each head's attention
     int ch0[160];                 // first attention head of each CTA (-1: idle CTA)
+    uint64_t qkv_bar, part_bar;   // CL: head cluster's q/k/v rows, attention partials arrived
+    float cpart[8][D + 2];        // CL: (m, l, o) partial of each cluster CTA
+    float kvf[2 * D];             // CL: this step's k | v row of the cluster's head (bf16 values)
     volatile long long prod_k[2]; // stages issued so far by each producer (for the prefetcher)
     int tphase;                   // diagnostics: phase of the ring waits being counted
     unsigned long long twait[3];  // diagnostics: ring-wait cycles of A, B, C (sum over warps)
@@ -673,9 +733,9 @@ __device__ __forceinline__ void stage_x(const MegaArgs& a, Smem<D>& sm, int h, i
 // from the ring, x from shared memory into registers once (lane holds
 // x[c*256 + lane*8 + e]).  q goes out as tagged words; k and v are rounded to
 // bf16, appended to the user cache, and go out as tagged words too.
-template <int D, int KC, bool TR>
+template <int D, int KC, bool TR, bool CL>
 __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm, Cursor& cu,
-                                         Split rows, int h, int ulen, uint32_t tag) {
+                                         Split rows, int h, int ulen, uint32_t tag, uint32_t cs) {
     const int lane = threadIdx.x & 31;
     f2x xr[KC * 4];  // x pairs {x[2k], x[2k+1]} of this lane's 8 elements per chunk
 #pragma unroll
@@ -734,12 +794,23 @@ __device__ __forceinline__ void proj_qkv(const MegaArgs& a, const MegaLayer& ly,
                 const int v = r + i0 + lane;
                 const int head = v / (3 * D), rem = v - head * 3 * D, part = rem / D;
                 if (part == 0) {
-                    ll_st(a.ll_qkv + v, yv, tag);
+                    if constexpr (CL) {
+                        const uint32_t dst = saddr(&sm.qs[0][rem]), bar = saddr(&sm.qkv_bar);
+                        for (uint32_t rk = 0; rk < cs; ++rk) cl_st_async(cl_map(dst, rk), yv, cl_map(bar, rk));
+                    } else {
+                        ll_st(a.ll_qkv + v, yv, tag);
+                    }
                 } else {
                     const uint16_t b = f32_to_bf16_bits(yv);
                     uint16_t* dst = part == 1 ? ly.uk : ly.uv;
                     dst[((size_t)head * a.cap + ulen) * D + (rem - part * D)] = b;
-                    ll_st(a.ll_qkv + v, __uint_as_float((uint32_t)b << 16), tag);
+                    if constexpr (CL) {
+                        const uint32_t sd = saddr(&sm.kvf[rem - D]), bar = saddr(&sm.qkv_bar);
+                        const float bv = __uint_as_float((uint32_t)b << 16);
+                        for (uint32_t rk = 0; rk < cs; ++rk) cl_st_async(cl_map(sd, rk), bv, cl_map(bar, rk));
+                    } else {
+                        ll_st(a.ll_qkv + v, __uint_as_float((uint32_t)b << 16), tag);
+                    }
                 }
             }
         }
@@ -864,17 +935,20 @@ __device__ __forceinline__ void park_warp_state(Smem<D>& sm, OState<Fmt<D, FMT>:
 // B: attention of the CTA's pieces.  q and this step's K/V row of each head
 // arrive as tagged words from A; the context and earlier user rows come
 // through the ring.  Ends with one tagged (m, l, o) partial per piece.
-template <int D, int FMT, bool TR>
+template <int D, int FMT, bool TR, bool CL>
 __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLayer& ly, Smem<D>& sm,
                                                 Cursor& cu, const AttnPlan& pl, int c, int ulen,
-                                                int l, uint32_t tag) {
+                                                int l, uint32_t tag, uint32_t cs) {
     using F = Fmt<D, FMT>;
     using FU = Fmt<D, 16>;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ng = FMT == 16 ? 0 : D / ly.group;
     const int cap = att_stage_rows(F::ROW, ng);
     const int ucap = att_stage_rows(D * 2, 0);
-    {
+    if constexpr (CL) {
+        cl_wait(&sm.qkv_bar, (uint32_t)l & 1u);  // the head's q and k | v rows are in sm.qs / kvf
+        if (threadIdx.x == 0 && l + 1 < a.L) mbar_expect(&sm.qkv_bar, 3 * D * 4);  // arm layer l+1
+    } else {
         constexpr int W = (2 * 3 * D + NCW * 32 - 1) / (NCW * 32);
         unsigned long long w[W];
         const int nw = pl.n * 3 * D;
@@ -895,8 +969,8 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                 else sm.nv[i][j - 2 * D] = (uint16_t)(__float_as_uint(v) >> 16);
             }
         }
+        consumers_sync();
     }
-    consumers_sync();
     stamp(a, TR, l, 3);
     for (int i = 0; i < pl.n; ++i) {
         const Piece& pc = pl.p[i];
@@ -945,9 +1019,17 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
                 ring_release(sm, cu.k + j);
             }
             cu.k += nsu;
-            if (ulen >= pc.u0 && ulen < pc.u1 && warp == (int)((cu.k + i) % NCW))
+            if (ulen >= pc.u0 && ulen < pc.u1 && warp == (int)((cu.k + i) % NCW)) {
+                if constexpr (CL) {
+                    for (int e = lane; e < D; e += 32) {
+                        sm.nk[i][e] = (uint16_t)(__float_as_uint(sm.kvf[e]) >> 16);
+                        sm.nv[i][e] = (uint16_t)(__float_as_uint(sm.kvf[D + e]) >> 16);
+                    }
+                    __syncwarp();
+                }
                 attend_rows_mk<D, 16, 1>((const uint8_t*)sm.nk[i], (const uint8_t*)sm.nv[i], nullptr,
                                          nullptr, 0, D, 1, qu, su);
+            }
             park_warp_state<D, 16>(sm, su, i, FMT == 16 ? 0 : 1);
             if (FMT == 16 && lane == 0) sm.ws_l[i][1][warp] = 0.0f;
         }
@@ -958,6 +1040,37 @@ __device__ __forceinline__ void attention_phase(const MegaArgs& a, const MegaLay
     // computes the 2*NCW rescale factors itself (one lane per state, shuffled to
     // every lane) -- no second block barrier, no serial warp-0 step.
     static_assert(2 * NCW <= 32, "one lane per (kind, warp) state");
+    if constexpr (CL) {
+        // one piece (or none: an empty partial, l = 0) into every cluster CTA's cpart[rank]
+        static_assert(D <= NCW * 32, "one fold pass");
+        if (warp * 32 < D) {
+            const int cix = warp * 32 + lane;
+            const int k = lane / NCW, w = lane % NCW;
+            const bool on = pl.n > 0 && lane < 2 * NCW && sm.ws_l[0][k][w] > 0.0f;
+            const float m = on ? sm.ws_m[0][k][w] : -CUDART_INF_F;
+            const float M = warp_max(m);
+            const float sc = on ? exp2f((m - M) * kLog2e) : 0.0f;
+            const float Ls = warp_sum(on ? sm.ws_l[0][k][w] * sc : 0.0f);
+            float o0 = 0.0f, o1 = 0.0f;
+            if (pl.n > 0) {
+#pragma unroll
+                for (int ww = 0; ww < NCW; ++ww) {
+                    o0 = fmaf(sm.ws_o[0][0][ww][cix], __shfl_sync(0xffffffffu, sc, ww), o0);
+                    o1 = fmaf(sm.ws_o[0][1][ww][cix], __shfl_sync(0xffffffffu, sc, NCW + ww), o1);
+                }
+            }
+            const uint32_t dst = saddr(&sm.cpart[cl_rank()][0]), bar = saddr(&sm.part_bar);
+            for (uint32_t rk = 0; rk < cs; ++rk) {
+                const uint32_t rd = cl_map(dst, rk), rb = cl_map(bar, rk);
+                if (warp == 0 && lane == 0) {
+                    cl_st_async(rd, M, rb);
+                    cl_st_async(rd + 4, Ls, rb);
+                }
+                cl_st_async(rd + 4 * (2 + cix), o0 + o1, rb);
+            }
+        }
+        return;
+    }
     for (int t0 = warp * 32; t0 < pl.n * D; t0 += NCW * 32) {
         const int i = t0 / D, cix = t0 - i * D + lane;
         const int k = lane / NCW, w = lane % NCW;
@@ -1053,6 +1166,28 @@ __device__ __forceinline__ void merge_heads(const MegaArgs& a, Smem<D>& sm, cons
         consumers_sync();
     }
     if (mine) sm.os[slot][col] = O / Ls;
+}
+
+// C, part 1 on a head cluster: the cs partials arrived in this CTA's cpart
+// (every cluster CTA attends the cluster's head, and is this CTA's W_o head).
+template <int D>
+__device__ __forceinline__ void merge_cluster(Smem<D>& sm, int l, int L, uint32_t cs) {
+    cl_wait(&sm.part_bar, (uint32_t)l & 1u);
+    if (threadIdx.x == 0 && l + 1 < L) mbar_expect(&sm.part_bar, cs * (D + 2) * 4);  // arm layer l+1
+    const int col = threadIdx.x;
+    if (col < D) {
+        float M = -CUDART_INF_F;
+        for (uint32_t j = 0; j < cs; ++j)
+            if (sm.cpart[j][1] > 0.0f) M = fmaxf(M, sm.cpart[j][0]);
+        float Ls = 0.0f, O = 0.0f;
+        for (uint32_t j = 0; j < cs; ++j) {
+            const float lj = sm.cpart[j][1];
+            const float sc = lj > 0.0f ? exp2f((sm.cpart[j][0] - M) * kLog2e) : 0.0f;
+            Ls += lj * sc;
+            O += sm.cpart[j][2 + col] * sc;
+        }
+        sm.os[0][col] = O / Ls;
+    }
 }
 
 // C, part 2: rows [n0, n1) of W_o[:, head] (2-D boxes from the ring, RPS rows of
@@ -1159,7 +1294,7 @@ __device__ __forceinline__ void plan_merge(const MegaArgs& a, Smem<D>& sm, int G
     consumers_sync();
 }
 
-template <int D, int KC, bool TR>
+template <int D, int KC, bool TR, bool CL>
 __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_constant__ MegaArgs a) {
     // (declared aligned and cast directly, so every access compiles to LDS/STS:
     // an integer round trip would lose the address space and give generic loads)
@@ -1180,13 +1315,23 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
         sm.prod_k[0] = sm.prod_k[1] = 0;
         sm.pl = plan_attention(c, G, a.H, a.S, ulen + 1);
         sm.op = plan_outproj(c, G, a.H, a.H * D);
+        if (CL) {  // one arrival (the arming) + the layer's bytes
+            mbar_init(&sm.qkv_bar, 1);
+            mbar_init(&sm.part_bar, 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (CL) {
+            mbar_expect(&sm.qkv_bar, 3 * D * 4);
+            mbar_expect(&sm.part_bar, cl_size() * (D + 2) * 4);
+        }
     }
     __syncthreads();
+    if (CL) cl_sync_all();  // every cluster CTA's barriers exist before the first remote arrive
     if (warp >= NCW) {  // producers
         if (lane == 0) produce<D, false, TR>(a, sm, c, G, ulen, warp - NCW);
         return;
     }
+    const uint32_t cs = CL ? cl_size() : 1u;
     Cursor cu;
     const Split qrows = rows_of(c, G, 3 * h), elems = rows_of(c, G, h);
     const AttnPlan& pl = sm.pl;
@@ -1204,16 +1349,17 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
         // ---- A: QKV (input transform fused at layer 0) ----
         stage_x<D>(a, sm, h, l, tag - 1u, ulen);
         stamp(a, TR, l, 1);
-        proj_qkv<D, KC, TR>(a, ly, sm, cu, qrows, h, ulen, tag);
+        proj_qkv<D, KC, TR, CL>(a, ly, sm, cu, qrows, h, ulen, tag, cs);
         stamp(a, TR, l, 2);
         set_tphase(TR, sm, 1);
         // ---- B: attention ----
-        if (ly.fmt == 16) attention_phase<D, 16, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
-        else if (ly.fmt == 8) attention_phase<D, 8, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
-        else attention_phase<D, 4, TR>(a, ly, sm, cu, pl, c, ulen, l, tag);
+        if (ly.fmt == 16) attention_phase<D, 16, TR, CL>(a, ly, sm, cu, pl, c, ulen, l, tag, cs);
+        else if (ly.fmt == 8) attention_phase<D, 8, TR, CL>(a, ly, sm, cu, pl, c, ulen, l, tag, cs);
+        else attention_phase<D, 4, TR, CL>(a, ly, sm, cu, pl, c, ulen, l, tag, cs);
         stamp(a, TR, l, 4);
         // ---- C: merge + output-projection column blocks of this CTA's heads ----
-        merge_heads<D>(a, sm, op, tag);
+        if constexpr (CL) merge_cluster<D>(sm, l, a.L, cs);
+        else merge_heads<D>(a, sm, op, tag);
         consumers_sync();
         stamp(a, TR, l, 5);
         set_tphase(TR, sm, 2);
@@ -1254,9 +1400,47 @@ bool mega_supported(int L, int H, int D, int S, int h) {
     return true;
 }
 
-template <int D, int KC, bool TR>
-static void launch_dkt(const MegaArgs& a, int grid, cudaStream_t st) {
-    auto fn = mk::decode_step_kernel<D, KC, TR>;
+// Head clusters (the CL kernels): every head has cs = grid / H CTAs, cs in [2, 8],
+// and the device can keep all grid / cs clusters resident at once (the dataflow
+// spins on its peers, so a cluster that is not scheduled would hang the step).
+static int mega_cluster(const void* fn, int grid, int H, size_t smem) {
+    if (grid % H != 0) return 1;
+    const int cs = grid / H;
+    if (cs < 2 || cs > 8) return 1;
+    if (const char* e = getenv("EKV_MEGA_CLUSTER"))  // experiments: 0 = off
+        if (atoi(e) == 0) return 1;
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, int> fits;
+    int dev = 0;
+    EKV_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(dev, fn, cs * 1000 + grid);
+    auto it = fits.find(key);
+    if (it == fits.end()) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(mk::THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        it = fits.emplace(key, n * cs >= grid ? cs : 1).first;
+    }
+    return it->second;
+}
+
+template <int D, int KC, bool TR, bool CL>
+static void launch_dkt(const MegaArgs& a, int grid, int cs, cudaStream_t st) {
+    auto fn = mk::decode_step_kernel<D, KC, TR, CL>;
     const size_t smem = mega_smem_bytes(D);
     ensure_smem_attr((const void*)fn, (int)smem);
     cudaLaunchConfig_t cfg{};
@@ -1264,11 +1448,15 @@ static void launch_dkt(const MegaArgs& a, int grid, cudaStream_t st) {
     cfg.blockDim = dim3(mk::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;  // co-residency of every CTA (the dataflow waits)
     at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = CL ? cs : 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CL ? 2 : 1;
     EKV_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
 }
 
@@ -1276,8 +1464,16 @@ static void launch_dkt(const MegaArgs& a, int grid, cudaStream_t st) {
 // instantiation, so the production kernel carries none of their code
 template <int D, int KC>
 static void launch_dk(const MegaArgs& a, int grid, cudaStream_t st) {
-    if (a.trace) launch_dkt<D, KC, true>(a, grid, st);
-    else launch_dkt<D, KC, false>(a, grid, st);
+    const size_t smem = mega_smem_bytes(D);
+    ensure_smem_attr((const void*)mk::decode_step_kernel<D, KC, false, true>, (int)smem);  // (the query)
+    const int cs = mega_cluster((const void*)mk::decode_step_kernel<D, KC, false, true>, grid, a.H, smem);
+    if (cs > 1) {
+        if (a.trace) launch_dkt<D, KC, true, true>(a, grid, cs, st);
+        else launch_dkt<D, KC, false, true>(a, grid, cs, st);
+    } else {
+        if (a.trace) launch_dkt<D, KC, true, false>(a, grid, 1, st);
+        else launch_dkt<D, KC, false, false>(a, grid, 1, st);
+    }
 }
 
 template <int D>

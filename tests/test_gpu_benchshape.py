@@ -94,6 +94,16 @@ def test_k8_decode_at_c2_matches_oracle(ek, ctx, oracle, c2):
                                          teacher=teacher, user_kv_bf16=True)
     errs = [normwise(pre[r], wp[r]) for r in range(U)] + [normwise(steps[t], ws[t]) for t in range(T)]
     assert max(errs) <= TOL, errs
+    # 4 CTAs per head = one thread-block cluster per head (DSMEM q/k/v + partial
+    # exchange); the global tagged-word exchange computes the identical bits
+    sess.reset()
+    import os
+    os.environ["EKV_MEGA_CLUSTER"] = "0"
+    try:
+        pre_n, steps_n = ek.collaborative_decode(sess, ue, T)
+    finally:
+        del os.environ["EKV_MEGA_CLUSTER"]
+    assert np.array_equal(steps_n, steps) and np.array_equal(pre_n, pre)
     # the per-layer-kernel graph path agrees with the persistent kernel at this shape
     sess.reset()
     assert sess.set_decode_path("graph") == "graph"

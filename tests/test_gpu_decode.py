@@ -9,6 +9,8 @@ cache is rounded to bf16 as the B200 stores it (oracle option user_kv_bf16), and
 each step is teacher-forced with the GPU's own input row.
 Bar: normwise max|gpu-ref|/max|ref| <= 1e-3 per output row, fp32 outputs.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -142,6 +144,44 @@ def test_collaborative_decode_matches_oracle(ek, ctx, oracle, formats, S, U, T, 
         assert np.array_equal(out.cpu().numpy(), pre)
     st = sess.decode(T).cpu().numpy()
     assert np.array_equal(st, steps)
+    if got_path == "mega":  # head clusters (when the grid has 2-8 CTAs per head) vs global exchange
+        sess.reset()
+        os.environ["EKV_MEGA_CLUSTER"] = "0"
+        try:
+            if U:
+                sess.forward(torch.from_numpy(ue32).cuda())
+            assert np.array_equal(sess.decode(T).cpu().numpy(), steps)
+        finally:
+            del os.environ["EKV_MEGA_CLUSTER"]
+
+
+@pytest.mark.parametrize("grid", [8, 16, 32, 36])
+def test_mega_head_clusters_bit_identical(ek, ctx, oracle, grid):
+    """The persistent kernel with 2 / 4 / 8 CTAs per head (thread-block clusters,
+    DSMEM exchange) and with 9 (no cluster: global tagged words) computes the same
+    bits as the global exchange, and matches the oracle."""
+    L, H, d, S, U, T = 4, 4, 64, 1024, 3, 3
+    h = H * d
+    bits, f64 = host_bf16_model(oracle, L, H, d, 512 + S, seed=91)
+    model = upload_model(ek, ctx, bits, L, H, d, 512 + S)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, [16, 8, 16, 8], seed=93)
+    ue32 = oracle.generate_embeddings(45, U, h).astype(np.float32)
+    runs = []
+    os.environ["EKV_MEGA_GRID"] = str(grid)
+    try:
+        for cl in ("1", "0"):
+            os.environ["EKV_MEGA_CLUSTER"] = cl
+            sess = ek.Session(model, kvc, U + T)
+            assert sess.set_decode_path("mega") == "mega"
+            runs.append(ek.collaborative_decode(sess, ue32, T))
+    finally:
+        del os.environ["EKV_MEGA_GRID"], os.environ["EKV_MEGA_CLUSTER"]
+    (pre, steps), (pre0, steps0) = runs
+    assert np.array_equal(steps, steps0) and np.array_equal(pre, pre0)
+    teacher = np.vstack([pre[-1:], steps[:-1]]).astype(np.float64)
+    _, want = oracle.collaborative_decode(f64, ck, cv, ue32.astype(np.float64), T, teacher=teacher,
+                                          user_kv_bf16=True)
+    assert max(normwise(steps[t], want[t]) for t in range(T)) <= TOL
 
 
 def test_collaborative_decode_errors(ek, ctx, oracle):
