@@ -493,8 +493,7 @@ void session_alloc(ekv_session_s* s) {
             a.wo_row0 = 3 * h;
             a.wo_layer_rows = 4 * h;
             a.prefetch_stages = 0;
-            if (const char* e = getenv("EKV_MEGA_PREFETCH")) a.prefetch_stages = atoi(e);
-            if (a.prefetch_stages > 0 && a.prefetch_stages < 4) a.prefetch_stages = 4;
+            a.prefetch_ctx = 1;
             for (int l = 0; l < L; ++l) {
                 const ekv_segment& sg = s->kv->seg[l];
                 MegaLayer& ly = a.layer[l];
@@ -508,6 +507,25 @@ void session_alloc(ekv_session_s* s) {
                 ly.uk = s->uk + (size_t)l * s->ukv_layer();
                 ly.uv = s->uv + (size_t)l * s->ukv_layer();
             }
+            // L2 prefetch warp 16 stages (~192 KB per CTA) ahead of the ring while a CTA's
+            // context share per layer is small: the phases then leave HBM idle between
+            // them (C2: 3439 -> 3617 tok/s; S = 8192 +3%), but once the context stream
+            // dominates, the early requests only compete with the demand loads (S = 16384
+            // -7%, C4 -16%): profiles/r02_megakernel_experiments.txt
+            {
+                const int grid = mega_grid(a, m->ctx->num_sms);
+                const double per = std::ceil((double)a.S * H / grid);  // context rows per CTA
+                double most = 0.0;
+                for (int l = 0; l < L; ++l) {
+                    const MegaLayer& ly = a.layer[l];
+                    const double rb = ly.fmt == 16 ? 2.0 * D : D * ly.fmt / 8.0 + 4.0 * D / ly.group;  // + scales
+                    most = std::max(most, per * 2.0 * rb);
+                }
+                a.prefetch_stages = most <= 640.0 * 1024.0 ? 16 : 0;
+            }
+            if (const char* e = getenv("EKV_MEGA_PREFETCH")) a.prefetch_stages = atoi(e);
+            if (const char* e = getenv("EKV_MEGA_PREFETCH_CTX")) a.prefetch_ctx = atoi(e);
+            if (a.prefetch_stages > 0 && a.prefetch_stages < 4) a.prefetch_stages = 4;
         }
     }
     EKV_CUDA(cudaMemsetAsync(s->counters, 0, sizeof(unsigned) * s->pchunk * m->cfg.num_heads, ast));

@@ -41,8 +41,8 @@ struct MegaArgs {
     unsigned long long* trace;  // optional [L][G][8] phase stamps + [G] start (ns)
     CUtensorMap wo_map;    // 2-D map over the weight buffer: rows [L*4h] x cols [h], box {D, rows}
     int wo_row0, wo_layer_rows;  // row of layer l's W_o = wo_row0 + l*wo_layer_rows
-    int prefetch_stages;   // L2 prefetch distance ahead of the ring (stages; 0 = off, the
-                           // default: measured slower, profiles/r01_megakernel_experiments.txt)
+    int prefetch_stages;   // L2 prefetch warp distance ahead of the ring, in stages (0 = off; default 16)
+    int prefetch_ctx;      // the prefetch warp also covers the context stages (else weights only)
     MegaLayer layer[kMegaMaxLayers];
 };
 

@@ -52,7 +52,7 @@ namespace mk {
 
 constexpr int NCW = 8;                  // consumer warps
 constexpr int NPW = 2;                  // producer warps (one issuing thread each)
-constexpr int THREADS = (NCW + NPW) * 32;
+constexpr int THREADS = (NCW + NPW + 1) * 32;  // + the L2 prefetch warp
 constexpr int NST = 16;                 // ring stages (a multiple of NCW: see the ring protocol)
 constexpr int STAGE = 12 * 1024;        // bytes per stage
 constexpr int UNIT = 16;                // attention rows per partition unit
@@ -604,7 +604,7 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
             const uint8_t* cv = ly.cv + (size_t)pc.head * a.S * row_b;
             #pragma unroll 1
             for (int r = pc.c0; r < pc.c1; r += cap) {
-                if (pr.mine()) {
+                if (pr.mine() && (!PF || a.prefetch_ctx)) {
                     const int n = min(cap, pc.c1 - r);
                     const uint32_t kb = n * row_b, sb = n * ng * 4;
                     uint8_t* dst = pr.acquire(2 * kb + 2 * sb);
@@ -621,7 +621,7 @@ __device__ void produce(const MegaArgs& a, Smem<D>& sm, int c, int G, int ulen, 
             const int ue = user_static_end(pc, ulen);
             #pragma unroll 1
             for (int r = pc.u0; r < ue; r += ucap) {
-                if (pr.mine()) {
+                if (pr.mine() && !PF) {  // (the user rows are L2-resident: written by earlier steps)
                     const int n = min(ucap, ue - r);
                     const size_t base = ((size_t)pc.head * a.cap + r) * D;
                     uint8_t* dst = pr.acquire((uint32_t)n * D * 4);
@@ -1328,7 +1328,10 @@ __global__ void __launch_bounds__(THREADS, 1) decode_step_kernel(const __grid_co
     __syncthreads();
     if (CL) cl_sync_all();  // every cluster CTA's barriers exist before the first remote arrive
     if (warp >= NCW) {  // producers
-        if (lane == 0) produce<D, false, TR>(a, sm, c, G, ulen, warp - NCW);
+        if (lane == 0) {
+            if (warp < NCW + NPW) produce<D, false, TR>(a, sm, c, G, ulen, warp - NCW);
+            else if (a.prefetch_stages > 0) produce<D, true, TR>(a, sm, c, G, ulen, 0);
+        }
         return;
     }
     const uint32_t cs = CL ? cl_size() : 1u;
