@@ -61,6 +61,8 @@ def main(rep, obj, fn, src):
     reasons = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
     base = int(rows[2][ai], 16)
     agg = collections.defaultdict(collections.Counter)
+    inst = collections.Counter()
+    ii = h.index("Instructions Executed")
     tot = 0
     for r in rows[2:]:
         try:
@@ -73,6 +75,7 @@ def main(rep, obj, fn, src):
             if any(lo <= x <= hi for x in ch):
                 ph = name
                 break
+        inst[ph] += int(r[ii] or 0)
         for c in reasons:
             v = int(r[h.index(c)] or 0)
             agg[ph][c] += v
@@ -81,7 +84,7 @@ def main(rep, obj, fn, src):
     for ph, cnt in sorted(agg.items(), key=lambda kv: -sum(kv[1].values())):
         s = sum(cnt.values())
         top = ", ".join(f"{k[6:]} {100 * v / s:.0f}%" for k, v in cnt.most_common(5) if v)
-        print(f"{ph:16s} {s:6d} {100 * s / tot:5.1f}%  | {top}")
+        print(f"{ph:16s} {s:6d} {100 * s / tot:5.1f}%  warp-inst {inst[ph]:>10d} | {top}")
 
 
 if __name__ == "__main__":
