@@ -58,6 +58,10 @@ struct BatchCtxAttn {
 
 struct BatchUserMerge {
     int B, H, D, L, layer, cap, KS, n_qkv, nsplit;
+    // prefill (R rows of ONE session, requires qfin): item b is row b of the chunk, whose
+    // k / v sit at cache row user_len + row0 + b of the single cache at uk / uv (b-stride 0);
+    // causal: row b attends to the cache rows before it and to itself
+    int prefill, row0;
     const float* qkv;      // [KS][B][3h]
     const float* qfin;     // non-null: q from qfin [B][h], k / v already appended by K10
     const float* part;     // context partials (nsplit may be 0)

@@ -187,17 +187,19 @@ void tc_qkv_rows(ekv_session_s* s, int l, const float* in, int R, int row0, cons
 }
 
 void tc_out_rows(ekv_session_s* s, int l, const float* x, float* y, float* y_hist, int R, int row0,
-                 const CUtensorMap& pmap_x, cudaStream_t st) {
+                 const CUtensorMap& pmap_x, cudaStream_t st, bool operand_ready = false) {
     const int h = s->model->h;
-    BatchXprep xp{};
-    xp.mode = 1;
-    xp.B = R;
-    xp.h = h;
-    xp.KS = 1;
-    xp.part = x;
-    xp.state = s->state;
-    xp.xhl = s->pxhl;
-    launch_batch_xprep(xp, st);
+    if (!operand_ready) {  // else the attention already wrote the bf16 hi / lo operand
+        BatchXprep xp{};
+        xp.mode = 1;
+        xp.B = R;
+        xp.h = h;
+        xp.KS = 1;
+        xp.part = x;
+        xp.state = s->state;
+        xp.xhl = s->pxhl;
+        launch_batch_xprep(xp, st);
+    }
     const int ks = R <= 8 ? s->pKSo : batch_proj_splits(h, h, R, s->model->ctx->num_sms);
     launch_batch_proj(s->pmap_w, l * 4 * h + 3 * h, h, h, pmap_x, R, ks, s->ppart, st);
     PrefillFinish f{};
@@ -216,6 +218,81 @@ void tc_out_rows(ekv_session_s* s, int l, const float* x, float* y, float* y_his
 CUtensorMap tc_operand_map(ekv_session_s* s, int R) {
     return make_map_3d_bf16(s->pxhl, (uint64_t)s->model->h, (uint64_t)R, 2, 64, (uint32_t)batch_proj_bn(R),
                             CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Tensor maps of context layer l for K10; false when K10 cannot read the layer
+// (head_dim != 64, int4, or int8 with more than one scale group per row).
+bool layer_ctx_maps(const ekv_kvctx_s* kv, int l, int H, int D, BatchCtxMaps& mp) {
+    const ekv_segment& sg = kv->seg[l];
+    mp.fmt = sg.format;
+    if (sg.S == 0) return true;
+    if (!batch_ctx_supported(D, sg.format, sg.group)) return false;
+    const uint64_t rows = (uint64_t)H * sg.S;
+    if (sg.format == EKV_KV_BF16) {
+        mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+        mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
+                           CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+        mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+        mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+        mp.ks = make_map_1d(sg.k_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
+        mp.vs = make_map_1d(sg.v_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
+    }
+    return true;
+}
+
+// Attention of R >= 2 prefill rows of one session on the tensor cores: K10 over
+// the context (the rows play K10's sessions: every row attends the same S
+// context rows, read once for all R rows instead of once per row), then K11 in
+// prefill mode for the causal user segment + the Eq. 5 merge, writing the
+// output projection's bf16 hi / lo operand.  q comes from the QKV finish
+// (s->q), k / v are already in the user cache.  False: the layer needs K4.
+bool tc_attn_rows(ekv_session_s* s, int l, int R, int row0, cudaStream_t st) {
+    ekv_model_s* m = s->model;
+    const int H = m->cfg.num_heads, D = d_of(m), h = m->h;
+    const ekv_segment& sg = s->kv->seg[l];
+    BatchCtxMaps mp{};
+    if (!s->pctx && sg.S > 0) return false;
+    if (!layer_ctx_maps(s->kv, l, H, D, mp)) return false;
+    const int ns = sg.S > 0 ? batch_ctx_splits(sg.S, H, R, m->ctx->num_sms) : 0;
+    if (ns > 0) {
+        BatchCtxAttn a{};
+        a.B = R;
+        a.H = H;
+        a.D = D;
+        a.S = sg.S;
+        a.nsplit = ns;
+        a.KS = 1;
+        a.n_qkv = h;  // q rows of s->q: row stride h, head hd at column hd * D
+        a.qkv = s->q;
+        a.part = s->pctx;
+        a.state = s->state;
+        launch_batch_ctx_attn(mp, a, st);
+    }
+    BatchUserMerge u{};
+    u.B = R;
+    u.H = H;
+    u.D = D;
+    u.L = 1;
+    u.layer = 0;
+    u.cap = s->cap;
+    u.KS = 1;
+    u.n_qkv = h;
+    u.nsplit = ns;
+    u.qkv = s->q;
+    u.qfin = s->q;
+    u.part = s->pctx;
+    u.uk = s->uk + (size_t)l * s->ukv_layer();
+    u.uv = s->uv + (size_t)l * s->ukv_layer();
+    u.state = s->state;
+    u.xhl = s->pxhl;
+    u.prefill = 1;
+    u.row0 = row0;
+    launch_batch_user_merge(u, st);
+    return true;
 }
 
 // One forward chunk of R <= 8 rows through every layer (merged_forward,
@@ -330,6 +407,9 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
     float* X = scratch;               // layer outputs [n][h]
     float* Y = scratch + (size_t)n * h;  // attention outputs [n][h]
     const int step = s->tc_prefill ? s->pchunk : 8;
+    // context attention of the prefill rows on the tensor cores (K10 + K11) where the
+    // layer's format allows; EKV_PREFILL_K4=1 keeps the split-KV kernel (experiments)
+    const bool prefill_k10 = !getenv("EKV_PREFILL_K4");
     for (int l = 0; l < L; ++l) {
         if (lev) EKV_CUDA(cudaEventRecord(lev[l], st));
         for (int r0 = 0; r0 < n; r0 += step) {
@@ -362,6 +442,7 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             g.user_base = base0 + r0;
             if (!tc) launch_gemv(g, st);
             if (r0 == 0 && ready && ready[l]) EKV_CUDA(cudaStreamWaitEvent(st, ready[l], 0));
+            const bool k10 = tc && prefill_k10 && tc_attn_rows(s, l, R, base0 + r0 - s->user_len, st);
             AttnArgs a{};
             a.R = R;
             a.H = H;
@@ -382,7 +463,7 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             a.out = Y + (size_t)r0 * h;
             a.ws = s->ws;
             a.counters = s->counters;
-            launch_decode_attention(a, st);
+            if (!k10) launch_decode_attention(a, st);
             GemvArgs o{};
             o.N = h;
             o.K = h;
@@ -394,7 +475,7 @@ void forward_layer_major(ekv_session_s* s, const float* emb, int n, int base0, c
             if (l == L - 1) o.y_hist = s->pre_out + (size_t)(base0 + r0) * h;
             if (tc)
                 tc_out_rows(s, l, Y + (size_t)r0 * h, X + (size_t)r0 * h,
-                            (l == L - 1) ? s->pre_out : nullptr, R, base0 + r0 - s->user_len, pmap_x, st);
+                            (l == L - 1) ? s->pre_out : nullptr, R, base0 + r0 - s->user_len, pmap_x, st, k10);
             else
                 launch_gemv(o, st);
         }
@@ -448,6 +529,10 @@ void session_alloc(ekv_session_s* s) {
             part = std::max(part, std::max((size_t)batch_proj_splits(3 * h, h, R, G) * 3 * h,
                                            (size_t)batch_proj_splits(h, h, R, G) * h) * R);
         s->ppart = dalloc_on<float>(part, ast);
+        if (s->kv->S > 0 && m->cfg.head_dim == 64) {
+            const int H = m->cfg.num_heads, ns = batch_ctx_splits(s->kv->S, H, 2, G);
+            s->pctx = dalloc_on<float>((size_t)s->pchunk * H * ns * (64 + 4), ast);
+        }
         s->pmap_w = make_map_2d(m->weights, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)h,
                                 (uint64_t)m->cfg.num_layers * 4 * h, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
         // the operand map is re-encoded per chunk size R (rows >= R read as zeros)
@@ -816,26 +901,7 @@ void batch_alloc(ekv_batch_s* b) {
     b->map_x = make_map_3d_bf16(b->xhl, (uint64_t)h, (uint64_t)B, 2, 64, (uint32_t)batch_proj_bn(B),
                                 CU_TENSOR_MAP_SWIZZLE_128B);
     b->maps.resize(L);
-    for (int l = 0; l < L; ++l) {
-        const ekv_segment& sg = b->kv->seg[l];
-        BatchCtxMaps& mp = b->maps[l];
-        mp.fmt = sg.format;
-        if (sg.S == 0) continue;
-        const uint64_t rows = (uint64_t)H * sg.S;
-        if (sg.format == EKV_KV_BF16) {
-            mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
-                               CU_TENSOR_MAP_SWIZZLE_128B);
-            mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)D, rows, (uint32_t)D, 128,
-                               CU_TENSOR_MAP_SWIZZLE_128B);
-        } else {
-            mp.k = make_map_2d(sg.k, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
-                               CU_TENSOR_MAP_SWIZZLE_NONE);
-            mp.v = make_map_2d(sg.v, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, (uint64_t)D, rows, (uint32_t)D, 128,
-                               CU_TENSOR_MAP_SWIZZLE_NONE);
-            mp.ks = make_map_1d(sg.k_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
-            mp.vs = make_map_1d(sg.v_scales, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rows, 128);
-        }
-    }
+    for (int l = 0; l < L; ++l) layer_ctx_maps(b->kv, l, H, D, b->maps[l]);
 }
 
 void batch_check(ekv_batch_s* b, int n) {
@@ -1596,7 +1662,7 @@ int ekv_session_create(ekv_model_t m, ekv_kvctx_t c, int max_user_rows, ekv_sess
             for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                             (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
                             (void*)s->ws, (void*)s->counters, (void*)s->pxhl, (void*)s->ppart,
-                            (void*)s->mega_ll, (void*)s->mega_sync})
+                            (void*)s->pctx, (void*)s->mega_ll, (void*)s->mega_sync})
                 if (p) cudaFreeAsync(p, m->ctx->stream);
             cudaStreamSynchronize(m->ctx->stream);
             delete s;
@@ -1619,7 +1685,7 @@ int ekv_session_destroy(ekv_session_t s) {
         for (void* p : {(void*)s->uk, (void*)s->uv, (void*)s->xa, (void*)s->xb, (void*)s->q,
                         (void*)s->emb, (void*)s->pre_out, (void*)s->hist, (void*)s->state,
                         (void*)s->ws, (void*)s->counters, (void*)s->mega_ll, (void*)s->mega_sync,
-                        (void*)s->pxhl, (void*)s->ppart})
+                        (void*)s->pxhl, (void*)s->ppart, (void*)s->pctx})
             if (p) cudaFreeAsync(p, fst);
         ekv_kvctx_s* kv = s->kv;
         ekv_model_s* m = s->model;

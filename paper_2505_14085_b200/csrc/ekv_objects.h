@@ -149,6 +149,7 @@ struct ekv_session_s {
     bool tc_prefill = false;
     uint16_t* pxhl = nullptr;      // [2][8][h] bf16 hi / lo operand
     float* ppart = nullptr;        // [max(KSq*3h, KSo*h)][8] split-K partials
+    float* pctx = nullptr;         // [pchunk][H][splits][d+4] context partials of the prefill rows (K10)
     int pKSq = 1, pKSo = 1;
     int pchunk = 8;                // rows per tensor-core chunk of the layer-major forward
     CUtensorMap pmap_w{}, pmap_x{};

@@ -794,12 +794,13 @@ __global__ void __launch_bounds__(128, NV == 1 ? 4 : 3) batch_user_merge_kernel(
     const int b = item / a.H, hd = item - b * a.H;
     const int grp = lane / G, c = lane - grp * G;  // row group, 8-dim chunk
     const int h = a.H * D;
-    const size_t head_off = (((size_t)b * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
+    const int owner = a.prefill ? 0 : b;  // the session whose user cache this row uses
+    const size_t head_off = (((size_t)owner * a.L + a.layer) * a.H + hd) * (size_t)a.cap * D;
     uint16_t* uk = a.uk + head_off;
     uint16_t* uv = a.uv + head_off;
     // ---- every independent load issued before the first use: the user-row count,
     //      this step's q/k/v partials, the first 32 user rows, the context partials ----
-    const int ulen = a.state->user_len;
+    const int ulen = a.state->user_len + (a.prefill ? a.row0 + b : 0);  // this row's cache row
     const size_t stride = (size_t)a.B * a.n_qkv;
     const float* p0 = a.qkv + (size_t)b * a.n_qkv + hd * D + c * 8;
     float4 v[NV][3][2];

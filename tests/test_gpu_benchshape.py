@@ -104,6 +104,15 @@ def test_k8_decode_at_c2_matches_oracle(ek, ctx, oracle, c2):
     finally:
         del os.environ["EKV_MEGA_CLUSTER"]
     assert np.array_equal(steps_n, steps) and np.array_equal(pre_n, pre)
+    # the prefill rows' context attention on the tensor cores (K10 + K11, the default)
+    # against the split-KV kernel K4
+    sess.reset()
+    os.environ["EKV_PREFILL_K4"] = "1"
+    try:
+        pre_k4, _ = ek.collaborative_decode(sess, ue, 1)
+    finally:
+        del os.environ["EKV_PREFILL_K4"]
+    assert max(normwise(pre[r], pre_k4[r].astype(np.float64)) for r in range(U)) <= 1e-4
     # the per-layer-kernel graph path agrees with the persistent kernel at this shape
     sess.reset()
     assert sess.set_decode_path("graph") == "graph"
