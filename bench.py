@@ -621,7 +621,25 @@ def run_b200(args, rank: int, world: int, local_rank: int):
             ncu_bytes = {k: v["dram_bytes_per_launch"] for k, v in json.load(f).items()}
     except (OSError, ValueError, KeyError):
         pass
-    if path == "mega":
+    if path == "mega" and launches == K:
+        # every launch of the timed region is one decode-step kernel: its average duration
+        # is the events' interval over the launches (inter-launch gaps included, so an
+        # upper bound); single launches timed alone add the launch latency each time
+        per_launch = ms / K  # ms
+        single = float(np.mean([p[0] for p in prof]))
+        achieved = step_bytes / (per_launch * 1e-3) / 1e9
+        roofline = {
+            "bound": "hbm", "kernel": "decode_step_kernel (persistent, 1 launch per token)",
+            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": ncu_bytes.get("decode_step_kernel"), "peak_kind": peak_kind,
+            "bytes_per_launch": step_bytes,
+            "avg_launch_us": per_launch * 1e3, "share_of_step": 1.0,
+            "single_launch_us": single * 1e3,
+            "how": f"CUDA events around the timed region on the launching stream / its {K} launches "
+                   f"(all decode_step_kernel); single_launch_us = {prof_steps} launches timed one at a "
+                   "time; bytes = weights + context KV + attended user rows of one token",
+        }
+    elif path == "mega":
         per_launch = float(np.mean([p[0] for p in prof]))  # ms, one kernel = one step
         achieved = step_bytes / (per_launch * 1e-3) / 1e9
         roofline = {
