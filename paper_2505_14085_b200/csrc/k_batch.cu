@@ -312,12 +312,71 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 
 __device__ __forceinline__ uint32_t pack2(uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); }
 
-// 4 signed int8 codes -> 2 words of 2 bf16 each (exact: |code| <= 127)
+// 4 signed int8 codes -> 2 words of 2 bf16 each (exact: |code| <= 128 fits bf16's 8-bit
+// significand).  No integer->float conversion (quarter rate): each biased byte is
+// placed in the significand of 2^23 (0x4B0000xx = 2^23 + byte) and the bias removed
+// with one packed FADD2 per pair; one PRMT keeps the two high halves.
 __device__ __forceinline__ void i8x4_to_bf16x4(uint32_t w, uint32_t& lo, uint32_t& hi) {
-    const float f0 = (float)(int8_t)(w & 0xFF), f1 = (float)(int8_t)((w >> 8) & 0xFF);
-    const float f2 = (float)(int8_t)((w >> 16) & 0xFF), f3 = (float)(int8_t)(w >> 24);
-    lo = (__float_as_uint(f0) >> 16) | (__float_as_uint(f1) & 0xFFFF0000u);
-    hi = (__float_as_uint(f2) >> 16) | (__float_as_uint(f3) & 0xFFFF0000u);
+    const uint32_t u = w ^ 0x80808080u;  // code + 128, as unsigned bytes
+    const f2x bias = f2pack(-8388736.0f, -8388736.0f);  // -(2^23 + 128)
+    const f2x a = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7440)),
+                               __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7441))), bias);
+    const f2x b = fadd2(f2pack(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7442)),
+                               __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7443))), bias);
+    lo = __byte_perm(__float_as_uint(f2lo(a)), __float_as_uint(f2hi(a)), 0x7632);
+    hi = __byte_perm(__float_as_uint(f2lo(b)), __float_as_uint(f2hi(b)), 0x7632);
+}
+
+// This row's k / v of head hd for split `split`'s share of the session tile:
+// split-K sum, bf16 rounding, append to the user caches (K11 then reads them
+// back).  Run by the 64 threads of warps 2-3 (idle on bf16 contexts, free after
+// the expansion on int8) while the softmax warps work; every load of a round
+// (4 units x up to 4 partials per thread) is issued before the first add.
+template <int D>
+__device__ __forceinline__ void append_kv(const BatchCtxAttn& a, int hd, int split, int bt, int t) {
+    constexpr int NTH = 64, UPT = 4, SPL = 4;
+    const int h = a.n_qkv / 3;
+    const size_t stride = (size_t)a.B * a.n_qkv;
+    const int ulen = a.state->user_len;
+    const int rA = split * BT / a.nsplit, rB = (split + 1) * BT / a.nsplit;
+    const int nun = (rB - rA) * 2 * (D / 4);
+    for (int u0 = t; u0 < nun; u0 += NTH * UPT) {
+        float4 v[UPT][SPL];
+        const float* src[UPT];
+        int bbs[UPT], kvs[UPT], c4s[UPT];
+#pragma unroll
+        for (int k = 0; k < UPT; ++k) {
+            const int u = u0 + k * NTH;
+            const int row = rA + u / (2 * (D / 4));
+            const int rem = u - (row - rA) * 2 * (D / 4);
+            kvs[k] = rem / (D / 4);
+            c4s[k] = rem - kvs[k] * (D / 4);
+            bbs[k] = (u < nun && bt * BT + row < a.B) ? bt * BT + row : -1;
+            src[k] = a.qkv + (size_t)max(bbs[k], 0) * a.n_qkv + (1 + kvs[k]) * h + hd * D + c4s[k] * 4;
+#pragma unroll
+            for (int s2 = 0; s2 < SPL; ++s2)
+                v[k][s2] = (bbs[k] >= 0 && s2 < a.KS) ? *reinterpret_cast<const float4*>(src[k] + s2 * stride)
+                                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < UPT; ++k) {
+            if (bbs[k] < 0) continue;
+            float4 x = v[k][0];
+#pragma unroll
+            for (int s2 = 1; s2 < SPL; ++s2) {
+                x.x += v[k][s2].x; x.y += v[k][s2].y; x.z += v[k][s2].z; x.w += v[k][s2].w;
+            }
+            for (int s2 = SPL; s2 < a.KS; ++s2) {  // rare: more than 4 splits
+                const float4 y = *reinterpret_cast<const float4*>(src[k] + s2 * stride);
+                x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
+            }
+            uint16_t* dst = (kvs[k] == 0 ? a.uk : a.uv) +
+                            ((((size_t)bbs[k] * a.L + a.layer) * a.H + hd) * a.cap + ulen) * D + c4s[k] * 4;
+            *reinterpret_cast<uint2*>(dst) =
+                make_uint2(f32_to_bf16_bits(x.x) | ((uint32_t)f32_to_bf16_bits(x.y) << 16),
+                           f32_to_bf16_bits(x.z) | ((uint32_t)f32_to_bf16_bits(x.w) << 16));
+        }
+    }
 }
 
 template <int D, int FMT>
@@ -469,6 +528,12 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else if (warp < 4) {
+        if constexpr (!Q8) {
+            if (a.qfin) {
+                pdl_wait();  // the QKV partials come from the previous kernel
+                append_kv<D>(a, hd, split, bt, threadIdx.x - 64);
+            }
+        }
         if constexpr (Q8) {
             // expand int8 codes to bf16 K-major / MN-major SW128 tiles (identical physical layout)
             const int t = threadIdx.x - 64;  // 0..63
@@ -509,6 +574,10 @@ __global__ void __launch_bounds__(THREADS, 1)
                     stage = 0;
                     phase ^= 1;
                 }
+            }
+            if (a.qfin) {  // after the last expansion: overlaps the last chunks' softmax
+                pdl_wait();
+                append_kv<D>(a, hd, split, bt, threadIdx.x - 64);
             }
         }
     } else {
@@ -574,33 +643,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             fence_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(qready);
-        }
-        // this row's k / v of head hd for this split's share of the session tile: split-K
-        // sum, bf16 rounding, append to the user caches (K11 then reads them back)
-        if (a.qfin) {
-            const int t = threadIdx.x - 128;
-            const int h = a.n_qkv / 3;
-            const size_t stride = (size_t)a.B * a.n_qkv;
-            const int ulen = a.state->user_len;
-            const int rA = split * BT / a.nsplit, rB = (split + 1) * BT / a.nsplit;
-            for (int u = t; u < (rB - rA) * 2 * (D / 4); u += 256) {
-                const int row = rA + u / (2 * (D / 4));
-                const int rem = u - (row - rA) * 2 * (D / 4);
-                const int kv = rem / (D / 4), c4 = rem - kv * (D / 4);
-                const int bb = bt * BT + row;
-                if (bb >= a.B) continue;
-                const float* src = a.qkv + (size_t)bb * a.n_qkv + (1 + kv) * h + hd * D + c4 * 4;
-                float4 x = *reinterpret_cast<const float4*>(src);
-                for (int s2 = 1; s2 < a.KS; ++s2) {
-                    const float4 y = *reinterpret_cast<const float4*>(src + s2 * stride);
-                    x.x += y.x; x.y += y.y; x.z += y.z; x.w += y.w;
-                }
-                uint16_t* dst = (kv == 0 ? a.uk : a.uv) +
-                                ((((size_t)bb * a.L + a.layer) * a.H + hd) * a.cap + ulen) * D + c4 * 4;
-                *reinterpret_cast<uint2*>(dst) =
-                    make_uint2(f32_to_bf16_bits(x.x) | ((uint32_t)f32_to_bf16_bits(x.y) << 16),
-                               f32_to_bf16_bits(x.z) | ((uint32_t)f32_to_bf16_bits(x.w) << 16));
-            }
         }
         constexpr float L2E = 1.4426950408889634f;
         float m = -INFINITY, l = 0.0f;
