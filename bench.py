@@ -867,7 +867,7 @@ def run_b200(args, rank: int, world: int, local_rank: int):
                 js, jc, jsc = arr(sp), arr(cp), arr(scp)
                 ctx.synchronize()
                 times = []
-                for it in range(4):
+                for it in range(9):  # median of 8 (one launch is ~50-100 us: single samples are noisy)
                     torch.cuda.synchronize()
                     with torch.cuda.stream(st):
                         torch.cuda._sleep(200_000)
