@@ -171,15 +171,21 @@ def link_deep_layers(link, context, session, layers) -> dict:
     rank, world = dist.get_rank(), dist.get_world_size()
     secs = []
     for dst in range(1, world):
-        if rank == 0:
-            secs.append(link.send_layers(context, layers, dst))
-        elif rank == dst:
-            secs.append(link.recv_forward(session, layers, 0)[1])
-        dist.barrier()
+        for rep in range(2):  # the first transfer of a pair also sets up NCCL's P2P connection
+            if rank == 0:
+                t = link.send_layers(context, layers, dst)
+            elif rank == dst:
+                t = link.recv_forward(session, layers, 0)[1]
+            else:
+                t = None
+            if rep == 1 and t is not None:
+                secs.append(t)
+            dist.barrier()
     sec = max_over_ranks(max(secs) if secs else 0.0, device="cuda")
     nbytes = int(sum(t.numel() for bufs in context_layer_views(context, layers) for t in bufs))
     return {"ms_per_destination": 1e3 * sec, "bytes": nbytes, "gbs": nbytes / max(sec, 1e-12) / 1e9,
             "destinations": world - 1, "layers": len(layers),
             "how": "C-ABI link (ekv_link_send_layers / ekv_link_recv_forward): ncclSend/ncclRecv of "
                    "each deep layer's codes + scales, one NCCL group per layer, from rank 0 (cloud "
-                   "role) to each edge rank in turn; once per prompt, outside the decode timing"}
+                   "role) to each edge rank in turn (second transfer of each pair: the first sets up "
+                   "the P2P connection); once per prompt, outside the decode timing"}
