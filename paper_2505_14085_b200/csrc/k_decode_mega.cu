@@ -1451,22 +1451,25 @@ static void launch_dkt(const MegaArgs& a, int grid, int cs, cudaStream_t st) {
     cfg.blockDim = dim3(mk::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    // co-residency of every CTA (the dataflow spins on its peers): a cooperative launch,
-    // or for head clusters the occupancy check of mega_cluster (grid <= the clusters the
-    // device keeps resident at once; the cooperative attribute combined with a cluster
-    // dimension is rejected under the profiler's kernel replay)
-    cudaLaunchAttribute at[1];
-    if (CL) {
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cs;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-    } else {
-        at[0].id = cudaLaunchAttributeCooperative;
-        at[0].val.cooperative = 1;
-    }
+    // Co-residency of every CTA (the dataflow spins on its peers): a cooperative launch
+    // (with the head clusters' dimension when CL).  Nsight Compute's kernel replay fails
+    // cooperative + cluster launches, so under the profiler (its injection environment)
+    // the cluster launch goes alone: mega_cluster checked its grid against the clusters
+    // the device keeps resident at once, and the profiler serialises kernels.
+    static const bool profiled = getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = CL ? cs : 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CL ? 2 : 1;
+    if (CL && profiled) {
+        cfg.attrs = at + 1;
+        cfg.numAttrs = 1;
+    }
     EKV_CUDA(cudaLaunchKernelEx(&cfg, fn, a));
 }
 

@@ -391,3 +391,30 @@ def test_pipelined_prefill_eq20(ek, ctx, oracle, overlap):
     wp, _ = oracle.collaborative_decode(f64, ck, cv, ue.cpu().numpy().astype(np.float64), 1,
                                         user_kv_bf16=True)
     assert max(normwise(want[r], wp[r]) for r in range(U)) <= TOL
+
+
+@pytest.mark.timeout(300)
+def test_persistent_kernels_on_two_streams(ek):
+    """Two contexts (two CUDA streams) on one GPU decoding at the same time: every K8
+    launch needs all of its CTAs resident (the dataflow spins on its peers), so two
+    launches in flight must not interleave their CTAs (cooperative launch, head clusters
+    at C2's 4 CTAs per head).  Same inputs on both streams -> same bits as run alone."""
+    L, H, d, S, U, T = 2, 32, 64, 1024, 4, 24
+    runs = []
+    for _ in range(2):
+        c = ek.Context(0)
+        m = ek.EdgeModel(c, L, H, d, S + 64)
+        m.synthesize(5)
+        kv = ek.AssembledContext(m, S, [16, 8], group=d)
+        kv.synthesize(6)
+        s = ek.Session(m, kv, U + T)
+        s.forward(torch.full((U, H * d), 0.25, device="cuda"))
+        runs.append((c, m, kv, s))
+    alone = runs[0][3].decode(T).cpu().numpy()
+    runs[0][3].reset()
+    runs[0][3].forward(torch.full((U, H * d), 0.25, device="cuda"))
+    outs = [r[3].decode(T, sync=False) for r in runs]  # both streams in flight
+    for r in runs:
+        r[0].synchronize()
+    assert np.array_equal(outs[0].cpu().numpy(), alone)
+    assert np.array_equal(outs[1].cpu().numpy(), alone)
