@@ -1520,7 +1520,7 @@ int mega_grid(const MegaArgs& a, int num_sms) {
     if (H <= num_sms && want >= H && want < g) g = want;
     if (const char* e = getenv("EKV_MEGA_GRID")) {  // experiments
         const int v = atoi(e);
-        if (v >= 1 && v < g) g = v;
+        if (v >= 1 && v <= num_sms) g = v;
     }
     return g;
 }
