@@ -209,3 +209,27 @@ def test_build_deep_kv_full_mask_and_errors(ek, ctx, oracle):
         ek.build_deep_kv(ctx, kvc, {1: 5}, X, W, K8, K8, 0.0, [5])
     with pytest.raises(ek.EkvError, match="not a quantised"):
         ek.build_deep_kv(ctx, kvc, {0: 5}, X, W, K, V, 0.0, [5])
+
+
+def test_long_prefill_tensor_core_attention(ek, ctx, oracle):
+    """A 200-row user prefill over a bf16 + int8 context: one layer-major chunk whose
+    context attention runs on K10 with two 128-row session tiles, then K11's causal
+    user segment; vs the split-KV kernel K4 (EKV_PREFILL_K4=1) and the oracle."""
+    import os
+    from test_gpu_decode import make_context
+    L, H, d, S, U = 2, 4, 64, 384, 200
+    h = H * d
+    bits, f64 = host_bf16_model(oracle, L, H, d, S + U + 8, seed=61)
+    model = upload_model(ek, ctx, bits, L, H, d, S + U + 8)
+    kvc, ck, cv = make_context(ek, ctx, oracle, model, S, [16, 8], seed=63)
+    ue = oracle.generate_embeddings(65, U, h).astype(np.float32)
+    out = ek.Session(model, kvc, U + 4).forward(dev32(ue)).cpu().numpy()
+    os.environ["EKV_PREFILL_K4"] = "1"
+    try:
+        out4 = ek.Session(model, kvc, U + 4).forward(dev32(ue)).cpu().numpy()
+    finally:
+        del os.environ["EKV_PREFILL_K4"]
+    assert max(normwise(out[r], out4[r].astype(np.float64)) for r in range(U)) <= 1e-4
+    want, _ = oracle.collaborative_decode(f64, ck, cv, ue.astype(np.float64), 1, user_kv_bf16=True)
+    for r in (0, 1, 127, 128, 129, U - 1):
+        assert normwise(out[r], want[r]) <= TOL, r
